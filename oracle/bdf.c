@@ -1,0 +1,661 @@
+/*
+ * bdf.c -- oracle variable-order, variable-step BDF for ONE cell
+ * (TEST INFRASTRUCTURE ONLY; see oracle.h).
+ *
+ * This is SURVEY.md §8(c).2 ("listing") written out in its own order: the
+ * CVODE fixed-leading-coefficient Nordsieck BDF (orders 1..5) that the paper
+ * uses with modified Newton and a
+ * dense direct LU solver with pivoting or CVDiag.  Constants
+ * are listing §8c.1 (paper-given: c_eps = 0.1, c_r = 0.3; all others
+ * are CVODE defaults, paper silent).  Readings R1..R24 in DESIGN.md.
+ *
+ * Notation follows the listing: zn[j] = h^j y^(j)/j!, q order, L = q+1,
+ * tau[1..6] past step sizes (most recent first), l[0..5], tq[1..5],
+ * gamma = h/l[1], gammap = gamma at the last matrix setup, crate = R (Eq. 4).
+ */
+#include <float.h>
+#include <math.h>
+#include <string.h>
+#include "oracle.h"
+
+/* listing §8c.1 */
+#define NLSCOEF 0.1     /* c_eps */
+#define CRDOWN 0.3      /* c_r, */
+#define MAXCOR 3
+#define RDIV 2.0
+#define MSBP 20
+#define DGMAX 0.3
+#define MSBJ 51
+#define DGMAX_JBAD 0.2
+#define BIAS1 6.0
+#define BIAS2 6.0
+#define BIAS3 10.0
+#define ADDON 1e-6
+#define THRESH 1.5
+#define ETAMX1 1e4
+#define ETAMX2 10.0
+#define ETAMIN 0.1
+#define ETAMXF 0.2
+#define SMALL_NEF 2
+#define MXNEF1 3
+#define MXNEF 7
+#define ETACF 0.25
+#define MXNCF 10
+#define LONG_WAIT 10
+#define HUB_FACTOR 0.1
+#define H_BIAS 0.5
+#define HIN_ITERS 4
+#define FRACT 0.1       /* CVDiag perturbation fraction */
+#define UROUND DBL_EPSILON
+
+enum { FIRST_CALL, PREV_CONV_FAIL, PREV_ERR_FAIL };
+enum { CF_NONE, CF_BAD_J, CF_OTHER };
+enum { NLS_OK = 0, NLS_RECOVERABLE = 1, NLS_RHS_UNREC = 2 };
+
+typedef struct {
+  const orc_problem *p;
+  const orc_opts *o;
+  int n, qmax;
+  double zn[ORC_QMAX + 1][ORC_NMAX];
+  double ewt[ORC_NMAX], acor[ORC_NMAX], y[ORC_NMAX], ftemp[ORC_NMAX], tmp[ORC_NMAX];
+  double J[ORC_NMAX * ORC_NMAX], M[ORC_NMAX * ORC_NMAX];
+  int piv[ORC_NMAX];
+  double Minv[ORC_NMAX];           /* CVDiag */
+  double gammasv;                  /* CVDiag */
+  double tn, h, hscale, hprime, eta, etamax;
+  double tau[ORC_QMAX + 2], l[ORC_QMAX + 1], tq[6];
+  double rl1, gamma, gammap, gamrat, crate, acnrm, saved_tq5;
+  int q, qprime, L, qwait;
+  long nstlp, nstlj;
+  orc_stats st;
+} cell;
+
+static double wrms(cell *c, const double *v) { return orc_wrms(c->n, v, c->ewt, c->o->group); }
+
+/* Eq. 3 weights: w_i = 1/(rtol |y_i| + atol_i) */
+static void set_ewt(cell *c, const double *y)
+{
+  for (int i = 0; i < c->n; ++i) c->ewt[i] = 1.0 / (c->o->rtol * fabs(y[i]) + c->o->atol[i]);
+}
+
+static int f_eval(cell *c, double t, const double *y, double *f)
+{
+  c->st.nfe++;
+  return orc_rhs(c->p, t, y, f);
+}
+
+/* RESCALE: zn[j] *= eta^j; h = hscale*eta; hscale = h (cvRescale) */
+static void rescale(cell *c)
+{
+  double r = c->eta;
+  for (int j = 1; j <= c->q; ++j) {
+    for (int i = 0; i < c->n; ++i) c->zn[j][i] = r * c->zn[j][i];
+    r = r * c->eta;
+  }
+  c->h = c->hscale * c->eta;
+  c->hscale = c->h;
+}
+
+/* PREDICT: tn += h; Pascal-triangle update zn[j-1] += zn[j] (cvPredict) */
+static void predict(cell *c, double tf)
+{
+  c->tn = c->tn + c->h;
+  if ((c->tn - tf) * c->h > 0.0) c->tn = tf;          /* never pass tf (R11) */
+  for (int k = 1; k <= c->q; ++k)
+    for (int j = c->q; j >= k; --j)
+      for (int i = 0; i < c->n; ++i) c->zn[j - 1][i] = c->zn[j - 1][i] + c->zn[j][i];
+}
+
+/* RESTORE: undo PREDICT (cvRestore) */
+static void restore(cell *c, double saved_t)
+{
+  c->tn = saved_t;
+  for (int k = 1; k <= c->q; ++k)
+    for (int j = c->q; j >= k; --j)
+      for (int i = 0; i < c->n; ++i) c->zn[j - 1][i] = c->zn[j - 1][i] - c->zn[j][i];
+}
+
+/* SET_BDF: cvSetBDF + cvSetTqBDF (listing) */
+void orc_set_bdf(int q, double h, const double *tau, int qwait, double *l, double *tq)
+{
+  double xi_inv = 1.0, xistar_inv = 1.0, alpha0 = -1.0, alpha0_hat = -1.0, hsum = h;
+  l[0] = l[1] = 1.0;
+  for (int i = 2; i <= ORC_QMAX; ++i) l[i] = 0.0;
+  if (q > 1) {
+    for (int j = 2; j < q; ++j) {
+      hsum = hsum + tau[j - 1];
+      xi_inv = h / hsum;
+      alpha0 = alpha0 - 1.0 / j;
+      for (int i = j; i >= 1; --i) l[i] = l[i] + l[i - 1] * xi_inv;
+    }
+    alpha0 = alpha0 - 1.0 / q;
+    xistar_inv = -l[1] - alpha0;
+    hsum = hsum + tau[q - 1];
+    xi_inv = h / hsum;
+    alpha0_hat = -l[1] - xi_inv;
+    for (int i = q; i >= 1; --i) l[i] = l[i] + l[i - 1] * xistar_inv;
+  }
+  /* cvSetTqBDF */
+  double A1 = 1.0 - alpha0_hat + alpha0;
+  double A2 = 1.0 + q * A1;
+  tq[2] = fabs(A1 / (alpha0 * A2));
+  tq[5] = fabs(A2 * xistar_inv / (l[q] * xi_inv));
+  if (qwait == 1) {
+    if (q > 1) {
+      double C = xistar_inv / l[q];
+      double A3 = alpha0 + 1.0 / q;
+      double A4 = alpha0_hat + xi_inv;
+      double Cpinv = (1.0 - A4 + A3) / A3;
+      tq[1] = fabs(C * Cpinv);
+    } else {
+      tq[1] = 1.0;
+    }
+    hsum = hsum + tau[q];
+    xi_inv = h / hsum;
+    double A5 = alpha0 - 1.0 / (q + 1);
+    double A6 = alpha0_hat - xi_inv;
+    double Cppinv = (1.0 - A6 + A5) / A2;
+    tq[3] = fabs(Cppinv / (xi_inv * (q + 2) * A5));
+  }
+  tq[4] = NLSCOEF / tq[2];            /* tol = c_eps * eps, eps = 1/tq[2] (R2) */
+}
+
+/* ADJUST_ORDER(+1): cvIncreaseBDF (hscale = old h, before RESCALE) */
+static void increase_bdf(cell *c)
+{
+  double l[ORC_QMAX + 1];
+  for (int i = 0; i <= ORC_QMAX; ++i) l[i] = 0.0;
+  double alpha1 = 1.0, prod = 1.0, xiold = 1.0, alpha0 = -1.0, hsum = c->hscale;
+  l[2] = 1.0;
+  if (c->q > 1) {
+    for (int j = 1; j < c->q; ++j) {
+      hsum = hsum + c->tau[j + 1];
+      double xi = hsum / c->hscale;
+      prod = prod * xi;
+      alpha0 = alpha0 - 1.0 / (j + 1);
+      alpha1 = alpha1 + 1.0 / xi;
+      for (int i = j + 2; i >= 2; --i) l[i] = l[i] * xiold + l[i - 1];
+      xiold = xi;
+    }
+  }
+  double A1 = (-alpha0 - alpha1) / prod;
+  int Lq = c->q + 1;
+  for (int i = 0; i < c->n; ++i) c->zn[Lq][i] = A1 * c->zn[c->qmax][i];
+  for (int j = 2; j <= c->q; ++j)
+    for (int i = 0; i < c->n; ++i) c->zn[j][i] = l[j] * c->zn[Lq][i] + c->zn[j][i];
+}
+
+/* ADJUST_ORDER(-1): cvDecreaseBDF */
+static void decrease_bdf(cell *c)
+{
+  double l[ORC_QMAX + 1];
+  for (int i = 0; i <= ORC_QMAX; ++i) l[i] = 0.0;
+  l[2] = 1.0;
+  double hsum = 0.0;
+  for (int j = 1; j <= c->q - 2; ++j) {
+    hsum = hsum + c->tau[j];
+    double xi = hsum / c->hscale;
+    for (int i = j + 2; i >= 2; --i) l[i] = l[i] * xi + l[i - 1];
+  }
+  for (int j = 2; j < c->q; ++j)
+    for (int i = 0; i < c->n; ++i) c->zn[j][i] = -l[j] * c->zn[c->q][i] + c->zn[j][i];
+}
+
+static void adjust_order(cell *c, int dq)
+{
+  if (c->q == 2 && dq != 1) return;   /* cvAdjustOrder: nothing to do 2 -> 1 */
+  if (dq == 1) increase_bdf(c); else decrease_bdf(c);
+}
+
+/* residual G = (rl1 zn[1] + ycor) - gamma f(tn, zn[0] + ycor)  (cvNlsResidual) */
+static int residual(cell *c, const double *ycor, double *G)
+{
+  for (int i = 0; i < c->n; ++i) c->y[i] = c->zn[0][i] + ycor[i];
+  int r = f_eval(c, c->tn, c->y, c->ftemp);
+  if (r) return r;
+  for (int i = 0; i < c->n; ++i) {
+    double t = c->rl1 * c->zn[1][i] + ycor[i];
+    G[i] = -c->gamma * c->ftemp[i] + t;
+  }
+  return 0;
+}
+
+/* matrix setup (cvLsSetup dense / CVDiagSetup).  Returns 0, >0 recoverable,
+ * <0 unrecoverable.  *jcur set when J was (re)evaluated.                  */
+static int lsetup(cell *c, int convfail, int *jcur)
+{
+  int n = c->n;
+  int rv = 0;
+  if (c->o->ls == ORC_LS_DENSE) {
+    double dgamma = fabs(c->gamma / c->gammap - 1.0);
+    int jbad = (c->st.nst == 0) || (c->st.nst >= c->nstlj + MSBJ) ||
+               (convfail == CF_BAD_J && dgamma < DGMAX_JBAD) || (convfail == CF_OTHER);
+    if (jbad) {
+      c->st.nje++;
+      c->nstlj = c->st.nst;
+      *jcur = 1;
+      int jr = orc_jac(c->p, c->tn, c->y, c->J);
+      if (jr) rv = -1;
+    } else {
+      *jcur = 0;
+    }
+    if (rv == 0) {
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+          c->M[i * n + j] = (i == j ? 1.0 : 0.0) - c->gamma * c->J[i * n + j];
+      if (orc_lu_factor(n, c->M, c->piv)) rv = 1;   /* zero pivot: recoverable */
+    }
+  } else {
+    /* CVDiagSetup: diagonal difference-quotient J, M = I - gamma J */
+    double r = FRACT * c->rl1;
+    double yp[ORC_NMAX], fp[ORC_NMAX], ft[ORC_NMAX];
+    for (int i = 0; i < n; ++i) ft[i] = c->h * c->ftemp[i] - c->zn[1][i];
+    for (int i = 0; i < n; ++i) yp[i] = r * ft[i] + c->y[i];
+    int fr = f_eval(c, c->tn, yp, fp);
+    c->st.nje++;
+    *jcur = 1;
+    if (fr) {
+      rv = fr;
+    } else {
+      for (int i = 0; i < n; ++i) {
+        double Mi;
+        if (fabs(ft[i] * c->ewt[i]) >= UROUND)
+          Mi = (FRACT * ft[i] + (-c->h) * (fp[i] - c->ftemp[i])) / (FRACT * ft[i]);
+        else
+          Mi = 1.0;
+        if (Mi == 0.0) { rv = 1; break; }
+        c->Minv[i] = 1.0 / Mi;
+      }
+      c->gammasv = c->gamma;
+    }
+  }
+  /* cvNlsLSetup bookkeeping */
+  c->st.nsetups++;
+  c->gamrat = 1.0;
+  c->gammap = c->gamma;
+  c->crate = 1.0;
+  c->nstlp = c->st.nst;
+  return rv;
+}
+
+/* linear solve b <- M^{-1} b  (cvLsSolve dense with 2/(1+gamrat) / CVDiagSolve) */
+static int lsolve(cell *c, double *b)
+{
+  int n = c->n;
+  if (c->o->ls == ORC_LS_DENSE) {
+    orc_lu_solve(n, c->M, c->piv, b);
+    if (c->gamrat != 1.0) {
+      double s = 2.0 / (1.0 + c->gamrat);
+      for (int i = 0; i < n; ++i) b[i] = s * b[i];
+    }
+    return 0;
+  }
+  if (c->gammasv != c->gamma) {
+    double r = c->gamma / c->gammasv;
+    for (int i = 0; i < n; ++i) {
+      double Mi = (1.0 / c->Minv[i] + (-1.0)) * r + 1.0;
+      if (Mi == 0.0) return 1;
+      c->Minv[i] = 1.0 / Mi;
+    }
+    c->gammasv = c->gamma;
+  }
+  for (int i = 0; i < n; ++i) b[i] = b[i] * c->Minv[i];
+  return 0;
+}
+
+/* NEWTON(nflag): cvNls + SUNNonlinSol_Newton + cvNlsConvTest (Eq. 4) */
+static int newton(cell *c, int nflag)
+{
+  int n = c->n;
+  int convfail = (nflag == FIRST_CALL || nflag == PREV_ERR_FAIL) ? CF_NONE : CF_OTHER;
+  int setup = (nflag == PREV_CONV_FAIL) || (nflag == PREV_ERR_FAIL) || (c->st.nst == 0) ||
+              (c->st.nst >= c->nstlp + MSBP) || (fabs(c->gamrat - 1.0) > DGMAX);
+  double ycor[ORC_NMAX], G[ORC_NMAX];
+  double tol = c->tq[4];
+  int jcur = 0;
+  for (int i = 0; i < n; ++i) ycor[i] = 0.0;
+  for (;;) {
+    int rv = residual(c, ycor, G);                               /* N4 */
+    if (rv < 0) return NLS_RHS_UNREC;
+    if (rv == 0 && setup) {
+      rv = lsetup(c, convfail, &jcur);
+      if (rv < 0) return NLS_RHS_UNREC;
+      setup = 0;
+    }
+    if (rv == 0) {
+      double dprev = 0.0;
+      int m = 0;
+      for (;;) {                                                  /* N6 */
+        c->st.nni++;
+        for (int i = 0; i < n; ++i) G[i] = -G[i];
+        rv = lsolve(c, G);
+        if (rv) break;
+        for (int i = 0; i < n; ++i) ycor[i] = ycor[i] + G[i];
+        double del = wrms(c, G);
+        if (m > 0) c->crate = fmax(CRDOWN * c->crate, del / dprev);     /* Eq. 4 rate */
+        double dcon = del * fmin(1.0, c->crate) / tol;
+        if (dcon <= 1.0) {                                                /* Eq. 4 test */
+          c->acnrm = (m == 0) ? del : wrms(c, ycor);
+          for (int i = 0; i < n; ++i) c->acor[i] = ycor[i];
+          return NLS_OK;
+        }
+        if (m >= 1 && del > RDIV * dprev) { rv = 1; break; }
+        dprev = del;
+        m++;
+        if (m >= MAXCOR) { rv = 1; break; }
+        rv = residual(c, ycor, G);
+        if (rv < 0) return NLS_RHS_UNREC;
+        if (rv) break;
+      }
+    }
+    /* FAIL: retry once with a fresh Jacobian if it was not current */
+    if (rv > 0 && !jcur) {
+      setup = 1;
+      convfail = CF_BAD_J;
+      for (int i = 0; i < n; ++i) ycor[i] = 0.0;
+      continue;
+    }
+    return NLS_RECOVERABLE;
+  }
+}
+
+/* SET_ETA (cvSetEta) */
+static void set_eta(cell *c)
+{
+  if (c->eta < THRESH) {
+    c->eta = 1.0;
+    c->hprime = c->h;
+  } else {
+    c->eta = fmin(c->eta, c->etamax);
+    if (c->o->hmax > 0.0) c->eta = c->eta / fmax(1.0, fabs(c->h) * c->eta / c->o->hmax);
+    c->hprime = c->h * c->eta;
+  }
+}
+
+/* PREPARE_NEXT (cvPrepareNextStep + cvChooseEta) */
+static void prepare_next(cell *c, double dsm)
+{
+  int n = c->n;
+  if (c->etamax == 1.0) {
+    c->qwait = c->qwait > 2 ? c->qwait : 2;
+    c->qprime = c->q;
+    c->hprime = c->h;
+    c->eta = 1.0;
+    return;
+  }
+  double etaq = 1.0 / (pow(BIAS2 * dsm, 1.0 / c->L) + ADDON);
+  if (c->qwait != 0) {
+    c->eta = etaq;
+    c->qprime = c->q;
+    set_eta(c);
+    return;
+  }
+  c->qwait = 2;
+  double etaqm1 = 0.0, etaqp1 = 0.0;
+  if (c->q > 1) {
+    double ddn = wrms(c, c->zn[c->q]) * c->tq[1];
+    etaqm1 = 1.0 / (pow(BIAS1 * ddn, 1.0 / c->q) + ADDON);
+  }
+  if (c->q != c->qmax && c->saved_tq5 != 0.0) {
+    double hr = c->h / c->tau[2];
+    double pw = 1.0;
+    for (int k = 0; k < c->L; ++k) pw = pw * hr;
+    double cquot = (c->tq[5] / c->saved_tq5) * pw;
+    for (int i = 0; i < n; ++i) c->tmp[i] = -cquot * c->zn[c->qmax][i] + c->acor[i];
+    double dup = wrms(c, c->tmp) * c->tq[3];
+    etaqp1 = 1.0 / (pow(BIAS3 * dup, 1.0 / (c->L + 1)) + ADDON);
+  }
+  double etam = fmax(etaqm1, fmax(etaq, etaqp1));
+  if (etam < THRESH) {
+    c->eta = 1.0;
+    c->qprime = c->q;
+  } else if (etam == etaq) {
+    c->eta = etaq;
+    c->qprime = c->q;
+  } else if (etam == etaqm1) {
+    c->eta = etaqm1;
+    c->qprime = c->q - 1;
+  } else {
+    c->eta = etaqp1;
+    c->qprime = c->q + 1;
+    for (int i = 0; i < n; ++i) c->zn[c->qmax][i] = c->acor[i];
+  }
+  set_eta(c);
+}
+
+/* cvHin: initial step estimate (reading R9) */
+static int hin(cell *c, double t0, double tf, double *h0)
+{
+  int n = c->n;
+  double tdist = tf - t0;
+  double tround = UROUND * fmax(fabs(t0), fabs(tf));
+  double hlb = 100.0 * tround;
+  /* cvUpperBoundH0 */
+  double hub_inv = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double d = HUB_FACTOR * fabs(c->zn[0][i]) + 1.0 / c->ewt[i];
+    double r = fabs(c->zn[1][i]) / d;
+    if (r > hub_inv) hub_inv = r;
+  }
+  double hub = HUB_FACTOR * tdist;
+  if (hub * hub_inv > 1.0) hub = 1.0 / hub_inv;
+  double hg = sqrt(hlb * hub);
+  if (hub < hlb) { *h0 = hg; return 0; }
+  double hs = hg, hnew = hg;
+  for (int count1 = 1; count1 <= HIN_ITERS; ++count1) {
+    int ok = 0;
+    double yddnrm = 0.0;
+    for (int count2 = 1; count2 <= HIN_ITERS; ++count2) {
+      /* cvYddNorm: ydd = (f(t0+hg, y0 + hg f0) - f0) * (1/hg) */
+      double yt[ORC_NMAX], ft[ORC_NMAX];
+      for (int i = 0; i < n; ++i) yt[i] = hg * c->zn[1][i] + c->zn[0][i];
+      int r = f_eval(c, t0 + hg, yt, ft);
+      if (r < 0) return -1;
+      if (r == 0) {
+        double ih = 1.0 / hg;
+        for (int i = 0; i < n; ++i) ft[i] = (ft[i] - c->zn[1][i]) * ih;
+        yddnrm = wrms(c, ft);
+        ok = 1;
+        break;
+      }
+      hg = hg * 0.2;
+    }
+    if (!ok) {
+      if (count1 <= 2) return -1;
+      hnew = hs;
+      break;
+    }
+    hs = hg;
+    hnew = (yddnrm * hub * hub > 2.0) ? sqrt(2.0 / yddnrm) : sqrt(hg * hub);
+    if (count1 == HIN_ITERS) break;
+    double hrat = hnew / hg;
+    if (hrat > 0.5 && hrat < 2.0) break;
+    if (count1 > 1 && hrat > 2.0) { hnew = hg; break; }
+    hg = hnew;
+  }
+  double h = H_BIAS * hnew;
+  if (h < hlb) h = hlb;
+  if (h > hub) h = hub;
+  *h0 = h;
+  return 0;
+}
+
+/* STEP: one accepted step of cvStep.  Returns ORC_OK or a failure status. */
+static int step(cell *c, double tf)
+{
+  int n = c->n;
+  double saved_t = c->tn;
+  int ncf = 0, nef = 0, nflag = FIRST_CALL;
+  if (c->st.nst > 0 && c->hprime != c->h) {
+    if (c->qprime != c->q) {
+      adjust_order(c, c->qprime - c->q);
+      c->q = c->qprime;
+      c->L = c->q + 1;
+      c->qwait = c->L;
+    }
+    rescale(c);
+  }
+  double dsm;
+  for (;;) {
+    predict(c, tf);
+    orc_set_bdf(c->q, c->h, c->tau, c->qwait, c->l, c->tq);
+    c->rl1 = 1.0 / c->l[1];
+    c->gamma = c->h * c->rl1;
+    if (c->st.nst == 0) c->gammap = c->gamma;
+    c->gamrat = (c->st.nst > 0) ? c->gamma / c->gammap : 1.0;
+
+    int r = newton(c, nflag);
+    if (r != NLS_OK) {
+      /* cvHandleNFlag: convergence failure */
+      c->st.ncfn++;
+      restore(c, saved_t);
+      if (r == NLS_RHS_UNREC) return ORC_RHS_FAIL;
+      ncf++;
+      c->etamax = 1.0;
+      if (fabs(c->h) <= c->o->hmin * (1.0 + UROUND) || ncf == MXNCF) return ORC_CONV_FAILURE;
+      c->eta = fmax(ETACF, c->o->hmin / fabs(c->h));
+      nflag = PREV_CONV_FAIL;
+      rescale(c);
+      continue;
+    }
+    /* local error test, ||LTE|| = acnrm * tq[2] <= 1 */
+    dsm = c->acnrm * c->tq[2];
+    if (dsm <= 1.0) break;
+    nef++;
+    c->st.netf++;
+    nflag = PREV_ERR_FAIL;
+    restore(c, saved_t);
+    if (fabs(c->h) <= c->o->hmin * (1.0 + UROUND) || nef == MXNEF) return ORC_ERR_FAILURE;
+    c->etamax = 1.0;
+    if (nef <= MXNEF1) {
+      c->eta = 1.0 / (pow(BIAS2 * dsm, 1.0 / c->L) + ADDON);
+      c->eta = fmax(ETAMIN, fmax(c->eta, c->o->hmin / fabs(c->h)));
+      if (nef >= SMALL_NEF) c->eta = fmin(c->eta, ETAMXF);
+      rescale(c);
+      continue;
+    }
+    if (c->q > 1) {
+      c->eta = fmax(ETAMIN, c->o->hmin / fabs(c->h));
+      adjust_order(c, -1);
+      c->L = c->q;
+      c->q = c->q - 1;
+      c->qwait = c->L;
+      rescale(c);
+      continue;
+    }
+    c->eta = fmax(ETAMIN, c->o->hmin / fabs(c->h));
+    c->h = c->h * c->eta;
+    c->hprime = c->h;
+    c->hscale = c->h;
+    c->qwait = LONG_WAIT;
+    int fr = f_eval(c, c->tn, c->zn[0], c->tmp);
+    if (fr < 0) return ORC_RHS_FAIL;
+    if (fr > 0) return ORC_RHS_FAIL;
+    for (int i = 0; i < n; ++i) c->zn[1][i] = c->h * c->tmp[i];
+  }
+
+  /* DONE: cvCompleteStep */
+  c->st.nst++;
+  for (int i = c->q; i >= 2; --i) c->tau[i] = c->tau[i - 1];
+  if (c->q == 1 && c->st.nst > 1) c->tau[2] = c->tau[1];
+  c->tau[1] = c->h;
+  for (int j = 0; j <= c->q; ++j)
+    for (int i = 0; i < n; ++i) c->zn[j][i] = c->l[j] * c->acor[i] + c->zn[j][i];
+  c->qwait--;
+  if (c->qwait == 1 && c->q != c->qmax) {
+    for (int i = 0; i < n; ++i) c->zn[c->qmax][i] = c->acor[i];
+    c->saved_tq5 = c->tq[5];
+  }
+  prepare_next(c, dsm);
+  c->etamax = ETAMX2;
+  return ORC_OK;
+}
+
+int orc_integrate(const orc_problem *p, const orc_opts *o, double t0, double tf,
+                  double *y, orc_stats *st, orc_trace *tr)
+{
+  cell C;
+  cell *c = &C;
+  memset(c, 0, sizeof(*c));
+  int n = p->n;
+  c->p = p; c->o = o; c->n = n;
+  c->qmax = o->qmax < 1 ? 1 : (o->qmax > ORC_QMAX ? ORC_QMAX : o->qmax);
+  c->st.status = ORC_OK;
+  c->st.t_reached = t0;
+
+  for (int i = 0; i < n; ++i)
+    if (!isfinite(y[i])) { c->st.status = ORC_NONFINITE_INPUT; goto out; }
+  if (p->fext)
+    for (int i = 0; i < n; ++i)
+      if (!isfinite(p->fext[i])) { c->st.status = ORC_NONFINITE_INPUT; goto out; }
+
+  /* INIT */
+  for (int i = 0; i < n; ++i) c->zn[0][i] = y[i];
+  set_ewt(c, y);
+  c->tn = t0;
+  if (f_eval(c, t0, y, c->zn[1])) { c->st.status = ORC_RHS_FAIL; goto out; }
+  double h0 = o->h0;
+  if (h0 == 0.0) {
+    if (hin(c, t0, tf, &h0)) { c->st.status = ORC_RHS_FAIL; goto out; }
+  }
+  if (h0 > tf - t0) h0 = tf - t0;
+  if (o->hmax > 0.0 && h0 > o->hmax) h0 = o->hmax;
+  for (int i = 0; i < n; ++i) c->zn[1][i] = h0 * c->zn[1][i];
+  c->h = c->hscale = c->hprime = h0;
+  c->q = c->qprime = 1;
+  c->L = 2;
+  c->qwait = 2;
+  c->etamax = ETAMX1;
+  c->crate = 1.0;
+  c->eta = 1.0;
+
+  /* LOOP */
+  for (;;) {
+    if (c->st.nst > 0) set_ewt(c, c->zn[0]);                        /* O1 */
+    if ((c->tn + c->hprime - tf) * c->h > 0.0) {                     /* O2 */
+      c->hprime = tf - c->tn;
+      c->eta = c->hprime / c->h;
+    }
+    if (c->st.nst >= o->mxstep) { c->st.status = ORC_TOO_MUCH_WORK; break; }   /* O3 */
+    int r = step(c, tf);                                             /* O4 */
+    if (r != ORC_OK) { c->st.status = r; break; }
+    if (tr && tr->count < tr->cap) {
+      int k = tr->count++;
+      tr->tn[k] = c->tn; tr->h[k] = c->h; tr->q[k] = c->q;
+      for (int j = 0; j <= ORC_QMAX; ++j)
+        for (int i = 0; i < n; ++i) tr->zn[(k * (ORC_QMAX + 1) + j) * n + i] = c->zn[j][i];
+    }
+    if (fabs(c->tn - tf) <= 100.0 * UROUND * (fabs(c->tn) + fabs(c->h))) {   /* O5 */
+      c->tn = tf;
+      break;
+    }
+  }
+  for (int i = 0; i < n; ++i) y[i] = c->zn[0][i];
+  c->st.t_reached = c->tn;
+out:
+  c->st.q_last = c->q;
+  c->st.h_last = c->h;
+  *st = c->st;
+  return c->st.status;
+}
+
+void orc_integrate_batch(const orc_problem *proto, const orc_opts *o, double t0, double tf,
+                         int64_t N, int64_t c0, int64_t c1, double *y, const double *fext,
+                         const double *rho, orc_stats *st)
+{
+  int n = proto->n;
+  for (int64_t c = c0; c < c1; ++c) {
+    orc_problem p = *proto;
+    double yc[ORC_NMAX], fc[ORC_NMAX];
+    for (int k = 0; k < n; ++k) yc[k] = y[k * N + c];
+    if (fext) {
+      for (int k = 0; k < n; ++k) fc[k] = fext[k * N + c];
+      p.fext = fc;
+    } else {
+      p.fext = NULL;
+    }
+    if (rho) p.rho = rho[c];
+    orc_integrate(&p, o, t0, tf, yc, &st[c - c0], NULL);
+    for (int k = 0; k < n; ++k) y[k * N + c] = yc[k];
+  }
+}

@@ -1,0 +1,161 @@
+/*
+ * oracle.h -- CPU oracle for the batched BDF hot path (arXiv 2405.01713).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing on the product path may include, link,
+ * load or execute anything under oracle/.  The only permitted users are
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` legs.  The oracle shares no code, header, table or
+ * constant generator with the CUDA path (paper_2405_01713_b200/csrc).
+ *
+ * Plain, slow, obviously-correct fp64 C99, one cell at a time.  Compiled with
+ * -O2 -ffp-contract=off so that a*b+c is never fused behind our back; fma()
+ * is called only where the listing (LU_FACTOR / LU_SOLVE)
+ * prescribes it.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+ * "listing" = SURVEY.md §8(c).2, the step-by-step reconstruction of CVODE's
+ * fixed-leading-coefficient Nordsieck BDF that the paper defers to
+ * (hindmarsh2005sundials).  Readings R1..R24 are SURVEY.md §8(c).3 and
+ * are restated in DESIGN.md.
+ *
+ * Parity pins: see tests/test_oracle_*.py.  Every function below is pinned by
+ * at least one test against something other than itself (closed forms,
+ * published values, brute force, invariants) -- except where the header of a
+ * function says "parity unpinned".
+ */
+#ifndef BDFB_ORACLE_H
+#define BDFB_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_QMAX 5          /* listing §8c.1: QMAX */
+#define ORC_NMAX 64         /* largest system the oracle handles (n <= 64) */
+
+/* ---- models -------------------------------------------- */
+enum {
+  ORC_MODEL_LINEAR = 0,     /* y' = lambda .* y + f_ext  (closed-form pins) */
+  ORC_MODEL_ROBERTSON = 1,  /* S:180, §8c.6 C1 */
+  ORC_MODEL_KWH = 2,        /* Nyx-style heating/cooling, §8c.6 C2, Appendix B */
+  ORC_MODEL_MECH = 3        /* constant-volume reactor, §8c.6 C3-C5 */
+};
+
+/* linear-solver choice inside Newton (P:399 dense direct, P:480 CVDiag) */
+enum { ORC_LS_DENSE = 0, ORC_LS_DIAG = 1 };
+
+/* Jacobian source for the dense solver */
+enum { ORC_JAC_ANALYTIC = 0 /* model's exact J: closed form or complex step */ };
+
+/* per-cell status */
+enum {
+  ORC_OK = 0,
+  ORC_TOO_MUCH_WORK = 1,
+  ORC_ERR_FAILURE = 2,
+  ORC_CONV_FAILURE = 3,
+  ORC_RHS_FAIL = 4,
+  ORC_NONFINITE_INPUT = 5
+};
+
+/* KWH96-form heating/cooling parameters (Appendix B; reading R21) */
+typedef struct {
+  double z;               /* redshift */
+  double X, Y;            /* H and He mass fractions */
+  double gamma_ad;        /* adiabatic index */
+  double gph[3];          /* photo-ionisation rates H0, He0, He+  [1/s] */
+  double eph[3];          /* photo-heating rates   H0, He0, He+  [erg/s] */
+} orc_kwh_params;
+
+/* Flattened reaction mechanism (constant-volume reactor, §8c.6).
+ * Units: CHEMKIN cgs (mol, cm^3, s), Ea in cal/mol, T in K.
+ * Species k = 0..K-1 hold mass fractions Y_k; state index K is T.        */
+typedef struct {
+  int K;                 /* number of species                          */
+  int nr;                /* number of reactions                        */
+  const double *W;       /* [K] molecular weights g/mol                */
+  const double *nasa;    /* [K][15]: Tmid, a_low[7], a_high[7]         */
+  const int *reac;       /* [I][3] reactant species, -1 = empty slot   */
+  const int *prod;       /* [I][3] product species,  -1 = empty slot   */
+  const int *rev;        /* [I] 1 = reversible via Kc                  */
+  const int *type;       /* [I] 0 elementary, 1 three-body, 2 Lindemann, 3 Troe */
+  const double *arr;     /* [I][3] A, beta, Ea (k_inf for falloff)     */
+  const double *arr0;    /* [I][3] A0, beta0, Ea0 (falloff low-p limit)*/
+  const double *troe;    /* [I][4] a, T3, T1, T2 (T2 used iff has_t2)  */
+  const int *has_t2;     /* [I]                                        */
+  const double *eff;     /* [I][K] third-body efficiencies             */
+} orc_mech;
+
+typedef struct {
+  int kind;              /* ORC_MODEL_* */
+  int n;                 /* system size */
+  const double *lambda;  /* LINEAR: [n] rates */
+  const double *rob_k;   /* ROBERTSON: k1,k2,k3 */
+  const orc_kwh_params *kwh;
+  const orc_mech *mech;
+  double rho;            /* per-cell aux: density g/cm^3 (KWH, MECH) */
+  const double *fext;    /* per-cell frozen forcing F, [n] or NULL */
+} orc_problem;
+
+typedef struct {
+  double rtol;
+  const double *atol;    /* [n] */
+  int qmax;              /* 1..5 */
+  int64_t mxstep;        /* R12: per outer step */
+  double h0;             /* 0 = cvHin */
+  double hmin, hmax;     /* hmax <= 0 means infinity */
+  int ls;                /* ORC_LS_DENSE | ORC_LS_DIAG */
+  int group;             /* G: WRMS summation order emulation (R15); 1 = sequential */
+} orc_opts;
+
+typedef struct {
+  int32_t status;
+  int32_t nst, nfe, nje, nsetups, nni, netf, ncfn;
+  int32_t q_last;
+  double h_last;
+  double t_reached;
+} orc_stats;
+
+/* optional trace of accepted steps, for the Nordsieck invariant pin */
+typedef struct {
+  int cap;               /* records available */
+  int count;             /* records written */
+  double *tn;            /* [cap] */
+  double *h;             /* [cap] */
+  int *q;                /* [cap] */
+  double *zn;            /* [cap][ORC_QMAX+1][n] */
+} orc_trace;
+
+/* ---- primitives -------------------------------------------------------- */
+double orc_wrms(int n, const double *v, const double *w, int group);
+int orc_lu_factor(int n, double *M /* row-major n*n, in/out */, int *piv);
+void orc_lu_solve(int n, const double *LU, const int *piv, double *b);
+
+/* f = R(t,y) + f_ext.  Returns 0, or >0 for a recoverable RHS failure. */
+int orc_rhs(const orc_problem *p, double t, const double *y, double *f);
+/* J = d f / d y (row-major).  Analytic (LINEAR, ROBERTSON) or complex-step
+ * (MECH).  Returns 0 or >0 on failure.  KWH has no J (CVDiag only).       */
+int orc_jac(const orc_problem *p, double t, const double *y, double *J);
+
+/* cvSetBDF + cvSetTqBDF for the coefficient pins: l[0..5], tq[1..5] */
+void orc_set_bdf(int q, double h, const double *tau /* [7], tau[1..6] */,
+                 int qwait, double *l, double *tq);
+
+/* Integrate one cell from t0 to tf in place (y: [n]).  Returns status.   */
+int orc_integrate(const orc_problem *p, const orc_opts *o, double t0,
+                  double tf, double *y, orc_stats *st, orc_trace *tr);
+
+/* Batch driver over cells [c0, c1) of a YC (component-major) field:
+ * y[k*N + c], fext[k*N + c] (or NULL), rho[c] (or NULL).  Stats written
+ * per cell into st[c - c0].  Model parameters come from *proto (its rho and
+ * fext fields are overwritten per cell).                                  */
+void orc_integrate_batch(const orc_problem *proto, const orc_opts *o,
+                         double t0, double tf, int64_t N, int64_t c0,
+                         int64_t c1, double *y, const double *fext,
+                         const double *rho, orc_stats *st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
