@@ -72,10 +72,46 @@ static void kwh_eval(const orc_kwh_params *q, double e, double nH, double yHe,
   P->nHepp = nHepp; P->ne = ne; P->g = xe - ne_new / nH;
 }
 
+static int kwh_solve(const orc_problem *p, double e, kwh_pop *out);
+
 static int kwh_rhs(const orc_problem *p, const double *y, double *f)
 {
+  kwh_pop Pp;
+  if (kwh_solve(p, y[0], &Pp)) return 1;
+  const kwh_pop *P = &Pp;
   const orc_kwh_params *q = p->kwh;
-  double e = y[0], rho = p->rho;
+  double rho = p->rho;
+  double T = P->T, sT = sqrt(T);
+  double T3 = T / 1e3, T5 = T / 1e5, T6 = T / 1e6;
+  double S5 = 1.0 / (1.0 + sqrt(T5));
+  double ne = P->ne;
+  double rec = pow(T3, -0.2) / (1.0 + pow(T6, 0.7));
+  double L = 0.0;
+  L += 7.50e-19 * exp(-118348.0 / T) * S5 * ne * P->nH0;
+  L += 5.54e-17 * pow(T, -0.397) * exp(-473638.0 / T) * S5 * ne * P->nHep;
+  L += 1.27e-21 * sT * exp(-157809.1 / T) * S5 * ne * P->nH0;
+  L += 9.38e-22 * sT * exp(-285335.4 / T) * S5 * ne * P->nHe0;
+  L += 4.95e-22 * sT * exp(-631515.0 / T) * S5 * ne * P->nHep;
+  L += 8.70e-27 * sT * rec * ne * P->nHp;
+  L += 1.55e-26 * pow(T, 0.3647) * ne * P->nHep;
+  L += 3.48e-26 * sT * rec * ne * P->nHepp;
+  L += 1.24e-13 * pow(T, -1.5) * exp(-470000.0 / T) * (1.0 + 0.3 * exp(-94000.0 / T)) * ne * P->nHep;
+  double lt = 5.5 - log10(T);
+  double gff = 1.1 + 0.34 * exp(-lt * lt / 3.0);
+  L += 1.42e-27 * gff * sT * (P->nHp + P->nHep + 4.0 * P->nHepp) * ne;
+  double zp1 = 1.0 + q->z;
+  L += 5.41e-36 * ne * T * (zp1 * zp1 * zp1 * zp1);
+  double H = P->nH0 * q->eph[0] + P->nHe0 * q->eph[1] + P->nHep * q->eph[2];
+  f[0] = (H - L) / rho;
+  if (p->fext) f[0] = f[0] + p->fext[0];
+  return 0;
+}
+
+/* ionisation-equilibrium solve for x_e (shared by the RHS and the pin entry) */
+static int kwh_solve(const orc_problem *p, double e, kwh_pop *out)
+{
+  const orc_kwh_params *q = p->kwh;
+  double rho = p->rho;
   double nH = q->X * rho / KWH_MP;
   double yHe = q->Y / (4.0 * q->X);
   double xmax = 1.0 + 2.0 * yHe;
@@ -117,31 +153,18 @@ static int kwh_rhs(const orc_problem *p, const double *y, double *f)
     }
     P = &Cc;
   }
-
-  double T = P->T, sT = sqrt(T);
-  double T3 = T / 1e3, T5 = T / 1e5, T6 = T / 1e6;
-  double S5 = 1.0 / (1.0 + sqrt(T5));
-  double ne = P->ne;
-  double rec = pow(T3, -0.2) / (1.0 + pow(T6, 0.7));
-  double L = 0.0;
-  L += 7.50e-19 * exp(-118348.0 / T) * S5 * ne * P->nH0;
-  L += 5.54e-17 * pow(T, -0.397) * exp(-473638.0 / T) * S5 * ne * P->nHep;
-  L += 1.27e-21 * sT * exp(-157809.1 / T) * S5 * ne * P->nH0;
-  L += 9.38e-22 * sT * exp(-285335.4 / T) * S5 * ne * P->nHe0;
-  L += 4.95e-22 * sT * exp(-631515.0 / T) * S5 * ne * P->nHep;
-  L += 8.70e-27 * sT * rec * ne * P->nHp;
-  L += 1.55e-26 * pow(T, 0.3647) * ne * P->nHep;
-  L += 3.48e-26 * sT * rec * ne * P->nHepp;
-  L += 1.24e-13 * pow(T, -1.5) * exp(-470000.0 / T) * (1.0 + 0.3 * exp(-94000.0 / T)) * ne * P->nHep;
-  double lt = 5.5 - log10(T);
-  double gff = 1.1 + 0.34 * exp(-lt * lt / 3.0);
-  L += 1.42e-27 * gff * sT * (P->nHp + P->nHep + 4.0 * P->nHepp) * ne;
-  double zp1 = 1.0 + q->z;
-  L += 5.41e-36 * ne * T * (zp1 * zp1 * zp1 * zp1);
-  double H = P->nH0 * q->eph[0] + P->nHe0 * q->eph[1] + P->nHep * q->eph[2];
-  f[0] = (H - L) / rho;
-  if (p->fext) f[0] = f[0] + p->fext[0];
+  *out = *P;
   return 0;
+}
+
+/* pin entry: converged populations [T, nH0, nH+, nHe0, nHe+, nHe++, ne, g] */
+int orc_kwh_state(const orc_problem *p, double e, double *out8)
+{
+  kwh_pop P;
+  int r = kwh_solve(p, e, &P);
+  out8[0] = P.T; out8[1] = P.nH0; out8[2] = P.nHp; out8[3] = P.nHe0;
+  out8[4] = P.nHep; out8[5] = P.nHepp; out8[6] = P.ne; out8[7] = P.g;
+  return r;
 }
 
 /* ---- dispatch ---------------------------------------------------------- */

@@ -138,6 +138,10 @@ int orc_rhs(const orc_problem *p, double t, const double *y, double *f);
  * (MECH).  Returns 0 or >0 on failure.  KWH has no J (CVDiag only).       */
 int orc_jac(const orc_problem *p, double t, const double *y, double *J);
 
+/* KWH pin entry: converged ionisation state for energy e:
+ * out8 = [T, n_H0, n_H+, n_He0, n_He+, n_He++, n_e, g(x_e)]              */
+int orc_kwh_state(const orc_problem *p, double e, double *out8);
+
 /* cvSetBDF + cvSetTqBDF for the coefficient pins: l[0..5], tq[1..5] */
 void orc_set_bdf(int q, double h, const double *tau /* [7], tau[1..6] */,
                  int qwait, double *l, double *tq);

@@ -96,6 +96,8 @@ def lib():
             L.orc_rhs.argtypes = [C.POINTER(Problem), C.c_double, dp, dp]
             L.orc_jac.restype = C.c_int
             L.orc_jac.argtypes = [C.POINTER(Problem), C.c_double, dp, dp]
+            L.orc_kwh_state.restype = C.c_int
+            L.orc_kwh_state.argtypes = [C.POINTER(Problem), C.c_double, dp]
             L.orc_set_bdf.restype = None
             L.orc_set_bdf.argtypes = [C.c_int, C.c_double, dp, C.c_int, dp, dp]
             L.orc_integrate.restype = C.c_int
@@ -292,6 +294,14 @@ def jac(model, y, rho=1.0, fext=None, t=0.0):
     p = model.problem(rho, fext)
     r = lib().orc_jac(C.byref(p), t, _dp(y), _dp(J))
     return J, r
+
+
+def kwh_state(model, e, rho):
+    """Converged KWH ionisation state: dict(T, nH0, nHp, nHe0, nHep, nHepp, ne, g), status."""
+    out = np.zeros(8)
+    p = model.problem(rho, None)
+    r = lib().orc_kwh_state(C.byref(p), float(e), _dp(out))
+    return dict(zip(["T", "nH0", "nHp", "nHe0", "nHep", "nHepp", "ne", "g"], out)), r
 
 
 def make_opts(n, rtol, atol, qmax=5, mxstep=10000, h0=0.0, hmin=0.0, hmax=0.0, ls=LS_DENSE, group=1):
