@@ -1,0 +1,206 @@
+/*
+ * bdfb.h -- C ABI of libbdfb: batched, per-cell adaptive, variable-order BDF
+ * integration of N independent stiff ODE systems on an NVIDIA B200 (sm_100a).
+ *
+ * What it computes (the hot path of arXiv 2405.01713, "SUNDIALS Time
+ * Integrators for Exascale Applications with Many Independent ODE Systems"):
+ *   for every cell c = 0..N-1 advance   dy_c/dt = R(t, y_c) + F_c      (Eq. 1,
+ *   P:91-96; split form "dU/dt = F + R" with F frozen over dt_CFD, P:196-201,
+ *   P:242-247) from t0 to tf = t0 + dt_CFD with CVODE's fixed-leading-
+ *   coefficient BDF of orders 1..5, modified Newton with the
+ *   stopping test of Eq. 4 and a dense LU with partial pivoting
+ *    or the CVDiag diagonal solver, errors measured in the WRMS
+ *   norm of Eq. 3.  The step-by-step algorithm is SURVEY.md
+ *   §8(c).2; DESIGN.md lists every reading of the paper it relies on.
+ *
+ * Paths: BDFB_MODE_PER_CELL (default) gives every cell its own h, q and
+ * history (the north_star design); the paper's lockstep batch with one
+ * batch-wide WRMS norm is BDFB_MODE_GLOBAL_NORM.
+ *
+ * Conventions for every entry point:
+ *  - All functions return int: 0 = success, < 0 = error (see BDFB_E*), and
+ *    never throw or abort across the ABI.  bdfb_last_error() describes the
+ *    last failure on a handle.
+ *  - Pointers documented "device" are CUDA device pointers on the handle's
+ *    device; "host" pointers are ordinary host memory.  The caller owns every
+ *    array it passes; the library owns only its workspace and model constants.
+ *  - Arrays are fp64 unless stated.  State layout is YC (component-major,
+ *    y[k*N + c], the coalescing order of P:290-300) unless BDFB_LAYOUT_CY
+ *    (cell-major, y[c*n + k]) is given.
+ *  - A handle is bound to one device and is not thread-safe; work is enqueued
+ *    on the caller's CUDA stream (cudaStream_t passed as void*, NULL = legacy
+ *    default stream).
+ */
+#ifndef BDFB_H
+#define BDFB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BDFB_VERSION_MAJOR 0
+#define BDFB_VERSION_MINOR 1
+
+/* ---- error codes (< 0) -------------------------------------------------- */
+#define BDFB_OK 0
+#define BDFB_EINVAL (-1)      /* invalid argument                           */
+#define BDFB_ENOMEM (-2)      /* device allocation failed (create only)     */
+#define BDFB_ECUDA (-3)       /* CUDA runtime / launch error                */
+#define BDFB_ENOMODEL (-4)    /* bdfb_set_model not called / wrong n        */
+#define BDFB_ENCCL (-5)       /* NCCL error (global-norm mode)              */
+#define BDFB_EUNSUPPORTED (-6)
+
+/* ---- per-cell status (mirrors CVODE return flags) ------ */
+#define BDFB_CELL_OK 0
+#define BDFB_CELL_TOO_MUCH_WORK 1    /* > mxstep internal steps (reading R12) */
+#define BDFB_CELL_ERR_FAILURE 2      /* 7 error-test failures in one step    */
+#define BDFB_CELL_CONV_FAILURE 3     /* 10 Newton convergence failures       */
+#define BDFB_CELL_RHS_FAIL 4         /* unrecoverable RHS failure            */
+#define BDFB_CELL_NONFINITE_INPUT 5  /* y0 or F not finite: not integrated  */
+
+/* ---- models: "set RHS and Jacobian kernels" ----------------------------- */
+#define BDFB_MODEL_LINEAR 0        /* n=1: y' = lambda y + F; params: double lambda          */
+#define BDFB_MODEL_ROBERTSON 1     /* n=3: Robertson kinetics; params: double k[3]    */
+#define BDFB_MODEL_NYX_KWH 2       /* n=1: Nyx-style heating/cooling, CVDiag;
+                                      params: bdfb_kwh_params; aux[c] = rho [g/cm^3]          */
+#define BDFB_MODEL_MECH_H2 3       /* n=10: H2/air mechanism (mechanisms/h2_lidryer.json),
+                                      constant-volume reactor; aux[c] = rho; params: NULL     */
+#define BDFB_MODEL_MECH_DRM19 4    /* n=22: DRM19-class CH4/air (mechanisms/drm19_class.json) */
+
+#define BDFB_LAYOUT_YC 0
+#define BDFB_LAYOUT_CY 1
+
+#define BDFB_MODE_PER_CELL 0
+#define BDFB_MODE_GLOBAL_NORM 1
+
+typedef struct bdfb_batch bdfb_batch;
+
+/* Nyx KWH96-form heating/cooling constants. */
+typedef struct {
+  double z;          /* redshift                                 */
+  double X, Y;       /* hydrogen / helium mass fractions          */
+  double gamma_ad;   /* adiabatic index                           */
+  double gph[3];     /* photo-ionisation rates H0, He0, He+ [1/s] */
+  double eph[3];     /* photo-heating rates H0, He0, He+ [erg/s]  */
+} bdfb_kwh_params;
+
+typedef struct {
+  int32_t qmax;      /* maximum BDF order, 1..5 (default 5)                       */
+  int32_t mode;      /* BDFB_MODE_PER_CELL (default) | BDFB_MODE_GLOBAL_NORM       */
+  int64_t mxstep;    /* max internal steps per cell per integrate (default 10000)  */
+  double h0;         /* initial step; 0 = CVODE cvHin estimate (default 0)         */
+  double hmin;       /* minimum |h| (default 0)                                    */
+  double hmax;       /* maximum |h|; 0 = unlimited (default 0)                     */
+} bdfb_options;
+
+/* Aggregate statistics of the last integrate (sums over cells). */
+typedef struct {
+  int64_t n_cells;
+  int64_t n_failed;          /* cells with status != BDFB_CELL_OK              */
+  int64_t nst, nfe, nje, nsetups, nni, netf, ncfn;   /* sums over cells       */
+  int64_t nst_max;           /* max over cells of nst                          */
+  int64_t nfe_max;
+} bdfb_stats;
+
+/* Optional per-cell outputs: device arrays of length N (any may be NULL). */
+typedef struct {
+  int32_t *status;
+  int32_t *nst, *nfe, *nje, *nsetups, *nni, *netf, *ncfn;
+  int32_t *q_last;
+  double *h_last;
+  double *t_reached;
+} bdfb_cell_stats;
+
+/* Fill *opt with the defaults above. */
+void bdfb_default_options(bdfb_options *opt);
+
+/* Create a batch of n_cells systems of size n on CUDA device `device`.
+ * rtol > 0; atol_host: host array of n values > 0 (Eq. 3; shared by
+ * all cells, reading R13).  Allocates ALL workspace once (no allocation ever
+ * happens in bdfb_integrate; the lesson of P:527-535).  opt may be NULL.
+ * Returns BDFB_EINVAL for bad sizes/tolerances, BDFB_ENOMEM, BDFB_ECUDA.   */
+int bdfb_create(bdfb_batch **out, int64_t n_cells, int32_t n, double rtol,
+                const double *atol_host, const bdfb_options *opt, int32_t device);
+
+/* Select the RHS + Jacobian kernels ("set RHS and Jacobian kernels").
+ * model_id: BDFB_MODEL_*; its n must equal the batch's n (else
+ * BDFB_ENOMODEL).  params/bytes: host pointer to the model's constant
+ * parameters (copied), or NULL for defaults.                               */
+int bdfb_set_model(bdfb_batch *b, int32_t model_id, const void *params, size_t bytes);
+
+/* Attach (or detach with NULL) caller-owned per-cell statistics arrays that
+ * the next bdfb_integrate fills.  The struct is copied.                     */
+int bdfb_set_cell_stats(bdfb_batch *b, const bdfb_cell_stats *cs);
+
+/* Integrate every cell from t0 to tf (tf > t0) on `stream`.
+ *  y     : device, in/out, N*n fp64 (layout as given).  On return each cell
+ *          holds y(tf), or, if its status is not OK, its last accepted state
+ *          (t_reached < tf).
+ *  f_ext : device, N*n fp64 frozen forcing F (same layout), or NULL for 0.
+ *  aux   : device, N fp64 per-cell auxiliary input (density for NYX_KWH and
+ *          MECH_*), or NULL when the model needs none.
+ * Per-cell mode enqueues asynchronously; results are valid when `stream`
+ * completes.  Returns 0 on enqueue, < 0 on an argument or launch error.
+ * Failed cells are counted by bdfb_get_stats (they are not an error here). */
+int bdfb_integrate(bdfb_batch *b, double t0, double tf, double *y, const double *f_ext,
+                   const double *aux, int32_t layout, void *stream);
+
+/* End-to-end variant with HOST buffers (same layout and meaning as
+ * bdfb_integrate): copies y, f_ext, aux host->device, integrates and copies
+ * y device->host, all on `stream`, then synchronises it.  Host buffers should
+ * be page-locked for full PCIe/C2C bandwidth.  The device staging buffers
+ * are allocated on the first call and kept until bdfb_destroy.            */
+int bdfb_integrate_host(bdfb_batch *b, double t0, double tf, double *y_host, const double *f_ext_host,
+                        const double *aux_host, int32_t layout, void *stream);
+
+/* Synchronise the last integrate's stream and return its aggregate
+ * statistics in *agg (host).  Return value: number of failed cells (>= 0)
+ * or < 0 on error.                                                          */
+int64_t bdfb_get_stats(bdfb_batch *b, bdfb_stats *agg);
+
+/* Kernel launches made by the last bdfb_integrate (for bench accounting). */
+int32_t bdfb_last_launch_count(const bdfb_batch *b);
+
+/* Device time in milliseconds of the last integrate's main kernel, measured
+ * with CUDA events on the launch stream (synchronises that stream).       */
+double bdfb_last_kernel_ms(bdfb_batch *b);
+
+/* Free everything owned by the handle (NULL is a no-op). */
+void bdfb_destroy(bdfb_batch *b);
+
+/* Message for the last failure on b (or a global message when b is NULL). */
+const char *bdfb_last_error(const bdfb_batch *b);
+
+/* "MAJOR.MINOR sm_100a" */
+const char *bdfb_version(void);
+
+/* ---- diagnostic entry points: the hot path's building blocks on identical
+ * inputs, for the RHS / Jacobian / LU parity tests.
+ * They run the SAME device functions the integrator uses.                  */
+
+/* f = R(t, y) + F for every cell (YC layout).  status: device int32[N] or
+ * NULL (0 = ok, 1 = recoverable RHS failure).                              */
+int bdfb_eval_rhs(bdfb_batch *b, double t, const double *y, const double *f_ext,
+                  const double *aux, double *f, int32_t *status, void *stream);
+
+/* J = dR/dy for every cell: J[(i*n + j)*N + c] (device, N*n*n fp64).
+ * Only for dense-solver models (not NYX_KWH).                               */
+int bdfb_eval_jac(bdfb_batch *b, double t, const double *y, const double *aux, double *J,
+                  void *stream);
+
+/* Batched LU with partial pivoting + solve, the integrator's own routine
+ * (listing LU_FACTOR / LU_SOLVE).  For each of N systems of size
+ * n (n in 1..32): M[(i*n + j)*N + c] (device, in/out: the LU factors in
+ * LAPACK getrf form, rows in pivoted order), piv[k*N + c] (device int32,
+ * getrf pivot indices), b[i*N + c] (device, in/out: the solution),
+ * info[c] (device int32: 0, or k+1 when pivot k is exactly zero).           */
+int bdfb_lu_factor_solve(int32_t n, int64_t N, double *M, int32_t *piv, double *b,
+                         int32_t *info, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

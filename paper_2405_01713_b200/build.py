@@ -1,0 +1,52 @@
+"""Build libbdfb.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+Steps: (1) codegen: mechanisms/*.json -> csrc/gen/mech_*.cuh; (2) nvcc
+-gencode arch=compute_100a,code=sm_100a -lineinfo into
+paper_2405_01713_b200/libbdfb.so.  Rebuilds only when a source is newer.
+-fmad=false: no implicit contraction, so decision-feeding scalar arithmetic
+follows the listing's operation order; fma() is written where intended.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(PKG)
+LIB = os.path.join(PKG, "libbdfb.so")
+CSRC = os.path.join(PKG, "csrc")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "--shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+
+
+def sources():
+    return (glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+            glob.glob(os.path.join(REPO, "include", "*.h")) + glob.glob(os.path.join(REPO, "mechanisms", "*.json")) +
+            [os.path.join(PKG, "codegen", "gen_mech.py"), __file__])
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    sys.path.insert(0, REPO)
+    from paper_2405_01713_b200.codegen import gen_mech
+    gen_mech.main([])
+    if not force and os.path.exists(LIB):
+        t = os.path.getmtime(LIB)
+        if all(os.path.getmtime(s) <= t for s in sources()):
+            return LIB
+    cmd = [NVCC] + ARCH + FLAGS + ["-o", LIB + ".tmp", os.path.join(CSRC, "bdfb.cu")]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+        f.write(r.stdout + r.stderr)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + r.stderr[-4000:])
+    os.replace(LIB + ".tmp", LIB)
+    if verbose:
+        print(r.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,514 @@
+// bdfb.cu -- C ABI of libbdfb (declared and documented in include/bdfb.h).
+//
+// Owns the workspace (allocated once in bdfb_create), the model selection and
+// the launch configuration of the persistent per-cell integrator kernel
+// (bdf_cell.cuh).  No allocation, host round trip or synchronisation happens
+// inside bdfb_integrate: one kernel launch + two tiny memsets on the caller's
+// stream.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+
+#include "../../include/bdfb.h"
+#include "bdf_cell.cuh"
+#include "gen/mech_drm19_class.cuh"
+#include "gen/mech_h2_lidryer.cuh"
+#include "mech_model.cuh"
+#include "models_simple.cuh"
+
+using namespace bdfb;
+
+using ModelH2 = ModelMech<mech_h2_lidryer::Traits>;
+using ModelDRM19 = ModelMech<mech_drm19_class::Traits>;
+
+struct bdfb_batch {
+  int device = 0;
+  long long ncells = 0;
+  int n = 0;
+  double rtol = 0.0;
+  bdfb_options opt{};
+  int model = -1;
+  unsigned char params[256] = {};
+  double* d_atol = nullptr;
+  unsigned long long* d_counter = nullptr;
+  Agg* d_agg = nullptr;
+  double *d_y = nullptr, *d_f = nullptr, *d_aux = nullptr;   // host-API staging
+  CellStatsPtrs cs{};
+  cudaStream_t last_stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+  int launches = 0;
+  std::string err;
+};
+
+static std::string g_err;
+
+static int fail(bdfb_batch* b, int code, const std::string& msg) {
+  if (b) b->err = msg; else g_err = msg;
+  return code;
+}
+
+static int cuda_fail(bdfb_batch* b, cudaError_t e, const char* where) {
+  return fail(b, BDFB_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+static int model_n(int model) {
+  switch (model) {
+    case BDFB_MODEL_LINEAR: return ModelLinear::N;
+    case BDFB_MODEL_ROBERTSON: return ModelRobertson::N;
+    case BDFB_MODEL_NYX_KWH: return ModelNyxKwh::N;
+    case BDFB_MODEL_MECH_H2: return ModelH2::N;
+    case BDFB_MODEL_MECH_DRM19: return ModelDRM19::N;
+  }
+  return -1;
+}
+
+extern "C" {
+
+void bdfb_default_options(bdfb_options* o) {
+  o->qmax = 5;
+  o->mode = BDFB_MODE_PER_CELL;
+  o->mxstep = 10000;
+  o->h0 = 0.0;
+  o->hmin = 0.0;
+  o->hmax = 0.0;
+}
+
+const char* bdfb_version(void) { return "0.1 sm_100a"; }
+
+const char* bdfb_last_error(const bdfb_batch* b) { return b ? b->err.c_str() : g_err.c_str(); }
+
+int bdfb_create(bdfb_batch** out, int64_t n_cells, int32_t n, double rtol, const double* atol_host,
+                const bdfb_options* opt, int32_t device) {
+  if (!out) return fail(nullptr, BDFB_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n_cells < 1) return fail(nullptr, BDFB_EINVAL, "n_cells must be >= 1");
+  if (n < 1 || n > 32) return fail(nullptr, BDFB_EINVAL, "n must be in 1..32");
+  if (!(rtol > 0.0) || !isfinite(rtol)) return fail(nullptr, BDFB_EINVAL, "rtol must be > 0");
+  if (!atol_host) return fail(nullptr, BDFB_EINVAL, "atol is NULL");
+  for (int i = 0; i < n; ++i)
+    if (!(atol_host[i] > 0.0) || !isfinite(atol_host[i])) return fail(nullptr, BDFB_EINVAL, "atol_i must be > 0");
+  bdfb_options o;
+  bdfb_default_options(&o);
+  if (opt) o = *opt;
+  if (o.qmax < 1 || o.qmax > 5) return fail(nullptr, BDFB_EINVAL, "qmax must be in 1..5");
+  if (o.mxstep < 1) return fail(nullptr, BDFB_EINVAL, "mxstep must be >= 1");
+  if (o.mode != BDFB_MODE_PER_CELL) return fail(nullptr, BDFB_EUNSUPPORTED, "global-norm mode not in this build");
+  if (o.h0 < 0.0 || o.hmin < 0.0 || o.hmax < 0.0) return fail(nullptr, BDFB_EINVAL, "h0/hmin/hmax must be >= 0");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+  bdfb_batch* b = new bdfb_batch();
+  b->device = device;
+  b->ncells = n_cells;
+  b->n = n;
+  b->rtol = rtol;
+  b->opt = o;
+  if ((e = cudaMalloc(&b->d_atol, sizeof(double) * n)) != cudaSuccess ||
+      (e = cudaMalloc(&b->d_counter, sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMalloc(&b->d_agg, sizeof(Agg))) != cudaSuccess) {
+    bdfb_destroy(b);
+    return fail(nullptr, BDFB_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  if ((e = cudaMemcpy(b->d_atol, atol_host, sizeof(double) * n, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaEventCreate(&b->ev0)) != cudaSuccess || (e = cudaEventCreate(&b->ev1)) != cudaSuccess) {
+    bdfb_destroy(b);
+    return cuda_fail(nullptr, e, "create");
+  }
+  *out = b;
+  return BDFB_OK;
+}
+
+void bdfb_destroy(bdfb_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  if (b->d_atol) cudaFree(b->d_atol);
+  if (b->d_counter) cudaFree(b->d_counter);
+  if (b->d_agg) cudaFree(b->d_agg);
+  if (b->d_y) cudaFree(b->d_y);
+  if (b->d_f) cudaFree(b->d_f);
+  if (b->d_aux) cudaFree(b->d_aux);
+  if (b->ev0) cudaEventDestroy(b->ev0);
+  if (b->ev1) cudaEventDestroy(b->ev1);
+  delete b;
+}
+
+int bdfb_set_model(bdfb_batch* b, int32_t model_id, const void* params, size_t bytes) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  const int mn = model_n(model_id);
+  if (mn < 0) return fail(b, BDFB_ENOMODEL, "unknown model id");
+  if (mn != b->n) return fail(b, BDFB_ENOMODEL, "model size n does not match the batch");
+  memset(b->params, 0, sizeof(b->params));
+  size_t need = 0;
+  switch (model_id) {
+    case BDFB_MODEL_LINEAR: {
+      ModelLinear::Params p{-1.0};
+      need = sizeof(p);
+      memcpy(b->params, &p, need);
+      break;
+    }
+    case BDFB_MODEL_ROBERTSON: {
+      ModelRobertson::Params p{{0.04, 3e7, 1e4}};
+      need = sizeof(p);
+      memcpy(b->params, &p, need);
+      break;
+    }
+    case BDFB_MODEL_NYX_KWH: {
+      ModelNyxKwh::Params p{3.0, 0.76, 0.24, 5.0 / 3.0, {1.0e-12, 6.0e-13, 3.0e-15}, {4.0e-24, 5.0e-24, 7.0e-26}};
+      static_assert(sizeof(ModelNyxKwh::Params) == sizeof(bdfb_kwh_params), "ABI layout");
+      need = sizeof(p);
+      memcpy(b->params, &p, need);
+      break;
+    }
+    default:
+      need = 0;
+  }
+  if (params) {
+    if (bytes != need) return fail(b, BDFB_EINVAL, "params size does not match the model");
+    memcpy(b->params, params, bytes);
+  }
+  b->model = model_id;
+  return BDFB_OK;
+}
+
+int bdfb_set_cell_stats(bdfb_batch* b, const bdfb_cell_stats* cs) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  CellStatsPtrs p{};
+  if (cs) {
+    p.status = cs->status; p.nst = cs->nst; p.nfe = cs->nfe; p.nje = cs->nje; p.nsetups = cs->nsetups;
+    p.nni = cs->nni; p.netf = cs->netf; p.ncfn = cs->ncfn; p.q_last = cs->q_last; p.h_last = cs->h_last;
+    p.t_reached = cs->t_reached;
+  }
+  b->cs = p;
+  return BDFB_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ launches
+template <class Model>
+static int launch_integrate(bdfb_batch* b, const Opts& o, double* y, const double* fext, const double* aux,
+                            cudaStream_t st) {
+  using I = Integrator<Model>;
+  auto kern = integrate_kernel<Model>;
+  const int warps = Model::BLOCK / 32;
+  const size_t smem = sizeof(double) * (size_t)I::SMEM_WARP * warps;
+  cudaError_t e;
+  if (smem > 48 * 1024) {
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      return cuda_fail(b, e, "cudaFuncSetAttribute");
+  }
+  int nsm = 0, per_sm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, b->device);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Model::BLOCK, smem)) != cudaSuccess)
+    return cuda_fail(b, e, "occupancy");
+  if (per_sm < 1) return fail(b, BDFB_ECUDA, "kernel does not fit on an SM");
+  const long long groups_needed = (o.ncells + I::CHUNK - 1) / I::CHUNK;
+  const long long groups_per_block = Model::BLOCK / Model::G;
+  long long grid = (long long)nsm * per_sm;
+  const long long need_blocks = (groups_needed + groups_per_block - 1) / groups_per_block;
+  if (grid > need_blocks) grid = need_blocks;
+  typename Model::Params prm;
+  memcpy(&prm, b->params, sizeof(prm));
+  cudaMemsetAsync(b->d_counter, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(b->d_agg, 0, sizeof(Agg), st);
+  cudaEventRecord(b->ev0, st);
+  kern<<<(unsigned)grid, Model::BLOCK, smem, st>>>(o, prm, y, fext, aux, b->d_atol, b->d_counter, b->d_agg, b->cs);
+  cudaEventRecord(b->ev1, st);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(b, e, "integrate launch");
+  b->launches = 1;
+  b->timed = true;
+  return BDFB_OK;
+}
+
+extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, const double* f_ext,
+                              const double* aux, int32_t layout, void* stream) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (b->model < 0) return fail(b, BDFB_ENOMODEL, "bdfb_set_model not called");
+  if (!y) return fail(b, BDFB_EINVAL, "y is NULL");
+  if (!(tf > t0) || !isfinite(t0) || !isfinite(tf)) return fail(b, BDFB_EINVAL, "need finite tf > t0");
+  if (layout != BDFB_LAYOUT_YC && layout != BDFB_LAYOUT_CY) return fail(b, BDFB_EINVAL, "bad layout");
+  const bool needs_aux = (b->model == BDFB_MODEL_NYX_KWH || b->model == BDFB_MODEL_MECH_H2 ||
+                          b->model == BDFB_MODEL_MECH_DRM19);
+  if (needs_aux && !aux) return fail(b, BDFB_EINVAL, "this model needs aux (density)");
+  cudaSetDevice(b->device);
+  Opts o;
+  o.rtol = b->rtol;
+  o.t0 = t0;
+  o.tf = tf;
+  o.h0 = b->opt.h0;
+  o.hmin = b->opt.hmin;
+  o.hmax = b->opt.hmax;
+  o.mxstep = b->opt.mxstep;
+  o.qmax = b->opt.qmax;
+  o.layout = layout;
+  o.ncells = b->ncells;
+  cudaStream_t st = (cudaStream_t)stream;
+  b->last_stream = st;
+  switch (b->model) {
+    case BDFB_MODEL_LINEAR: return launch_integrate<ModelLinear>(b, o, y, f_ext, aux, st);
+    case BDFB_MODEL_ROBERTSON: return launch_integrate<ModelRobertson>(b, o, y, f_ext, aux, st);
+    case BDFB_MODEL_NYX_KWH: return launch_integrate<ModelNyxKwh>(b, o, y, f_ext, aux, st);
+    case BDFB_MODEL_MECH_H2: return launch_integrate<ModelH2>(b, o, y, f_ext, aux, st);
+    case BDFB_MODEL_MECH_DRM19: return launch_integrate<ModelDRM19>(b, o, y, f_ext, aux, st);
+  }
+  return fail(b, BDFB_ENOMODEL, "unknown model");
+}
+
+extern "C" int bdfb_integrate_host(bdfb_batch* b, double t0, double tf, double* y_host, const double* f_ext_host,
+                                   const double* aux_host, int32_t layout, void* stream) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (!y_host) return fail(b, BDFB_EINVAL, "y is NULL");
+  cudaSetDevice(b->device);
+  cudaError_t e;
+  const size_t ybytes = sizeof(double) * (size_t)b->ncells * b->n;
+  const size_t abytes = sizeof(double) * (size_t)b->ncells;
+  if (!b->d_y) {
+    if ((e = cudaMalloc(&b->d_y, ybytes)) != cudaSuccess) return fail(b, BDFB_ENOMEM, "staging y");
+  }
+  if (f_ext_host && !b->d_f) {
+    if ((e = cudaMalloc(&b->d_f, ybytes)) != cudaSuccess) return fail(b, BDFB_ENOMEM, "staging f_ext");
+  }
+  if (aux_host && !b->d_aux) {
+    if ((e = cudaMalloc(&b->d_aux, abytes)) != cudaSuccess) return fail(b, BDFB_ENOMEM, "staging aux");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((e = cudaMemcpyAsync(b->d_y, y_host, ybytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(b, e, "H2D y");
+  if (f_ext_host && (e = cudaMemcpyAsync(b->d_f, f_ext_host, ybytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(b, e, "H2D f_ext");
+  if (aux_host && (e = cudaMemcpyAsync(b->d_aux, aux_host, abytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(b, e, "H2D aux");
+  int rc = bdfb_integrate(b, t0, tf, b->d_y, f_ext_host ? b->d_f : nullptr, aux_host ? b->d_aux : nullptr, layout,
+                          stream);
+  if (rc) return rc;
+  if ((e = cudaMemcpyAsync(y_host, b->d_y, ybytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(b, e, "D2H y");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(b, e, "synchronize");
+  return BDFB_OK;
+}
+
+extern "C" int64_t bdfb_get_stats(bdfb_batch* b, bdfb_stats* agg) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  cudaSetDevice(b->device);
+  cudaError_t e = cudaStreamSynchronize(b->last_stream);
+  if (e != cudaSuccess) return cuda_fail(b, e, "stream synchronize");
+  Agg h{};
+  if ((e = cudaMemcpy(&h, b->d_agg, sizeof(Agg), cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return cuda_fail(b, e, "stats copy");
+  if (agg) {
+    agg->n_cells = (int64_t)h.cells_done;
+    agg->n_failed = (int64_t)h.n_failed;
+    agg->nst = (int64_t)h.nst;
+    agg->nfe = (int64_t)h.nfe;
+    agg->nje = (int64_t)h.nje;
+    agg->nsetups = (int64_t)h.nsetups;
+    agg->nni = (int64_t)h.nni;
+    agg->netf = (int64_t)h.netf;
+    agg->ncfn = (int64_t)h.ncfn;
+    agg->nst_max = (int64_t)h.nst_max;
+    agg->nfe_max = (int64_t)h.nfe_max;
+  }
+  return (int64_t)h.n_failed;
+}
+
+extern "C" int32_t bdfb_last_launch_count(const bdfb_batch* b) { return b ? b->launches : 0; }
+
+extern "C" double bdfb_last_kernel_ms(bdfb_batch* b) {
+  if (!b || !b->timed) return -1.0;
+  cudaSetDevice(b->device);
+  if (cudaEventSynchronize(b->ev1) != cudaSuccess) return -1.0;
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, b->ev0, b->ev1) != cudaSuccess) return -1.0;
+  return (double)ms;
+}
+
+// ------------------------------------------------------- diagnostic kernels
+template <class Model>
+__global__ void __launch_bounds__(128) eval_kernel(typename Model::Params prm, long long N, double t, const double* y,
+                                                   const double* fext, const double* aux, double* f, int* status,
+                                                   double* J) {
+  constexpr int G = Model::G, NN = Model::N, R = (NN + G - 1) / G;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5;
+  constexpr int MAT = (G == 1 ? NN * NN : NN) * WS;
+  constexpr int SW = MAT + Model::SCRATCH;
+  double* Jm = smem + warp * SW;
+  double* scratch = Jm + MAT;
+  Grp<G> g;
+  const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const bool live = grp < N;
+  const long long c = live ? grp : 0;
+  double yy[R], ff[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int k = g.lane + G * r;
+    yy[r] = (k < NN) ? y[(long long)k * N + c] : 0.0;
+  }
+  const double a = aux ? aux[c] : 0.0;
+  // every group of the warp runs the device function (dead groups on cell 0)
+  if (J == nullptr) {
+    int rv = Model::rhs(g, prm, t, yy, ff, a, scratch);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int k = g.lane + G * r;
+      if (live && k < NN) f[(long long)k * N + c] = ff[r] + (fext ? fext[(long long)k * N + c] : 0.0);
+    }
+    if (live && g.lane == 0 && status) status[c] = rv;
+  } else {
+    if constexpr (!Model::DIAG) {
+      int rv = Model::jac(g, prm, t, yy, a, Jm, scratch);
+      (void)rv;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = g.lane + G * r;
+        if (live && i < NN)
+          for (int j = 0; j < NN; ++j) J[((long long)i * NN + j) * N + c] = mat<NN, G>(Jm, g, r, j);
+      }
+    }
+  }
+}
+
+template <class Model>
+static int launch_eval(bdfb_batch* b, double t, const double* y, const double* fext, const double* aux, double* f,
+                       int* status, double* J, cudaStream_t st) {
+  constexpr int G = Model::G, NN = Model::N;
+  constexpr int MAT = (G == 1 ? NN * NN : NN) * WS;
+  const size_t smem = sizeof(double) * (size_t)(MAT + Model::SCRATCH) * 4;
+  auto kern = eval_kernel<Model>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  typename Model::Params prm;
+  memcpy(&prm, b->params, sizeof(prm));
+  const long long threads = b->ncells * G;
+  const unsigned grid = (unsigned)((threads + 127) / 128);
+  kern<<<grid, 128, smem, st>>>(prm, b->ncells, t, y, fext, aux, f, status, J);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(b, e, "eval launch");
+  return BDFB_OK;
+}
+
+extern "C" int bdfb_eval_rhs(bdfb_batch* b, double t, const double* y, const double* f_ext, const double* aux,
+                             double* f, int32_t* status, void* stream) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (b->model < 0) return fail(b, BDFB_ENOMODEL, "bdfb_set_model not called");
+  if (!y || !f) return fail(b, BDFB_EINVAL, "y/f NULL");
+  cudaSetDevice(b->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (b->model) {
+    case BDFB_MODEL_LINEAR: return launch_eval<ModelLinear>(b, t, y, f_ext, aux, f, status, nullptr, st);
+    case BDFB_MODEL_ROBERTSON: return launch_eval<ModelRobertson>(b, t, y, f_ext, aux, f, status, nullptr, st);
+    case BDFB_MODEL_NYX_KWH: return launch_eval<ModelNyxKwh>(b, t, y, f_ext, aux, f, status, nullptr, st);
+    case BDFB_MODEL_MECH_H2: return launch_eval<ModelH2>(b, t, y, f_ext, aux, f, status, nullptr, st);
+    case BDFB_MODEL_MECH_DRM19: return launch_eval<ModelDRM19>(b, t, y, f_ext, aux, f, status, nullptr, st);
+  }
+  return fail(b, BDFB_ENOMODEL, "unknown model");
+}
+
+extern "C" int bdfb_eval_jac(bdfb_batch* b, double t, const double* y, const double* aux, double* J, void* stream) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (b->model < 0) return fail(b, BDFB_ENOMODEL, "bdfb_set_model not called");
+  if (!y || !J) return fail(b, BDFB_EINVAL, "y/J NULL");
+  if (b->model == BDFB_MODEL_NYX_KWH) return fail(b, BDFB_EUNSUPPORTED, "CVDiag model has no Jacobian");
+  cudaSetDevice(b->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (b->model) {
+    case BDFB_MODEL_LINEAR: return launch_eval<ModelLinear>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
+    case BDFB_MODEL_ROBERTSON: return launch_eval<ModelRobertson>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
+    case BDFB_MODEL_MECH_H2: return launch_eval<ModelH2>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
+    case BDFB_MODEL_MECH_DRM19: return launch_eval<ModelDRM19>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
+  }
+  return fail(b, BDFB_ENOMODEL, "unknown model");
+}
+
+// LU factor + solve over N systems (diagnostic; the integrator's routines)
+template <int NN, int G>
+__global__ void __launch_bounds__(128) lu_kernel(long long N, double* M, int* piv, double* bvec, int* info) {
+  extern __shared__ double smem[];
+  constexpr int MAT = (G == 1 ? NN * NN : NN) * WS;
+  const int warp = threadIdx.x >> 5;
+  double* A = smem + warp * (MAT + 16);
+  int* perm = reinterpret_cast<int*>(A + MAT);
+  Grp<G> g;
+  const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const bool live = grp < N;
+  const long long c = live ? grp : 0;
+  if constexpr (G == 1) {
+    for (int i = 0; i < NN; ++i)
+      for (int j = 0; j < NN; ++j) mat<NN, 1>(A, g, i, j) = M[((long long)i * NN + j) * N + c];
+    int pv[NN];
+    int inf = lu_factor_thread<NN>(g, A, pv);
+    double bb[NN];
+    for (int i = 0; i < NN; ++i) bb[i] = bvec[(long long)i * N + c];
+    if (!inf) lu_solve_thread<NN>(g, A, pv, bb);
+    if (live) {
+      info[c] = inf;
+      for (int i = 0; i < NN; ++i) {
+        bvec[(long long)i * N + c] = bb[i];
+        piv[(long long)i * N + c] = pv[i];
+        for (int j = 0; j < NN; ++j) M[((long long)i * NN + j) * N + c] = mat<NN, 1>(A, g, i, j);
+      }
+    }
+  } else {
+    const int i = g.lane;
+    if (i < NN)
+      for (int j = 0; j < NN; ++j) A[j * WS + g.wlane] = M[((long long)i * NN + j) * N + c];
+    g.sync();
+    int pos = 0;
+    const int inf = lu_factor_group<NN, G>(g, A, pos, perm);
+    double bb = (i < NN) ? bvec[(long long)i * N + c] : 0.0;
+    if (!inf) bb = lu_solve_group<NN, G>(g, A, pos, perm, bb);
+    if (live) {
+      if (g.lane == 0) info[c] = inf;
+      if (i < NN) {
+        bvec[(long long)i * N + c] = bb;
+        if (!inf)
+          for (int j = 0; j < NN; ++j) M[((long long)pos * NN + j) * N + c] = A[j * WS + g.wlane];
+      }
+      if (!inf && i < NN) {
+        // LAPACK pivot indices from the position permutation: replay the swaps
+        if (g.lane == 0) {
+          int at[32], where[32];  // at[position] = original row, where[row] = position
+          for (int k = 0; k < NN; ++k) { at[k] = k; where[k] = k; }
+          for (int k = 0; k < NN; ++k) {
+            const int row = perm[g.gbase + k];   // original row (= lane) at final position k
+            const int p = where[row];
+            piv[(long long)k * N + c] = p;
+            const int rk = at[k];
+            at[p] = rk; where[rk] = p;
+            at[k] = row; where[row] = k;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int NN>
+static int launch_lu(int64_t N, double* M, int32_t* piv, double* b, int32_t* info, cudaStream_t st) {
+  constexpr int G = NN <= 4 ? 1 : (NN <= 16 ? 16 : 32);
+  constexpr int MAT = (G == 1 ? NN * NN : NN) * WS;
+  const size_t smem = sizeof(double) * (MAT + 16) * 4;
+  auto kern = lu_kernel<NN, G>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const long long threads = N * G;
+  kern<<<(unsigned)((threads + 127) / 128), 128, smem, st>>>(N, M, piv, b, info);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BDFB_OK : cuda_fail(nullptr, e, "lu launch");
+}
+
+extern "C" int bdfb_lu_factor_solve(int32_t n, int64_t N, double* M, int32_t* piv, double* b, int32_t* info,
+                                    void* stream) {
+  if (N < 1 || !M || !piv || !b || !info) return fail(nullptr, BDFB_EINVAL, "bad LU arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (n) {
+#define LU_CASE(k) \
+  case k: return launch_lu<k>(N, M, piv, b, info, st);
+    LU_CASE(1) LU_CASE(2) LU_CASE(3) LU_CASE(4) LU_CASE(5) LU_CASE(6) LU_CASE(7) LU_CASE(8) LU_CASE(10) LU_CASE(12)
+    LU_CASE(16) LU_CASE(22) LU_CASE(32)
+#undef LU_CASE
+  }
+  return fail(nullptr, BDFB_EUNSUPPORTED, "n not instantiated (1-8,10,12,16,22,32)");
+}
