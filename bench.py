@@ -1,0 +1,348 @@
+"""Benchmark: cell ODE integrations per second per outer step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+A "step" is one outer fluid step of the hot path: bdfb_integrate of every cell
+of the workload from t0 to t0 + dt_CFD (per-cell BDF: RHS, Jacobian, Newton,
+LU, WRMS, step/order control -- SURVEY.md §8(a)), restarted each step from the
+same pristine synthetic field (copied in untimed; the state alone is 2.9 GB,
+far larger than the 126 MB L2).  Multi-GPU (torchrun): every rank integrates
+its own slab of cells (weak scaling, no collective on the data path); the
+timed total is the max over ranks.
+
+The JSON line carries the device-timed value, the FP64 roofline of the
+integrator kernel, the CPU oracle timed on the host cores (cpu_baseline), an
+end-to-end number through the host-buffer C-ABI call (e2e), the GPU clocks
+sampled during the timed region and the per-cell statistics behind the flop
+count.  `--impl reference` times the CPU oracle instead (the reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import re
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIGS = {
+    # id: (model, mech table, n, L, dt_CFD, rtol, atol, description)
+    "C1": ("robertson", None, 3, None, 40.0, 1e-4, (1e-8, 1e-14, 1e-6),
+           "C1 Robertson 3-species kinetics, 1024 cells, t in [0,40], rtol 1e-4"),
+    "C2": ("nyx_kwh", None, 1, 128, 3.0e15, 1e-6, 1e-10,
+           "C2 Nyx-style scalar heating/cooling (KWH96 form, CVDiag), 128^3 cells, dt 3e15 s"),
+    "C3": ("h2", "h2_lidryer", 10, 64, 1e-5, 1e-6, 1e-10,
+           "C3 H2/air (9 species + T, n=10) flame field on 64^3 cells, dt_CFD 1e-5 s"),
+    "C4": ("drm19", "drm19_class", 22, 256, 1e-5, 1e-6, 1e-10,
+           "C4 DRM19-class CH4/air (21 species + T, n=22) flame field on 256^3 cells, dt_CFD 1e-5 s"),
+}
+METRIC = "cell ODE integrations/sec per outer step"
+UNIT = "cells/s"
+FP64_FMA_PER_SM_CLK = 64        # B200 FP64 units per SM (sm_100a): 148 x 64 x 2 x 1.965 GHz = 37.2 TF
+SMS = 148
+SM_MAX_MHZ = 1965.0
+TRANSC_FLOPS = 20               # FP64 flops charged per exp/log
+
+
+# ------------------------------------------------------------------ inputs
+def make_inputs(cfg, rank=0, cells_per_rank=None):
+    from synth import flame_field, nyx_field, robertson_field
+    model, mech, n, L, dt, rtol, atol, _ = CONFIGS[cfg]
+    if cfg == "C1":
+        N = cells_per_rank or 1024
+        y = robertson_field(N, cells=np.arange(rank * N, (rank + 1) * N))
+        return y, None, None, np.arange(N)
+    if cfg == "C2":
+        N = cells_per_rank or L ** 3
+        e, rho, fe = nyx_field(L, cells=np.arange(rank * N, (rank + 1) * N), dt=dt)
+        return e, rho, fe, None
+    N = cells_per_rank or L ** 3
+    y, rho, F, prog = flame_field(mech, L, cells=np.arange(rank * N, (rank + 1) * N), dt=dt)
+    return y, rho, F, prog
+
+
+def flop_model(cfg, st):
+    """Algorithmic FP64 flops of one launch from the aggregate per-cell statistics."""
+    model, mech, n, *_ = CONFIGS[cfg]
+    if mech:
+        hdr = open(os.path.join(REPO, "paper_2405_01713_b200", "csrc", "gen", f"mech_{mech}.cuh")).read()
+        g = lambda k: int(re.search(rf"{k} = (\d+)", hdr).group(1))  # noqa: E731
+        f_rhs = g("FLOPS_RHS_ARITH") + TRANSC_FLOPS * g("RHS_TRANSCENDENTALS")
+        f_jac = g("FLOPS_JAC_ARITH") + TRANSC_FLOPS * g("JAC_TRANSCENDENTALS")
+    elif model == "robertson":
+        f_rhs, f_jac = 12, 10
+    else:  # nyx_kwh: ~12 regula-falsi evaluations x (~16 transcendental + 40 arith) + cooling sum
+        f_rhs, f_jac = 12 * (16 * TRANSC_FLOPS + 40) + 20 * TRANSC_FLOPS + 60, 0
+    f_lu = (2 * (n - 1) * n * (2 * n - 1)) // 6 + n * (n - 1) // 2 + n + 2 * n * n
+    f_sol = 2 * n * n - n
+    att = st["nst"] + st["netf"] + st["ncfn"]
+    return (st["nfe"] * f_rhs + st["nje"] * f_jac + st["nsetups"] * f_lu + st["nni"] * (f_sol + 9 * n) +
+            att * (6 * n + 20 * n + 60) + st["nst"] * (8 * n + 3 * n + 80))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.p = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+        return self
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) == len(self.FIELDS)]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in rows:
+            for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], r[4:]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][2]),
+                "reasons": sorted(reasons), "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+# ------------------------------------------------------------------ CPU oracle
+def oracle_cells_per_s(cfg, budget_s=15.0, threads=None, rank_cells=None, steps=1):
+    """Time the CPU oracle (as it stands) on a bounded stratified sample of the workload."""
+    from oracle import oracle as O
+    from synth.fields import stratified_sample
+    model, mech, n, L, dt, rtol, atol, _ = CONFIGS[cfg]
+    threads = threads or os.cpu_count() or 1
+    if cfg == "C1":
+        y, rho, F, prog = make_inputs(cfg)
+        om, G, idx = O.Model.robertson(), 1, np.arange(y.shape[1])
+    elif cfg == "C2":
+        from synth import nyx_field
+        idx = np.sort(np.random.default_rng(0).choice(L ** 3, 65536, replace=False))
+        e, rho, fe = nyx_field(L, cells=idx, dt=dt)
+        y, F, om, G = e, fe, O.Model.nyx_kwh(), 1
+        idx = np.arange(len(idx))
+    else:
+        from synth import flame_field
+        # stratified by flame progress over a 2M-cell window of the grid
+        cand = np.arange(min(L ** 3, 1 << 21))
+        _, _, _, prog = flame_field(mech, L, cells=cand, dt=dt, forcing=False)
+        pick = stratified_sample(prog, 40000)
+        y, rho, F, _ = flame_field(mech, L, cells=cand[pick], dt=dt)
+        om, G = O.Model.mechanism(mech), CONFIGS_G[cfg]
+        idx = np.arange(len(pick))
+
+    def run(sel):
+        t = time.perf_counter()
+        O.integrate_batch(om, y[:, sel], 0.0, dt, rtol, atol, rho=None if rho is None else rho[sel],
+                          fext_yc=None if F is None else F[:, sel], group=G, threads=threads)
+        return time.perf_counter() - t
+
+    probe = idx[: min(len(idx), 512)]
+    tp = run(probe)
+    m = int(min(len(idx), max(len(probe), len(probe) * budget_s / max(tp, 1e-6))))
+    # interleave strata: take every k-th cell so the sample keeps the class mix
+    sel = idx[np.linspace(0, len(idx) - 1, m).astype(int)]
+    times = [run(sel) for _ in range(steps)]
+    return m, times, threads
+
+
+CONFIGS_G = {"C3": 16, "C4": 32}
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cells", type=int, default=0, help="override cells per rank (debug)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = args.config
+    model, mech, n, L, dt, rtol, atol, desc = CONFIGS[cfg]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        for _ in range(0):
+            pass
+        m, times, thr = oracle_cells_per_s(cfg, budget_s=max(5.0, 60.0 / max(args.steps, 1)), steps=args.warmup +
+                                           args.steps)
+        times = times[args.warmup:] or times
+        tt = sum(times)
+        val = m * len(times) / tt
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / len(times),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": desc, "sample_cells_per_step": m},
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": thr, "kind": "oracle",
+                                 "sample": f"{m} stratified cells of the {cfg} workload per step"},
+                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_2405_01713_b200 as P
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    y0, rho, F, prog = make_inputs(cfg, rank, args.cells or None)
+    N = y0.shape[1]
+    b = P.Batch(N, n, rtol, atol, device=local)
+    b.set_model(model)
+    y_pristine = torch.tensor(y0, device=dev)
+    y = torch.empty_like(y_pristine)
+    Fd = None if F is None else torch.tensor(F, device=dev)
+    rd = None if rho is None else torch.tensor(rho, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        b.integrate(0.0, dt, y, f_ext=Fd, aux=rd)
+
+    for _ in range(args.warmup):
+        y.copy_(y_pristine)
+        step()
+    torch.cuda.synchronize()
+    st_w = b.stats()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kern_ms, stats = [], []
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            y.copy_(y_pristine)
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            kern_ms.append(b.last_kernel_ms())
+            stats.append(b.stats())
+    step_ms = [a.elapsed_time(z) for a, z in ev]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = N * world / (ms_per_step * 1e-3)
+
+    # roofline: algorithmic FP64 flops of the integrator kernel / its event-timed duration
+    flops = [flop_model(cfg, s) for s in stats]
+    achieved = statistics.mean(f / (k * 1e-3) for f, k in zip(flops, kern_ms)) / 1e12
+    peak = SMS * FP64_FMA_PER_SM_CLK * 2 * SM_MAX_MHZ * 1e6 / 1e12
+    probe = C_double = None
+    try:
+        import ctypes as C
+        tf, sm = C.c_double(), C.c_int32()
+        if P._lib.lib().bdfb_probe_fp64(local, 200.0, C.byref(tf), C.byref(sm)) == 0:
+            probe = tf.value
+    except Exception:
+        pass
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "integrate_kernel<ModelMech<%s>>" % (mech or model),
+            "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
+            "fp64_probe_tflops": probe, "kernel_ms": statistics.mean(kern_ms),
+            "flops_per_launch": statistics.mean(flops)}
+
+    # e2e through the host-buffer C-ABI call (pinned host memory; H2D + integrate + D2H timed)
+    yh0 = torch.tensor(y0).pin_memory()
+    yh = torch.empty_like(yh0).pin_memory()
+    Fh = None if F is None else torch.tensor(F).pin_memory()
+    rh = None if rho is None else torch.tensor(rho).pin_memory()
+    yh.copy_(yh0)
+    b.integrate_host(0.0, dt, yh, f_ext=Fh, aux=rh)            # allocates the staging buffers (warm-up)
+    e2e_ms = []
+    for i in range(args.steps):
+        yh.copy_(yh0)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        b.integrate_host(0.0, dt, yh, f_ext=Fh, aux=rh)
+        z.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(a.elapsed_time(z))
+    e2e_total = sum(e2e_ms)
+    if dist:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    h2d = y0.nbytes + (0 if F is None else F.nbytes) + (0 if rho is None else rho.nbytes)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        m, times, thr = oracle_cells_per_s(cfg, budget_s=15.0)
+        cpu = {"value": m / times[0], "unit": UNIT, "cores": thr, "kind": "oracle",
+               "sample": f"{m} stratified cells of the {cfg} workload (same recipe and seed), one pass"}
+
+    s = stats[-1]
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "cells_per_gpu": N, "n": n, "rtol": rtol,
+                           "atol": atol if np.isscalar(atol) else list(atol), "dt_CFD": dt,
+                           "mode": "per-cell", "parallelism": f"dp{world} (cells sharded, no collective)",
+                           "l2": "inputs larger than L2 (state %.2f GB per GPU); pristine field restored "
+                                 "untimed before each step" % (y0.nbytes / 1e9),
+                           "mechanism": mech},
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": {"value": N * world / (e2e_total / args.steps * 1e-3), "unit": UNIT,
+                        "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(y0.nbytes)},
+                "gpu_launches": args.steps * b.last_launch_count(),
+                "clocks": clk.summary(),
+                "stats": {k: s[k] for k in ("n_cells", "n_failed", "nst", "nfe", "nje", "nsetups", "nni", "netf",
+                                            "ncfn", "nst_max")},
+                "kernel_ms_per_step": kern_ms}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -200,6 +200,12 @@ int bdfb_eval_jac(bdfb_batch *b, double t, const double *y, const double *aux, d
 int bdfb_lu_factor_solve(int32_t n, int64_t N, double *M, int32_t *piv, double *b,
                          int32_t *info, void *stream);
 
+/* FP64 roofline probe: runs a DFMA-throughput kernel (all SMs, 8 independent
+ * chains per thread) for about `ms` milliseconds on `device` and returns the
+ * achieved FP64 TFLOP/s (2 flops per DFMA) in *tflops and the launch's SM
+ * count in *sms.  Used as the measured denominator of the FP64 roofline.   */
+int bdfb_probe_fp64(int32_t device, double ms, double *tflops, int32_t *sms);
+
 #ifdef __cplusplus
 }
 #endif

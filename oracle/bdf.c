@@ -70,6 +70,36 @@ typedef struct {
   orc_stats st;
 } cell;
 
+/*
+ * x^(1/L) for the step-size factors (reading R25): CVODE calls
+ * libm's power function with exponent 1.0/L; here the real L-th root is
+ * evaluated by a fixed sequence of IEEE operations (frexp/ldexp exponent
+ * split, Newton from above with a monotone stop), which the GPU path
+ * implements identically, so that step-size decisions are bit-reproducible
+ * across CPU and GPU.  It differs from the libm value by at most about
+ * |ln x| u (the rounding of 1.0/L) + 1.5 ulp.
+ * Pin: tests/test_oracle_primitives.py (exact powers, high-precision root).
+ */
+double orc_root(double x, int L)
+{
+  if (!(x > 0.0) || isinf(x)) return x > 0.0 ? x : 0.0;
+  if (L == 1) return x;
+  int e;
+  double m = frexp(x, &e);                    /* x = m 2^e, m in [0.5, 1) */
+  int k = (e >= 0) ? e / L : -((-e + L - 1) / L);
+  int r = e - L * k;                          /* 0 <= r < L */
+  double y = ldexp(m, r);
+  double t = 1.0 + (y - 1.0) / L;             /* >= y^(1/L) (Bernoulli) */
+  for (int it = 0; it < 100; ++it) {
+    double p = 1.0;
+    for (int j = 0; j < L - 1; ++j) p = p * t;
+    double tn = ((L - 1) * t + y / p) / L;
+    if (!(tn < t)) break;
+    t = tn;
+  }
+  return ldexp(t, k);
+}
+
 static double wrms(cell *c, const double *v) { return orc_wrms(c->n, v, c->ewt, c->o->group); }
 
 /* Eq. 3 weights: w_i = 1/(rtol |y_i| + atol_i) */
@@ -383,7 +413,7 @@ static void prepare_next(cell *c, double dsm)
     c->eta = 1.0;
     return;
   }
-  double etaq = 1.0 / (pow(BIAS2 * dsm, 1.0 / c->L) + ADDON);
+  double etaq = 1.0 / (orc_root(BIAS2 * dsm, c->L) + ADDON);
   if (c->qwait != 0) {
     c->eta = etaq;
     c->qprime = c->q;
@@ -394,7 +424,7 @@ static void prepare_next(cell *c, double dsm)
   double etaqm1 = 0.0, etaqp1 = 0.0;
   if (c->q > 1) {
     double ddn = wrms(c, c->zn[c->q]) * c->tq[1];
-    etaqm1 = 1.0 / (pow(BIAS1 * ddn, 1.0 / c->q) + ADDON);
+    etaqm1 = 1.0 / (orc_root(BIAS1 * ddn, c->q) + ADDON);
   }
   if (c->q != c->qmax && c->saved_tq5 != 0.0) {
     double hr = c->h / c->tau[2];
@@ -403,7 +433,7 @@ static void prepare_next(cell *c, double dsm)
     double cquot = (c->tq[5] / c->saved_tq5) * pw;
     for (int i = 0; i < n; ++i) c->tmp[i] = -cquot * c->zn[c->qmax][i] + c->acor[i];
     double dup = wrms(c, c->tmp) * c->tq[3];
-    etaqp1 = 1.0 / (pow(BIAS3 * dup, 1.0 / (c->L + 1)) + ADDON);
+    etaqp1 = 1.0 / (orc_root(BIAS3 * dup, c->L + 1) + ADDON);
   }
   double etam = fmax(etaqm1, fmax(etaq, etaqp1));
   if (etam < THRESH) {
@@ -528,7 +558,7 @@ static int step(cell *c, double tf)
     if (fabs(c->h) <= c->o->hmin * (1.0 + UROUND) || nef == MXNEF) return ORC_ERR_FAILURE;
     c->etamax = 1.0;
     if (nef <= MXNEF1) {
-      c->eta = 1.0 / (pow(BIAS2 * dsm, 1.0 / c->L) + ADDON);
+      c->eta = 1.0 / (orc_root(BIAS2 * dsm, c->L) + ADDON);
       c->eta = fmax(ETAMIN, fmax(c->eta, c->o->hmin / fabs(c->h)));
       if (nef >= SMALL_NEF) c->eta = fmin(c->eta, ETAMXF);
       rescale(c);

@@ -11,7 +11,7 @@
  * Required macros: RT, FN(name), EXPF, LOGF, REALPART.
  */
 
-static int FN(mech_rhs)(const orc_problem *p, const RT *y, RT *f)
+static int FN(mech_rhs)(const orc_problem *p, const RT *y, RT *f, double *scale)
 {
   const orc_mech *m = p->mech;
   const int K = m->K;
@@ -21,6 +21,7 @@ static int FN(mech_rhs)(const orc_problem *p, const RT *y, RT *f)
   const double rho = p->rho;
 
   RT C[ORC_NMAX], cpR[ORC_NMAX], hRT[ORC_NMAX], gRT[ORC_NMAX], wdot[ORC_NMAX];
+  double wabs[ORC_NMAX];          /* sum_r |nu_rk| (|fwd_r| + |rvs_r|): reading R19 scale */
   RT T = y[K];
   if (!(REALPART(T) > 0.0)) return 1;
   RT lnT = LOGF(T);
@@ -40,6 +41,7 @@ static int FN(mech_rhs)(const orc_problem *p, const RT *y, RT *f)
           + a[4] * T4 / 4.0 + a[6];
     gRT[k] = hRT[k] - sR;
     wdot[k] = 0.0;
+    wabs[k] = 0.0;
   }
 
   for (int r = 0; r < m->nr; ++r) {
@@ -78,6 +80,7 @@ static int FN(mech_rhs)(const orc_problem *p, const RT *y, RT *f)
       if (k >= 0) fwd = fwd * C[k];
     }
     RT q = fwd;
+    double qabs = REALPART(fwd) < 0 ? -REALPART(fwd) : REALPART(fwd);
     if (m->rev[r]) {
       RT sg = 0.0;
       int dnu = 0;
@@ -100,14 +103,15 @@ static int FN(mech_rhs)(const orc_problem *p, const RT *y, RT *f)
         if (k >= 0) rvs = rvs * C[k];
       }
       q = fwd - rvs;
+      qabs += REALPART(rvs) < 0 ? -REALPART(rvs) : REALPART(rvs);
     }
     for (int s = 0; s < 3; ++s) {
       int k = m->reac[3 * r + s];
-      if (k >= 0) wdot[k] = wdot[k] - q;
+      if (k >= 0) { wdot[k] = wdot[k] - q; wabs[k] += qabs; }
     }
     for (int s = 0; s < 3; ++s) {
       int k = m->prod[3 * r + s];
-      if (k >= 0) wdot[k] = wdot[k] + q;
+      if (k >= 0) { wdot[k] = wdot[k] + q; wabs[k] += qabs; }
     }
   }
 
@@ -120,6 +124,17 @@ static int FN(mech_rhs)(const orc_problem *p, const RT *y, RT *f)
   }
   /* dT/dt = -sum_k u_k wdot_k / (rho cv) + F_T */
   f[K] = -su / (rho * cv);
+  if (scale) {
+    double st = 0.0, cvr = REALPART(cv);
+    for (int k = 0; k < K; ++k) {
+      scale[k] = m->W[k] * wabs[k] / rho;
+      double u = (REALPART(hRT[k]) - 1.0) * Ru * REALPART(T);
+      st += (u < 0 ? -u : u) * wabs[k];
+    }
+    scale[K] = st / (rho * (cvr < 0 ? -cvr : cvr));
+    if (p->fext)
+      for (int k = 0; k <= K; ++k) scale[k] += p->fext[k] < 0 ? -p->fext[k] : p->fext[k];
+  }
   if (p->fext) for (int k = 0; k <= K; ++k) f[k] = f[k] + p->fext[k];
   return 0;
 }

@@ -134,6 +134,8 @@ void orc_lu_solve(int n, const double *LU, const int *piv, double *b);
 
 /* f = R(t,y) + f_ext.  Returns 0, or >0 for a recoverable RHS failure. */
 int orc_rhs(const orc_problem *p, double t, const double *y, double *f);
+/* S_i: the RHS with |.| on every term (reading R19 parity scale). */
+int orc_rhs_scale(const orc_problem *p, double t, const double *y, double *S);
 /* J = d f / d y (row-major).  Analytic (LINEAR, ROBERTSON) or complex-step
  * (MECH).  Returns 0 or >0 on failure.  KWH has no J (CVDiag only).       */
 int orc_jac(const orc_problem *p, double t, const double *y, double *J);
@@ -141,6 +143,9 @@ int orc_jac(const orc_problem *p, double t, const double *y, double *J);
 /* KWH pin entry: converged ionisation state for energy e:
  * out8 = [T, n_H0, n_H+, n_He0, n_He+, n_He++, n_e, g(x_e)]              */
 int orc_kwh_state(const orc_problem *p, double e, double *out8);
+
+/* x^(1/L) by the fixed IEEE sequence of reading R25 (step-size factors) */
+double orc_root(double x, int L);
 
 /* cvSetBDF + cvSetTqBDF for the coefficient pins: l[0..5], tq[1..5] */
 void orc_set_bdf(int q, double h, const double *tau /* [7], tau[1..6] */,

@@ -94,10 +94,14 @@ def lib():
             L.orc_lu_solve.argtypes = [C.c_int, dp, ip, dp]
             L.orc_rhs.restype = C.c_int
             L.orc_rhs.argtypes = [C.POINTER(Problem), C.c_double, dp, dp]
+            L.orc_rhs_scale.restype = C.c_int
+            L.orc_rhs_scale.argtypes = [C.POINTER(Problem), C.c_double, dp, dp]
             L.orc_jac.restype = C.c_int
             L.orc_jac.argtypes = [C.POINTER(Problem), C.c_double, dp, dp]
             L.orc_kwh_state.restype = C.c_int
             L.orc_kwh_state.argtypes = [C.POINTER(Problem), C.c_double, dp]
+            L.orc_root.restype = C.c_double
+            L.orc_root.argtypes = [C.c_double, C.c_int]
             L.orc_set_bdf.restype = None
             L.orc_set_bdf.argtypes = [C.c_int, C.c_double, dp, C.c_int, dp, dp]
             L.orc_integrate.restype = C.c_int
@@ -139,6 +143,10 @@ def lu_solve(LU, piv, b):
     b = np.array(b, dtype=np.float64, copy=True)
     lib().orc_lu_solve(LU.shape[0], _dp(LU), _ip(piv), _dp(b))
     return b
+
+
+def root(x, L):
+    return lib().orc_root(float(x), int(L))
 
 
 def set_bdf(q, h, tau, qwait):
@@ -286,6 +294,14 @@ def rhs(model, y, rho=1.0, fext=None, t=0.0):
     p = model.problem(rho, fext)
     r = lib().orc_rhs(C.byref(p), t, _dp(y), _dp(f))
     return f, r
+
+
+def rhs_scale(model, y, rho=1.0, fext=None, t=0.0):
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    S = np.zeros(model.n)
+    p = model.problem(rho, fext)
+    r = lib().orc_rhs_scale(C.byref(p), t, _dp(y), _dp(S))
+    return S, r
 
 
 def jac(model, y, rho=1.0, fext=None, t=0.0):

@@ -73,6 +73,30 @@ struct Vec {
   double v[R];
 };
 
+// x^(1/L) for the step-size factors, reading R25: the real L-th
+// root by a fixed IEEE operation sequence (exponent split with frexp/ldexp,
+// Newton from above with a monotone stop) instead of pow(x, 1.0/L), so that
+// CPU and GPU step-size decisions are bit-reproducible.  Compiled with
+// -fmad=false: no contraction changes the sequence.
+__device__ __forceinline__ double root_l(double x, int L) {
+  if (!(x > 0.0) || isinf(x)) return x > 0.0 ? x : 0.0;
+  if (L == 1) return x;
+  int e;
+  const double m = frexp(x, &e);
+  const int k = (e >= 0) ? e / L : -((-e + L - 1) / L);
+  const int r = e - L * k;
+  const double y = ldexp(m, r);
+  double t = 1.0 + (y - 1.0) / L;
+  for (int it = 0; it < 100; ++it) {
+    double p = 1.0;
+    for (int j = 0; j < L - 1; ++j) p = p * t;
+    const double tn = ((L - 1) * t + y / p) / L;
+    if (!(tn < t)) break;
+    t = tn;
+  }
+  return ldexp(t, k);
+}
+
 // select arr[idx] for a small register array without dynamic indexing
 template <int M>
 __device__ __forceinline__ double sel(const double (&a)[M], int idx) {
@@ -332,7 +356,7 @@ struct Integrator {
       s.eta = 1.0;
       return;
     }
-    const double etaq = 1.0 / (pow(BIAS2 * dsm, 1.0 / s.L) + ADDON);
+    const double etaq = 1.0 / (root_l(BIAS2 * dsm, s.L) + ADDON);
     if (s.qwait != 0) {
       s.eta = etaq;
       s.qprime = s.q;
@@ -345,7 +369,7 @@ struct Integrator {
       double zq[R];
       zn_get(s, s.q, zq);
       const double ddn = wrms(g, zq, s.ewt) * s.tq[1];
-      etaqm1 = 1.0 / (pow(BIAS1 * ddn, 1.0 / s.q) + ADDON);
+      etaqm1 = 1.0 / (root_l(BIAS1 * ddn, s.q) + ADDON);
     }
     if (s.q != o.qmax && s.saved_tq5 != 0.0) {
       const double hr = s.h / s.tau[2];
@@ -359,7 +383,7 @@ struct Integrator {
 #pragma unroll
       for (int r = 0; r < R; ++r) t[r] = -cquot * zq[r] + s.acor[r];
       const double dup = wrms(g, t, s.ewt) * s.tq[3];
-      etaqp1 = 1.0 / (pow(BIAS3 * dup, 1.0 / (s.L + 1)) + ADDON);
+      etaqp1 = 1.0 / (root_l(BIAS3 * dup, s.L + 1) + ADDON);
     }
     const double etam = fmax(etaqm1, fmax(etaq, etaqp1));
     if (etam < THRESH) {
@@ -854,7 +878,7 @@ struct Integrator {
           }
           s.etamax = 1.0;
           if (s.nef <= MXNEF1) {
-            s.eta = 1.0 / (pow(BIAS2 * dsm, 1.0 / s.L) + ADDON);
+            s.eta = 1.0 / (root_l(BIAS2 * dsm, s.L) + ADDON);
             s.eta = fmax(ETAMIN, fmax(s.eta, o.hmin / fabs(s.h)));
             if (s.nef >= SMALL_NEF) s.eta = fmin(s.eta, ETAMXF);
             rescale(s);

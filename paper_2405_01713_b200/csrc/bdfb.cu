@@ -512,3 +512,55 @@ extern "C" int bdfb_lu_factor_solve(int32_t n, int64_t N, double* M, int32_t* pi
   }
   return fail(nullptr, BDFB_EUNSUPPORTED, "n not instantiated (1-8,10,12,16,22,32)");
 }
+
+// ------------------------------------------------------------ FP64 probe
+__global__ void __launch_bounds__(256) fp64_probe_kernel(long long iters, double seed, double* out) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+         a7 = a0 + 7;
+  const double m = 0.999999999, c = 1e-9;
+  for (long long i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 1234.5678) out[0] = s;  // keep the chains alive
+}
+
+extern "C" int bdfb_probe_fp64(int32_t device, double ms, double* tflops, int32_t* sms) {
+  if (!tflops || !(ms > 0)) return fail(nullptr, BDFB_EINVAL, "bad probe arguments");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+  int nsm = 0, per = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fp64_probe_kernel, 256, 0);
+  const long long blocks = (long long)nsm * (per > 0 ? per : 1);
+  double* d = nullptr;
+  cudaMalloc(&d, sizeof(double));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  long long iters = 256;
+  double best = 0.0;
+  for (int pass = 0; pass < 8; ++pass) {
+    cudaEventRecord(a);
+    fp64_probe_kernel<<<(unsigned)blocks, 256>>>(iters, 1.0, d);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    const double flops = 2.0 * 8 * 16 * (double)iters * blocks * 256;
+    if (t > 0) best = fmax(best, flops / (t * 1e-3) / 1e12);
+    if (t < ms * 0.5) iters *= 2;
+  }
+  e = cudaGetLastError();
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "probe");
+  *tflops = best;
+  if (sms) *sms = nsm;
+  return BDFB_OK;
+}

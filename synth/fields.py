@@ -146,10 +146,31 @@ def fresh_state(mech):
     return Y, W, T_cold, T_u, rho_u
 
 
-def flame_field(mech, L, seed=None, cells=None, dt=1e-5, forcing=True):
-    """SURVEY §8(d).1 flame-field template: returns (y [n, M] YC, rho [M], F [n, M], c [M])."""
-    seed = config_seed(4 if mech.startswith("drm19") else 3) if seed is None else seed
+def flame_field(mech, L, seed=None, cells=None, dt=1e-5, forcing=True, threads=None, chunk=1 << 19):
+    """SURVEY §8(d).1 flame-field template: returns (y [n, M] YC, rho [M], F [n, M], c [M]).
+    Large requests are generated in cell chunks on a thread pool (values are per-cell pure
+    functions, so chunking does not change them)."""
     c_idx = np.arange(L ** 3) if cells is None else np.asarray(cells)
+    M = len(c_idx)
+    if M > chunk:
+        from concurrent.futures import ThreadPoolExecutor
+        K = len(fresh_state(mech)[0])
+        y = np.empty((K + 1, M))
+        F = np.empty((K + 1, M))
+        rho = np.empty(M)
+        prog = np.empty(M)
+        def work(s):
+            e = min(M, s + chunk)
+            y[:, s:e], rho[s:e], F[:, s:e], prog[s:e] = flame_field(mech, L, seed, c_idx[s:e], dt, forcing,
+                                                                    chunk=chunk)
+        with ThreadPoolExecutor(max_workers=threads or min(32, os.cpu_count() or 1)) as ex:
+            list(ex.map(work, range(0, M, chunk)))
+        return y, rho, F, prog
+    return _flame_chunk(mech, L, seed, c_idx, dt, forcing)
+
+
+def _flame_chunk(mech, L, seed, c_idx, dt, forcing):
+    seed = config_seed(4 if mech.startswith("drm19") else 3) if seed is None else seed
     M = len(c_idx)
     Yf, W, T_cold, T_u, rho_u = fresh_state(mech)
     K = len(Yf)

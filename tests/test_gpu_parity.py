@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on identical
+seeded inputs.
+
+Bars (written in each test): LU factor/solve bit-identical (integer pivots
+equal); RHS |f_gpu - f_orc| <= 1e-12 S_i (reading R19); Jacobian row-scaled
+<= 1e-12 vs the oracle's complex-step J; integrated end states
+|dy| <= 10 (rtol |y| + atol) per cell and component plus the conservation
+check on both sides."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2405_01713_b200 as P  # noqa: E402
+from synth import flame_field, nyx_field, robertson_field, uniform  # noqa: E402
+from synth.fields import stratified_sample  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+STAT_KEYS = ("nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn")
+MECH = {"h2": ("h2_lidryer", 10, 16), "drm19": ("drm19_class", 22, 32)}
+
+
+def cu(a):
+    return None if a is None else torch.tensor(np.ascontiguousarray(a), device=DEV)
+
+
+def end_state_check(yg, yo, rtol, atol, frac_min=0.0):
+    tol = 10.0 * (rtol * np.abs(yo) + atol)
+    err = np.abs(yg - yo)
+    ok = err <= tol
+    assert ok.all(), f"{(~ok.all(axis=0)).sum()} cells outside 10 tol; worst {np.max(err / tol):.3g}"
+
+
+def run_gpu(model, n, y0, t1, rtol, atol, rho=None, F=None, layout="YC", **kw):
+    N = y0.shape[1]
+    b = P.Batch(N, n, rtol, atol, **kw)
+    b.set_model(model)
+    cs = b.attach_cell_stats()
+    y = cu(y0 if layout == "YC" else y0.T)
+    b.integrate(0.0, t1, y, f_ext=cu(F if (F is None or layout == "YC") else F.T), aux=cu(rho), layout=layout)
+    st = b.stats()
+    yy = y.cpu().numpy()
+    return (yy if layout == "YC" else yy.T), {k: v.cpu().numpy() for k, v in cs.items()}, st
+
+
+# ------------------------------------------------------------------ LU
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 22, 32])
+def test_lu_bit_identical(oracle, n):
+    rng = np.random.default_rng(n)
+    N = 1000 + 37  # several warps + a ragged tail
+    M = rng.standard_normal((n, n, N)) * 10.0 ** rng.uniform(-3, 3, (n, 1, N))
+    b = rng.standard_normal((n, N))
+    if n > 1:
+        M[:, :, 5] = M[:, :, 6]
+        M[0, :, 5] = M[1, :, 5]              # exact duplicate rows: pivot ties
+        M[:, 0, 7] = 0.0                      # singular column
+    LU, piv, x, info = (t.cpu().numpy() for t in P.lu_factor_solve(cu(M), cu(b)))
+    for c in range(N):
+        LUo, pivo, io = oracle.lu_factor(M[:, :, c])
+        assert info[c] == io, c
+        if io:
+            continue
+        assert np.array_equal(piv[:, c], pivo), c
+        assert np.array_equal(LU[:, :, c], LUo), c
+        assert np.array_equal(x[:, c], oracle.lu_solve(LUo, pivo, b[:, c])), c
+
+
+# ------------------------------------------------------------------ RHS / J
+def model_states(name, count, seed=7):
+    if name == "robertson":
+        y = robertson_field(count, seed=seed)
+        y[1] = 4e-5 * uniform(seed, np.arange(count), 30)
+        return y, None, 0.1 * (uniform(seed, np.arange(count), 31) - 0.5)[None, :] * np.ones((3, 1))
+    if name == "nyx_kwh":
+        L = int(round(count ** (1 / 3)))
+        e, rho, fe = nyx_field(L)
+        return e, rho, fe
+    mech = MECH[name][0]
+    L = int(round(count ** (1 / 3)))
+    y, rho, F, prog = flame_field(mech, L)
+    return y, rho, F
+
+
+def oracle_model(oracle, name):
+    if name == "robertson":
+        return oracle.Model.robertson()
+    if name == "nyx_kwh":
+        return oracle.Model.nyx_kwh()
+    return oracle.Model.mechanism(MECH[name][0])
+
+
+@pytest.mark.parametrize("name", ["robertson", "nyx_kwh", "h2", "drm19"])
+def test_rhs_parity(oracle, name):
+    y, rho, F = model_states(name, 32768)
+    n, N = y.shape
+    b = P.Batch(N, n, 1e-6, 1e-10)
+    b.set_model(name)
+    f, st = P.eval_rhs(b, cu(y), f_ext=cu(F), aux=cu(rho))
+    f, st = f.cpu().numpy(), st.cpu().numpy()
+    m = oracle_model(oracle, name)
+    idx = np.arange(N) if N <= 4096 else np.sort(np.random.default_rng(1).choice(N, 4096, replace=False))
+    worst = 0.0
+    for c in idx:
+        r = rho[c] if rho is not None else 1.0
+        fo, ro = oracle.rhs(m, y[:, c], r, None if F is None else F[:, c])
+        S, _ = oracle.rhs_scale(m, y[:, c], r, None if F is None else F[:, c])
+        assert st[c] == ro
+        if ro:
+            continue
+        d = np.abs(f[:, c] - fo)
+        assert np.all(d <= 1e-12 * S + 1e-300), (c, d / (S + 1e-300))
+        worst = max(worst, float(np.max(d / (S + 1e-300))))
+    print(f"{name}: worst |df|/S = {worst:.3g}")
+
+
+@pytest.mark.parametrize("name", ["robertson", "h2", "drm19"])
+def test_jacobian_parity(oracle, name):
+    y, rho, F = model_states(name, 4096)
+    n, N = y.shape
+    b = P.Batch(N, n, 1e-6, 1e-10)
+    b.set_model(name)
+    J = P.eval_jac(b, cu(y), aux=cu(rho)).cpu().numpy()
+    m = oracle_model(oracle, name)
+    worst = 0.0
+    for c in range(0, N, 7):
+        Jo, r = oracle.jac(m, y[:, c], rho[c] if rho is not None else 1.0)
+        assert r == 0
+        scale = np.abs(Jo).max(axis=1, keepdims=True) + 1e-300
+        e = np.abs(J[:, :, c] - Jo) / scale
+        assert np.all(e <= 1e-12), (c, np.unravel_index(np.argmax(e), e.shape), e.max())
+        worst = max(worst, float(e.max()))
+    print(f"{name}: worst row-scaled |dJ| = {worst:.3g}")
+
+
+# ------------------------------------------------------------------ integration
+def test_robertson_c1_bit_identical(oracle):
+    """C1 (1024 cells, t in [0, 40], rtol 1e-4): RHS, J, LU, WRMS and step-size root all follow
+    the same IEEE operation sequence on both sides, so every cell is bit-identical."""
+    y0 = robertson_field(1024)
+    for rtol, atol in ((1e-4, (1e-8, 1e-14, 1e-6)), (1e-6, 1e-10)):
+        yg, sg, st = run_gpu("robertson", 3, y0, 40.0, rtol, atol)
+        yo, so = oracle.integrate_batch(oracle.Model.robertson(), y0, 0.0, 40.0, rtol, atol, threads=8)
+        end_state_check(yg, yo, rtol, np.broadcast_to(np.asarray(atol, dtype=float), (3,))[:, None])
+        assert np.abs(yg.sum(axis=0) - y0.sum(axis=0)).max() <= 1e-14
+        assert st["n_failed"] == 0 and st["n_cells"] == 1024
+        for k in STAT_KEYS:
+            assert np.array_equal(sg[k], so[k]), k
+        assert np.array_equal(yg, yo)
+
+
+def test_nyx_c2_parity(oracle):
+    e, rho, fe = nyx_field(16)
+    dt = 3e15
+    yg, sg, st = run_gpu("nyx_kwh", 1, e, dt, 1e-6, 1e-10, rho=rho, F=fe)
+    yo, so = oracle.integrate_batch(oracle.Model.nyx_kwh(), e, 0.0, dt, 1e-6, 1e-10, rho=rho, fext_yc=fe, threads=8)
+    assert np.array_equal(sg["status"], so["status"])
+    ok = sg["status"] == 0
+    end_state_check(yg[:, ok], yo[:, ok], 1e-6, 1e-10)
+    same = np.mean([all(sg[k][c] == so[k][c] for k in STAT_KEYS) for c in range(e.shape[1])])
+    print(f"C2: identical per-cell stats {same:.4f}")
+
+
+@pytest.mark.parametrize("name,dt", [("h2", 1e-5), ("h2", 1e-6), ("drm19", 1e-5), ("drm19", 1e-6)])
+def test_flame_parity(oracle, name, dt):
+    mech, n, G = MECH[name]
+    y0, rho, F, prog = flame_field(mech, 16, dt=dt)
+    yg, sg, st = run_gpu(name, n, y0, dt, 1e-6, 1e-10, rho=rho, F=F)
+    yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, dt, 1e-6, 1e-10, rho=rho, fext_yc=F,
+                                    group=G, threads=8)
+    assert st["n_failed"] == 0
+    end_state_check(yg, yo, 1e-6, 1e-10)
+    same = np.mean([all(sg[k][c] == so[k][c] for k in STAT_KEYS) for c in range(y0.shape[1])])
+    print(f"{name} dt={dt}: identical per-cell stats {same:.4f}")
+    assert same > 0.95
+
+
+def test_mass_conservation_both_sides(oracle):
+    """F_Y = 0 (only F_T forcing): sum_k Y_k is conserved to round-off on both sides."""
+    y0, rho, F, prog = flame_field("drm19_class", 8, dt=1e-5)
+    yg, _, _ = run_gpu("drm19", 22, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    yo, _ = oracle.integrate_batch(oracle.Model.mechanism("drm19_class"), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho,
+                                   fext_yc=F, group=32, threads=8)
+    s0 = y0[:-1].sum(axis=0)
+    assert np.abs(yg[:-1].sum(axis=0) - s0).max() <= 1e-13
+    assert np.abs(yo[:-1].sum(axis=0) - s0).max() <= 1e-13
+
+
+# ------------------------------------------------------------------ edge cases
+def test_edge_cases(oracle):
+    y0, rho, F, prog = flame_field("h2_lidryer", 4)        # 64 cells, 2 cells per warp (G=16)
+    y0 = y0[:, :61].copy()                                    # ragged tail
+    rho, F = rho[:61].copy(), F[:, :61].copy()
+    y0[0, 3] = np.nan                                         # non-finite input
+    F[5, 9] = np.inf
+    yg, sg, st = run_gpu("h2", 10, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    assert sg["status"][3] == 5 and sg["status"][9] == 5
+    assert np.isnan(yg[0, 3]) and np.array_equal(yg[:, 9], y0[:, 9])
+    ok = np.ones(61, bool)
+    ok[[3, 9]] = False
+    yo, so = oracle.integrate_batch(oracle.Model.mechanism("h2_lidryer"), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho,
+                                    fext_yc=F, group=16)
+    assert np.array_equal(so["status"], sg["status"])
+    end_state_check(yg[:, ok], yo[:, ok], 1e-6, 1e-10)
+    assert st["n_failed"] == 2
+    # too much work: mxstep = 3
+    yg2, sg2, st2 = run_gpu("h2", 10, y0[:, ok], 1e-5, 1e-6, 1e-10, rho=rho[ok], F=F[:, ok], mxstep=3)
+    assert np.all(sg2["status"] == 1) and np.all(sg2["t_reached"] < 1e-5) and np.all(sg2["nst"] == 3)
+    # CY layout == YC layout, bit for bit
+    ycy, _, _ = run_gpu("h2", 10, y0[:, ok], 1e-5, 1e-6, 1e-10, rho=rho[ok], F=F[:, ok], layout="CY")
+    assert np.array_equal(ycy, yg[:, ok])
+    # single cell
+    y1, s1, _ = run_gpu("robertson", 3, np.array([[1.0], [0.0], [0.0]]), 40.0, 1e-6, 1e-10)
+    yo1, _, _ = oracle.integrate(oracle.Model.robertson(), [1.0, 0.0, 0.0], 0.0, 40.0, 1e-6, 1e-10)
+    assert np.array_equal(y1[:, 0], yo1)
+
+
+def test_sharding_invariance_bitwise():
+    """Cells are independent: integrating any subset (what a rank does) gives bit-identical results."""
+    y0, rho, F, prog = flame_field("drm19_class", 8, dt=1e-5)
+    yall, _, _ = run_gpu("drm19", 22, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    for r in range(3):
+        sub = np.arange(r, y0.shape[1], 3)
+        ys, _, _ = run_gpu("drm19", 22, y0[:, sub], 1e-5, 1e-6, 1e-10, rho=rho[sub], F=F[:, sub])
+        assert np.array_equal(ys, yall[:, sub])
+
+
+def test_full_size_c3_sampled(oracle):
+    """C3 at its BASELINE size (64^3 cells), launch configuration as in bench.py; parity on a
+    stratified sample of cells the oracle integrates one by one."""
+    mech, n, G = MECH["h2"]
+    y0, rho, F, prog = flame_field(mech, 64, dt=1e-5)
+    yg, sg, st = run_gpu("h2", n, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    assert st["n_failed"] == 0 and st["n_cells"] == 64 ** 3
+    idx = stratified_sample(prog, 300)
+    yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho, fext_yc=F,
+                                    group=G, threads=8, cells=idx)
+    end_state_check(yg[:, idx], yo, 1e-6, 1e-10)
