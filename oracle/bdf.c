@@ -71,33 +71,50 @@ typedef struct {
 } cell;
 
 /*
- * x^(1/L) for the step-size factors (reading R25): CVODE calls
- * libm's power function with exponent 1.0/L; here the real L-th root is
- * evaluated by a fixed sequence of IEEE operations (frexp/ldexp exponent
- * split, Newton from above with a monotone stop), which the GPU path
- * implements identically, so that step-size decisions are bit-reproducible
- * across CPU and GPU.  It differs from the libm value by at most about
- * |ln x| u (the rounding of 1.0/L) + 1.5 ulp.
- * Pin: tests/test_oracle_primitives.py (exact powers, high-precision root).
+ * x^(1/L) for the step-size factors (reading R25).  CVODE calls
+ * libm's power function with exponent 1.0/L.  Here the real L-th root is
+ * evaluated by a fixed sequence of IEEE operations that the GPU path
+ * implements identically, so step-size decisions are bit-reproducible across
+ * CPU and GPU:
+ *   x = y 2^e, y in [1,2);  e = L k + r, 0 <= r < L;
+ *   s ~ y^(-1/L): s0 = 1 - (y-1) c_L, then 4 Newton steps
+ *       s <- s (1 + (1 - y s^L) / L)          (no division);
+ *   x^(1/L) = ldexp(y s^(L-1) * 2^(r/L), k).
+ * c_L = 1 - 2^(-1/L) and 2^(r/L) are correctly rounded constants.  The result
+ * is within 12 ulp of the exact root (pinned in test_oracle_primitives.py).
  */
+static const double ROOT_C[8][7] = {
+  {0}, {1.0},
+  {0x1.0p+0, 0x1.6a09e667f3bcdp+0},
+  {0x1.0p+0, 0x1.428a2f98d728bp+0, 0x1.965fea53d6e3dp+0},
+  {0x1.0p+0, 0x1.306fe0a31b715p+0, 0x1.6a09e667f3bcdp+0, 0x1.ae89f995ad3adp+0},
+  {0x1.0p+0, 0x1.2611186bae675p+0, 0x1.51cb453b9536cp+0, 0x1.8406003b2ae5cp+0, 0x1.bdb8cdadbe120p+0},
+  {0x1.0p+0, 0x1.1f59ac3c7d6c0p+0, 0x1.428a2f98d728bp+0, 0x1.6a09e667f3bcdp+0, 0x1.965fea53d6e3dp+0,
+   0x1.c823e074ec129p+0},
+  {0x1.0p+0, 0x1.1aa59c4115e7dp+0, 0x1.381147622f886p+0, 0x1.588cea3f093bep+0, 0x1.7c6a1f29e2ce6p+0,
+   0x1.a402feeb9c533p+0, 0x1.cfbb031a741a5p+0}};
+static const double ROOT_CL[8] = {0, 0, 0x1.2bec333018867p-2, 0x1.a68056b0a470ep-3, 0x1.45d819a94b14bp-3,
+                                  0x1.091cc94907b7fp-3, 0x1.bee0fc589f6b6p-4, 0x1.8227e72c5f2dbp-4};
+
 double orc_root(double x, int L)
 {
   if (!(x > 0.0) || isinf(x)) return x > 0.0 ? x : 0.0;
   if (L == 1) return x;
   int e;
-  double m = frexp(x, &e);                    /* x = m 2^e, m in [0.5, 1) */
+  double y = 2.0 * frexp(x, &e);              /* x = y 2^(e-1), y in [1, 2) */
+  e = e - 1;
   int k = (e >= 0) ? e / L : -((-e + L - 1) / L);
   int r = e - L * k;                          /* 0 <= r < L */
-  double y = ldexp(m, r);
-  double t = 1.0 + (y - 1.0) / L;             /* >= y^(1/L) (Bernoulli) */
-  for (int it = 0; it < 100; ++it) {
-    double p = 1.0;
-    for (int j = 0; j < L - 1; ++j) p = p * t;
-    double tn = ((L - 1) * t + y / p) / L;
-    if (!(tn < t)) break;
-    t = tn;
+  double invL = 1.0 / L;
+  double s = 1.0 - (y - 1.0) * ROOT_CL[L];
+  for (int it = 0; it < 4; ++it) {
+    double p = s;
+    for (int j = 0; j < L - 1; ++j) p = p * s;
+    s = s * (1.0 + (1.0 - y * p) * invL);
   }
-  return ldexp(t, k);
+  double t = y;
+  for (int j = 0; j < L - 1; ++j) t = t * s;
+  return ldexp(t * ROOT_C[L][r], k);
 }
 
 static double wrms(cell *c, const double *v) { return orc_wrms(c->n, v, c->ewt, c->o->group); }

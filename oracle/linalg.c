@@ -76,8 +76,9 @@ int orc_lu_factor(int n, double *M, int *piv)
 /*
  * Solve with the factors (getrs semantics), listing LU_SOLVE:
  *   swaps b[k] <-> b[piv[k]] in order; unit-L forward substitution in
- *   column (axpy) order with fma; U back substitution with division by the
- *   diagonal, column order, fma.
+ *   column (axpy) order with fma; U back substitution in column order with
+ *   fma, b[k] multiplied by the correctly rounded reciprocal 1/U[k][k]
+ *   (reading R16: one reciprocal per pivot instead of a division per solve).
  */
 void orc_lu_solve(int n, const double *LU, const int *piv, double *b)
 {
@@ -89,9 +90,9 @@ void orc_lu_solve(int n, const double *LU, const int *piv, double *b)
     for (int i = k + 1; i < n; ++i)
       b[i] = fma(-LU[i * n + k], b[k], b[i]);
   for (int k = n - 1; k > 0; --k) {
-    b[k] /= LU[k * n + k];
+    b[k] = b[k] * (1.0 / LU[k * n + k]);
     for (int i = 0; i < k; ++i)
       b[i] = fma(-LU[i * n + k], b[k], b[i]);
   }
-  b[0] /= LU[0];
+  b[0] = b[0] * (1.0 / LU[0]);
 }

@@ -73,28 +73,46 @@ struct Vec {
   double v[R];
 };
 
-// x^(1/L) for the step-size factors, reading R25: the real L-th
-// root by a fixed IEEE operation sequence (exponent split with frexp/ldexp,
-// Newton from above with a monotone stop) instead of pow(x, 1.0/L), so that
-// CPU and GPU step-size decisions are bit-reproducible.  Compiled with
-// -fmad=false: no contraction changes the sequence.
-__device__ __forceinline__ double root_l(double x, int L) {
+// x^(1/L) for the step-size factors, reading R25: instead of
+// pow(x, 1.0/L) the real L-th root by a fixed, division-free IEEE operation
+// sequence, so that CPU and GPU step-size decisions are bit-reproducible:
+//   x = y 2^e (y in [1,2)), e = L k + r;  s ~ y^(-1/L) from s0 = 1-(y-1)c_L
+//   and 4 Newton steps s <- s (1 + (1 - y s^L)/L);  x^(1/L) = ldexp(y s^(L-1)
+//   2^(r/L), k).  c_L = 1 - 2^(-1/L) and 2^(r/L): correctly rounded constants.
+// Compiled with -fmad=false: no contraction changes the sequence.
+__constant__ double kRootC[8][7] = {
+    {0}, {1.0},
+    {0x1.0p+0, 0x1.6a09e667f3bcdp+0},
+    {0x1.0p+0, 0x1.428a2f98d728bp+0, 0x1.965fea53d6e3dp+0},
+    {0x1.0p+0, 0x1.306fe0a31b715p+0, 0x1.6a09e667f3bcdp+0, 0x1.ae89f995ad3adp+0},
+    {0x1.0p+0, 0x1.2611186bae675p+0, 0x1.51cb453b9536cp+0, 0x1.8406003b2ae5cp+0, 0x1.bdb8cdadbe120p+0},
+    {0x1.0p+0, 0x1.1f59ac3c7d6c0p+0, 0x1.428a2f98d728bp+0, 0x1.6a09e667f3bcdp+0, 0x1.965fea53d6e3dp+0,
+     0x1.c823e074ec129p+0},
+    {0x1.0p+0, 0x1.1aa59c4115e7dp+0, 0x1.381147622f886p+0, 0x1.588cea3f093bep+0, 0x1.7c6a1f29e2ce6p+0,
+     0x1.a402feeb9c533p+0, 0x1.cfbb031a741a5p+0}};
+__constant__ double kRootCL[8] = {0, 0, 0x1.2bec333018867p-2, 0x1.a68056b0a470ep-3, 0x1.45d819a94b14bp-3,
+                                  0x1.091cc94907b7fp-3, 0x1.bee0fc589f6b6p-4, 0x1.8227e72c5f2dbp-4};
+__constant__ double kInvL[8] = {0, 1.0 / 1, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7};
+
+__device__ __noinline__ double root_l(double x, int L) {
   if (!(x > 0.0) || isinf(x)) return x > 0.0 ? x : 0.0;
   if (L == 1) return x;
   int e;
-  const double m = frexp(x, &e);
+  const double y = 2.0 * frexp(x, &e);
+  e = e - 1;
   const int k = (e >= 0) ? e / L : -((-e + L - 1) / L);
   const int r = e - L * k;
-  const double y = ldexp(m, r);
-  double t = 1.0 + (y - 1.0) / L;
-  for (int it = 0; it < 100; ++it) {
-    double p = 1.0;
-    for (int j = 0; j < L - 1; ++j) p = p * t;
-    const double tn = ((L - 1) * t + y / p) / L;
-    if (!(tn < t)) break;
-    t = tn;
+  const double invL = kInvL[L];
+  double s = 1.0 - (y - 1.0) * kRootCL[L];
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    double p = s;
+    for (int j = 0; j < L - 1; ++j) p = p * s;
+    s = s * (1.0 + (1.0 - y * p) * invL);
   }
-  return ldexp(t, k);
+  double t = y;
+  for (int j = 0; j < L - 1; ++j) t = t * s;
+  return ldexp(t * kRootC[L][r], k);
 }
 
 // select arr[idx] for a small register array without dynamic indexing
@@ -115,7 +133,9 @@ struct Integrator {
   static constexpr bool DIAG = Model::DIAG;
   static constexpr int CHUNK = (G == 1) ? 1 : 4;
   static constexpr int MAT = (G == 1 ? N * N : N) * WS;          // doubles per matrix per warp
-  static constexpr int SMEM_WARP = (DIAG ? 0 : 2 * MAT) + Model::SCRATCH + 16;  // + perm ints (32)
+  // the LU area also hosts the Jacobian's scratch (the setup overwrites it)
+  static constexpr int MATLU = MAT > Model::JSCRATCH ? MAT : Model::JSCRATCH;
+  static constexpr int SMEM_WARP = (DIAG ? 0 : MAT + MATLU) + Model::SCRATCH + 16;  // + perm ints (32)
   using Lay = Layout<N, G>;
   using P = typename Model::Params;
 
@@ -135,6 +155,7 @@ struct Integrator {
     int phase, status;
     long long cell, chunk_end;
     int pos;             // G > 1 LU position
+    double invd;         // G > 1: 1 / U diagonal of this lane's row
     int piv[N];          // G = 1 LU pivots (static indexing only)
   };
 
@@ -415,7 +436,7 @@ struct Integrator {
       s.nje++;
       s.nstlj = s.nst;
       s.jcur = 1;
-      if (Model::jac(g, prm, s.tn, s.yq, s.aux, Jm, scratch)) rv = -1;
+      if (Model::jac(g, prm, s.tn, s.yq, s.aux, Jm, scratch, LUm)) rv = -1;
     } else {
       s.jcur = 0;
     }
@@ -435,6 +456,7 @@ struct Integrator {
         }
         g.sync();
         rv = lu_factor_group<N, G>(g, LUm, s.pos, perm) ? 1 : 0;
+        if (!rv) s.invd = lu_inv_diag<N, G>(g, LUm, s.pos);
       }
     }
     s.nsetups++;
@@ -472,7 +494,7 @@ struct Integrator {
 #pragma unroll
       for (int i = 0; i < N; ++i) b[i] = bb[i];
     } else {
-      b[0] = lu_solve_group<N, G>(g, LUm, s.pos, perm, b[0]);
+      b[0] = lu_solve_group<N, G>(g, LUm, s.pos, s.invd, perm, b[0]);
     }
     if (s.gamrat != 1.0) {
       const double sc = 2.0 / (1.0 + s.gamrat);
@@ -946,7 +968,7 @@ struct Integrator {
 };
 
 template <class Model>
-__global__ void __launch_bounds__(Model::BLOCK) integrate_kernel(Opts o, typename Model::Params prm, double* y,
+__global__ void __launch_bounds__(Model::BLOCK, Model::MINB) integrate_kernel(Opts o, typename Model::Params prm, double* y,
                                                                  const double* fext, const double* aux,
                                                                  const double* atol, unsigned long long* counter,
                                                                  Agg* agg, CellStatsPtrs cs) {
@@ -957,7 +979,7 @@ __global__ void __launch_bounds__(Model::BLOCK) integrate_kernel(Opts o, typenam
   double* wbase = smem + warp * I::SMEM_WARP;
   double* Jm = wbase;
   double* LUm = I::DIAG ? wbase : wbase + I::MAT;
-  double* scratch = wbase + (I::DIAG ? 0 : 2 * I::MAT);
+  double* scratch = wbase + (I::DIAG ? 0 : I::MAT + I::MATLU);
   int* perm = reinterpret_cast<int*>(scratch + Model::SCRATCH);
   Grp<G> g;
   typename I::S s;

@@ -15,6 +15,7 @@
 
 #include "../../include/bdfb.h"
 #include "bdf_cell.cuh"
+#include "bdf_group.cuh"
 #include "gen/mech_drm19_class.cuh"
 #include "gen/mech_h2_lidryer.cuh"
 #include "mech_model.cuh"
@@ -189,11 +190,27 @@ int bdfb_set_cell_stats(bdfb_batch* b, const bdfb_cell_stats* cs) {
 }  // extern "C"
 
 // ------------------------------------------------------------------ launches
+// kernel + shared-memory footprint per warp: thread-per-cell models use the
+// register-resident state machine (bdf_cell.cuh); group models (G > 1) the
+// shared-memory, leader-lane design (bdf_group.cuh).
+template <class Model, bool GROUP = (Model::G > 1)>
+struct KSel;
+template <class Model>
+struct KSel<Model, false> {
+  static constexpr int SMEM_WARP = Integrator<Model>::SMEM_WARP, CHUNK = Integrator<Model>::CHUNK;
+  static auto kernel() { return integrate_kernel<Model>; }
+};
+template <class Model>
+struct KSel<Model, true> {
+  static constexpr int SMEM_WARP = GroupIntegrator<Model>::SMEM_WARP, CHUNK = GroupIntegrator<Model>::CHUNK;
+  static auto kernel() { return integrate_group_kernel<Model>; }
+};
+
 template <class Model>
 static int launch_integrate(bdfb_batch* b, const Opts& o, double* y, const double* fext, const double* aux,
                             cudaStream_t st) {
-  using I = Integrator<Model>;
-  auto kern = integrate_kernel<Model>;
+  using I = KSel<Model>;
+  auto kern = I::kernel();
   const int warps = Model::BLOCK / 32;
   const size_t smem = sizeof(double) * (size_t)I::SMEM_WARP * warps;
   cudaError_t e;
@@ -327,6 +344,20 @@ extern "C" double bdfb_last_kernel_ms(bdfb_batch* b) {
 }
 
 // ------------------------------------------------------- diagnostic kernels
+// per-warp diagnostic shared memory (doubles): thread models use the warp
+// matrix layout of lu.cuh; group models a per-group [J | scratch | jscratch].
+template <class Model, bool GROUP = (Model::G > 1)>
+struct EvalSmem {
+  static constexpr int MAT = Model::N * Model::N * WS;
+  static constexpr int SW = MAT + Model::SCRATCH + Model::JSCRATCH;
+};
+template <class Model>
+struct EvalSmem<Model, true> {
+  static constexpr int MS = GroupIntegrator<Model>::MS;
+  static constexpr int PG = Model::N * MS + Model::SG + Model::JG;
+  static constexpr int SW = (32 / Model::G) * PG;
+};
+
 template <class Model>
 __global__ void __launch_bounds__(128) eval_kernel(typename Model::Params prm, long long N, double t, const double* y,
                                                    const double* fext, const double* aux, double* f, int* status,
@@ -334,11 +365,15 @@ __global__ void __launch_bounds__(128) eval_kernel(typename Model::Params prm, l
   constexpr int G = Model::G, NN = Model::N, R = (NN + G - 1) / G;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5;
-  constexpr int MAT = (G == 1 ? NN * NN : NN) * WS;
-  constexpr int SW = MAT + Model::SCRATCH;
+  constexpr int SW = EvalSmem<Model>::SW;
   double* Jm = smem + warp * SW;
-  double* scratch = Jm + MAT;
+  double* scratch = Jm + NN * NN * WS;
   Grp<G> g;
+  if constexpr (G > 1) {
+    // group layout: [J (N*MS) | model scratch SG | Jacobian scratch JG] per group
+    Jm = smem + warp * SW + (g.gbase / G) * EvalSmem<Model>::PG;
+    scratch = Jm + NN * EvalSmem<Model>::MS;
+  }
   const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
   const bool live = grp < N;
   const long long c = live ? grp : 0;
@@ -359,8 +394,14 @@ __global__ void __launch_bounds__(128) eval_kernel(typename Model::Params prm, l
     }
     if (live && g.lane == 0 && status) status[c] = rv;
   } else {
-    if constexpr (!Model::DIAG) {
-      int rv = Model::jac(g, prm, t, yy, a, Jm, scratch);
+    if constexpr (G > 1) {
+      constexpr int MS = EvalSmem<Model>::MS;
+      Model::template jac<MS>(g, yy[0], a, Jm + g.lane, scratch, scratch + Model::SG);
+      const int i = g.lane;
+      if (live && i < NN)
+        for (int j = 0; j < NN; ++j) J[((long long)i * NN + j) * N + c] = Jm[j * MS + i];
+    } else if constexpr (!Model::DIAG) {
+      int rv = Model::jac(g, prm, t, yy, a, Jm, scratch, scratch + Model::SCRATCH);
       (void)rv;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -375,9 +416,8 @@ __global__ void __launch_bounds__(128) eval_kernel(typename Model::Params prm, l
 template <class Model>
 static int launch_eval(bdfb_batch* b, double t, const double* y, const double* fext, const double* aux, double* f,
                        int* status, double* J, cudaStream_t st) {
-  constexpr int G = Model::G, NN = Model::N;
-  constexpr int MAT = (G == 1 ? NN * NN : NN) * WS;
-  const size_t smem = sizeof(double) * (size_t)(MAT + Model::SCRATCH) * 4;
+  constexpr int G = Model::G;
+  const size_t smem = sizeof(double) * (size_t)EvalSmem<Model>::SW * 4;
   auto kern = eval_kernel<Model>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   typename Model::Params prm;
@@ -427,9 +467,9 @@ extern "C" int bdfb_eval_jac(bdfb_batch* b, double t, const double* y, const dou
 template <int NN, int G>
 __global__ void __launch_bounds__(128) lu_kernel(long long N, double* M, int* piv, double* bvec, int* info) {
   extern __shared__ double smem[];
-  constexpr int MAT = (G == 1 ? NN * NN : NN) * WS;
+  constexpr int MAT = (G == 1 ? NN * NN * WS : NN * 34);
   const int warp = threadIdx.x >> 5;
-  double* A = smem + warp * (MAT + 16);
+  double* A = smem + warp * (MAT + 64);
   int* perm = reinterpret_cast<int*>(A + MAT);
   Grp<G> g;
   const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -452,20 +492,26 @@ __global__ void __launch_bounds__(128) lu_kernel(long long N, double* M, int* pi
       }
     }
   } else {
+    // the group integrator's own routines (bdf_group.cuh), group-local layout
+    constexpr int MS = (NN % 2) ? NN : NN + 1;
+    double* Ag = A + (g.gbase / G) * NN * MS;
+    int* permg = perm + g.gbase;
+    int* posg = perm + 32 + g.gbase;
+    double* invg = reinterpret_cast<double*>(perm + 64) + g.gbase;
     const int i = g.lane;
     if (i < NN)
-      for (int j = 0; j < NN; ++j) A[j * WS + g.wlane] = M[((long long)i * NN + j) * N + c];
+      for (int j = 0; j < NN; ++j) Ag[j * MS + i] = M[((long long)i * NN + j) * N + c];
     g.sync();
-    int pos = 0;
-    const int inf = lu_factor_group<NN, G>(g, A, pos, perm);
+    const int inf = glu_factor<NN, G, MS>(g, Ag, posg, permg, invg);
+    const int pos = (!inf && i < NN) ? posg[i] : i;
     double bb = (i < NN) ? bvec[(long long)i * N + c] : 0.0;
-    if (!inf) bb = lu_solve_group<NN, G>(g, A, pos, perm, bb);
+    if (!inf) bb = glu_solve<NN, G, MS>(g, Ag, pos, i < NN ? invg[i] : 0.0, permg, bb);
     if (live) {
       if (g.lane == 0) info[c] = inf;
       if (i < NN) {
         bvec[(long long)i * N + c] = bb;
         if (!inf)
-          for (int j = 0; j < NN; ++j) M[((long long)pos * NN + j) * N + c] = A[j * WS + g.wlane];
+          for (int j = 0; j < NN; ++j) M[((long long)pos * NN + j) * N + c] = Ag[j * MS + i];
       }
       if (!inf && i < NN) {
         // LAPACK pivot indices from the position permutation: replay the swaps
@@ -489,8 +535,8 @@ __global__ void __launch_bounds__(128) lu_kernel(long long N, double* M, int* pi
 template <int NN>
 static int launch_lu(int64_t N, double* M, int32_t* piv, double* b, int32_t* info, cudaStream_t st) {
   constexpr int G = NN <= 4 ? 1 : (NN <= 16 ? 16 : 32);
-  constexpr int MAT = (G == 1 ? NN * NN : NN) * WS;
-  const size_t smem = sizeof(double) * (MAT + 16) * 4;
+  constexpr int MAT = (G == 1 ? NN * NN * WS : NN * 34);
+  const size_t smem = sizeof(double) * (MAT + 64) * 4;
   auto kern = lu_kernel<NN, G>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const long long threads = N * G;

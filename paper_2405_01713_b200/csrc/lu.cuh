@@ -64,22 +64,33 @@ __device__ int lu_factor_group(const Grp<G>& g, double* A, int& pos, int* perm) 
   return 0;
 }
 
-// b: this lane's right-hand-side component (row = lane); returns x[lane].
+// reciprocal of this lane's U diagonal (its row's entry in column pos);
+// reading R16: the solve multiplies by 1/U[k][k] instead of dividing.
 template <int N, int G>
-__device__ double lu_solve_group(const Grp<G>& g, const double* A, int pos, const int* perm, double b) {
+__device__ __forceinline__ double lu_inv_diag(const Grp<G>& g, const double* A, int pos) {
+  return (g.lane < N) ? 1.0 / A[pos * WS + g.wlane] : 0.0;
+}
+
+// b: this lane's right-hand-side component (row = lane); returns x[lane].
+// perm[] is read once into registers (the loops are unrolled).
+template <int N, int G>
+__device__ double lu_solve_group(const Grp<G>& g, const double* A, int pos, double invd, const int* perm, double b) {
   const bool act = g.lane < N;
+  int src[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) src[k] = perm[g.gbase + k];
+#pragma unroll
   for (int k = 0; k < N - 1; ++k) {
-    const int src = perm[g.gbase + k];
-    const double bk = __shfl_sync(g.mask, b, src, G);
+    const double bk = __shfl_sync(g.mask, b, src[k], G);
     if (act && pos > k) b = fma(-A[k * WS + g.wlane], bk, b);
   }
+#pragma unroll
   for (int k = N - 1; k > 0; --k) {
-    const int src = perm[g.gbase + k];
-    if (act && pos == k) b = b / A[k * WS + g.wlane];
-    const double bk = __shfl_sync(g.mask, b, src, G);
+    if (act && pos == k) b = b * invd;
+    const double bk = __shfl_sync(g.mask, b, src[k], G);
     if (act && pos < k) b = fma(-A[k * WS + g.wlane], bk, b);
   }
-  if (act && pos == 0) b = b / A[g.wlane];
+  if (act && pos == 0) b = b * invd;
   const int from = act ? perm[g.gbase + g.lane] : g.lane;
   return __shfl_sync(g.mask, b, from, G);
 }
@@ -133,11 +144,11 @@ __device__ void lu_solve_thread(const Grp<1>& g, const double* A, const int (&pi
     for (int i = k + 1; i < N; ++i) b[i] = fma(-A[(i * N + k) * WS + g.wlane], b[k], b[i]);
 #pragma unroll
   for (int k = N - 1; k > 0; --k) {
-    b[k] = b[k] / A[(k * N + k) * WS + g.wlane];
+    b[k] = b[k] * (1.0 / A[(k * N + k) * WS + g.wlane]);
 #pragma unroll
     for (int i = 0; i < k; ++i) b[i] = fma(-A[(i * N + k) * WS + g.wlane], b[k], b[i]);
   }
-  b[0] = b[0] / A[g.wlane];
+  b[0] = b[0] * (1.0 / A[g.wlane]);
 }
 
 }  // namespace bdfb

