@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libbdfb.so")
+LIB_PATH = os.environ.get("BDFB_LIB") or os.path.join(PKG, "libbdfb.so")   # BDFB_LIB: experiments only
 
 MODEL_LINEAR, MODEL_ROBERTSON, MODEL_NYX_KWH, MODEL_MECH_H2, MODEL_MECH_DRM19 = 0, 1, 2, 3, 4
 LAYOUT_YC, LAYOUT_CY = 0, 1

@@ -107,11 +107,15 @@ __device__ __noinline__ double root_l(double x, int L) {
 #pragma unroll
   for (int it = 0; it < 4; ++it) {
     double p = s;
-    for (int j = 0; j < L - 1; ++j) p = p * s;
+#pragma unroll
+    for (int j = 0; j < 6; ++j)
+      if (j < L - 1) p = p * s;
     s = s * (1.0 + (1.0 - y * p) * invL);
   }
   double t = y;
-  for (int j = 0; j < L - 1; ++j) t = t * s;
+#pragma unroll
+  for (int j = 0; j < 6; ++j)
+    if (j < L - 1) t = t * s;
   return ldexp(t * kRootC[L][r], k);
 }
 

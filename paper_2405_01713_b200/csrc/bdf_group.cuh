@@ -26,11 +26,16 @@ namespace bdfb {
 // Matrix of a group: element (row = lane i, column j) at A[j * MS + i].
 // Rows never move between lanes; each lane tracks its LAPACK position so the
 // pivots and factors are bit-identical to the listing's LU_FACTOR (R16).
+//
+// The update reads the pivot row from shared memory (broadcast) and updates
+// this lane's row in place (a register-resident variant measured 35% slower:
+// its out-of-line call forces the caller's live registers to be saved).
 template <int N, int G, int MS>
 __device__ __noinline__ int glu_factor(const Grp<G> g, double* A, int* posv, int* perm, double* invd) {
   const bool act = g.lane < N;
   int pos = g.lane;
   for (int k = 0; k < N; ++k) {
+#ifdef BDFB_LU_BFLY
     double a = (act && pos >= k) ? fabs(A[k * MS + g.lane]) : -1.0;
     int key = (pos << 5) | g.lane;
 #pragma unroll
@@ -40,6 +45,20 @@ __device__ __noinline__ int glu_factor(const Grp<G> g, double* A, int* posv, int
       if (oa > a || (oa == a && ok < key)) { a = oa; key = ok; }
     }
     const int p = key >> 5, pl = key & 31;
+#else
+    // |a| >= 0 orders like its IEEE bit pattern: first index of max |a| by
+    // three warp reductions (max high word, max low word among those, min
+    // position among the ties)
+    const bool cand = act && pos >= k;
+    const unsigned long long bits =
+        cand ? (unsigned long long)__double_as_longlong(fabs(A[k * MS + g.lane])) : 0ull;
+    const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+    const unsigned mhi = __reduce_max_sync(g.mask, hi);
+    const unsigned mlo = __reduce_max_sync(g.mask, (cand && hi == mhi) ? lo : 0u);
+    const bool top = cand && hi == mhi && lo == mlo;
+    const unsigned key = __reduce_min_sync(g.mask, top ? (unsigned)((pos << 5) | g.lane) : 0xffffffffu);
+    const int p = (int)(key >> 5), pl = (int)(key & 31u);
+#endif
     const double pv = A[k * MS + pl];
     if (pv == 0.0) { g.sync(); return k + 1; }
     if (g.lane == pl) pos = k;
@@ -63,16 +82,20 @@ __device__ __noinline__ int glu_factor(const Grp<G> g, double* A, int* posv, int
 
 // x = M^{-1} b for this lane's component (row = lane).  Reciprocal diagonal
 // (reading R16), axpy-ordered substitutions with fma.
+#ifndef BDFB_SOLVE_UNROLL
+#define BDFB_SOLVE_UNROLL 2
+#endif
+constexpr int kSolveUnroll = BDFB_SOLVE_UNROLL;
 template <int N, int G, int MS>
 __device__ __forceinline__ double glu_solve(const Grp<G>& g, const double* A, int pos, double invd,
                                             const int* perm, double b) {
   const bool act = g.lane < N;
-#pragma unroll 2
+#pragma unroll kSolveUnroll
   for (int k = 0; k < N - 1; ++k) {
     const double bk = __shfl_sync(g.mask, b, perm[k], G);
     if (act && pos > k) b = fma(-A[k * MS + g.lane], bk, b);
   }
-#pragma unroll 2
+#pragma unroll kSolveUnroll
   for (int k = N - 1; k > 0; --k) {
     if (act && pos == k) b = b * invd;
     const double bk = __shfl_sync(g.mask, b, perm[k], G);
@@ -896,7 +919,13 @@ __global__ void __launch_bounds__(Model::BLOCK, Model::MINB)
   bool live = true;
   for (;;) {
     if (live) live = I::advance(g, so, prm, c, rv, fr, y, fext, aux, counter, acc, cs);
+#ifndef BDFB_NO_BLOCK_SYNC
+    // keep the block's warps phase-aligned so the RHS code is fetched once for
+    // all of them (the kernel is instruction-fetch bound; +14% measured)
+    if (!__syncthreads_or(live)) break;
+#else
     if (!__any_sync(0xffffffffu, live)) break;
+#endif
     if (live) {
       double yq[1] = {I::V(c, g, I::V_YQ)}, f[1];
       rv = Model::rhs(g, prm, c.s->treq, yq, f, c.s->aux, c.sc);

@@ -31,8 +31,14 @@ template <class T>
 struct ModelMech {
   static constexpr int K = T::K, N = T::N, G = T::G, NR = T::NR, NTB = T::NTB, ELL = T::ELL;
   static constexpr bool DIAG = false;
-  static constexpr int BLOCK = 128;
-  static constexpr int MINB = 3;                        // target resident blocks per SM
+#ifndef BDFB_MECH_BLOCK
+#define BDFB_MECH_BLOCK 128
+#endif
+#ifndef BDFB_MECH_MINB
+#define BDFB_MECH_MINB 3
+#endif
+  static constexpr int BLOCK = BDFB_MECH_BLOCK;
+  static constexpr int MINB = BDFB_MECH_MINB;           // target resident blocks per SM
   static constexpr int GPW = 32 / G;                    // groups per warp
   static constexpr int ROUNDS = (NR + G - 1) / G;
   // shared scratch per group (doubles); q[NR] is a zero slot for ELL padding
@@ -81,7 +87,7 @@ struct ModelMech {
   // phase 2: rates of progress (and partial derivatives into js if DERIV)
   template <bool DERIV>
   __device__ static void reactions(const Grp<G>& g, double* sc, double* js, double Tt, double lnT, double invT) {
-    const double cRT = RU * Tt / PATM;
+    const double cRT = RU * Tt / PATM, icRT = PATM / (RU * Tt);
 #pragma unroll 1
     for (int rr = 0; rr < ROUNDS; ++rr) {
       const int r = rr * G + g.lane;
@@ -102,8 +108,7 @@ struct ModelMech {
           const double er = sc[O_EG + i0] * (i1 >= 0 ? sc[O_EG + i1] : 1.0) * (i2 >= 0 ? sc[O_EG + i2] : 1.0);
           const double ep = sc[O_EG + j0] * (j1 >= 0 ? sc[O_EG + j1] : 1.0) * (j2 >= 0 ? sc[O_EG + j2] : 1.0);
           const int dn = T::dnu()[r];
-          const double cf = dn == 0 ? 1.0 : (dn > 0 ? (dn == 1 ? cRT : cRT * cRT) : (dn == -1 ? 1.0 / cRT
-                                                                                        : 1.0 / (cRT * cRT)));
+          const double cf = dn == 0 ? 1.0 : (dn == 1 ? cRT : (dn == -1 ? icRT : (dn > 0 ? cRT * cRT : icRT * icRT)));
           invKc = er / ep * cf;
           if (DERIV) {
             double hs = sc[O_H + j0] - sc[O_H + i0];
@@ -115,7 +120,12 @@ struct ModelMech {
           }
         }
         const double b = T::beta()[r], ea = T::EaR()[r];
+        // constant-rate reactions (beta = Ea = 0) are grouped into whole rounds by the codegen
+#ifdef BDFB_NO_KCONST
         const double kinf = exp(fma(b, lnT, T::lnA()[r]) - ea * invT);
+#else
+        const double kinf = T::kconst()[r] ? T::Aconst()[r] : exp(fma(b, lnT, T::lnA()[r]) - ea * invT);
+#endif
         const double net = fma(-Cr, invKc, Cf);
         double k = kinf, M = 1.0, dkdT = 0.0, dkdM = 0.0;
         if (DERIV) dkdT = kinf * (b + ea * invT) * invT;
@@ -136,10 +146,11 @@ struct ModelMech {
             const double Pr1 = 1.0 / (1.0 + Pr);
             double F = 1.0, dlFdlPr = 0.0, dFdT = 0.0;
             if (ty == 3) {
-              const double a = T::troe_a()[r], T3 = T::troe_T3()[r], T1 = T::troe_T1()[r];
-              const double e3 = exp(-Tt / T3), e1 = exp(-Tt / T1);
+              const double a = T::troe_a()[r], iT3 = T::troe_iT3()[r], iT1 = T::troe_iT1()[r];
+              const double e3 = exp(-Tt * iT3), e1 = exp(-Tt * iT1);
               double Fc = (1.0 - a) * e3 + a * e1;
-              double dFc = -(1.0 - a) / T3 * e3 - a / T1 * e1;
+              double dFc = 0.0;
+              if (DERIV) dFc = -(1.0 - a) * iT3 * e3 - a * iT1 * e1;
               if (T::troe_has_t2()[r]) {
                 const double T2 = T::troe_T2()[r];
                 const double e2 = exp(-T2 * invT);
