@@ -53,19 +53,19 @@ TRANSC_FLOPS = 20               # FP64 flops charged per exp/log (DESIGN.md "roo
 
 
 # ------------------------------------------------------------------ inputs
-def make_inputs(cfg, rank=0, cells_per_rank=None):
+def make_inputs(cfg, rank=0, cells_per_rank=None, world=1):
+    """This rank's slab of the seeded field (paper_2405_01713_b200.parallel.shard)."""
+    from paper_2405_01713_b200.parallel import shard
     from synth import flame_field, nyx_field, robertson_field
     model, mech, n, L, dt, rtol, atol, _ = CONFIGS[cfg]
+    N = cells_per_rank or (1024 if cfg == "C1" else L ** 3)
+    cells = np.arange(*shard(rank, world, N))
     if cfg == "C1":
-        N = cells_per_rank or 1024
-        y = robertson_field(N, cells=np.arange(rank * N, (rank + 1) * N))
-        return y, None, None, np.arange(N)
+        return robertson_field(N * world, cells=cells), None, None, np.arange(N)
     if cfg == "C2":
-        N = cells_per_rank or L ** 3
-        e, rho, fe = nyx_field(L, cells=np.arange(rank * N, (rank + 1) * N), dt=dt)
+        e, rho, fe = nyx_field(L, cells=cells, dt=dt)
         return e, rho, fe, None
-    N = cells_per_rank or L ** 3
-    y, rho, F, prog = flame_field(mech, L, cells=np.arange(rank * N, (rank + 1) * N), dt=dt)
+    y, rho, F, prog = flame_field(mech, L, cells=cells, dt=dt)
     return y, rho, F, prog
 
 
@@ -86,6 +86,17 @@ def flop_model(cfg, st):
     att = st["nst"] + st["netf"] + st["ncfn"]
     return (st["nfe"] * f_rhs + st["nje"] * f_jac + st["nsetups"] * f_lu + st["nni"] * (f_sol + 9 * n) +
             att * (6 * n + 20 * n + 60) + st["nst"] * (8 * n + 3 * n + 80))
+
+
+def traffic_per_launch(cfg, cells):
+    """DRAM bytes (read + write) per launch, scaled per cell from the committed ncu --set full capture
+    (profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of one capture / its cells)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            t = json.load(f)[cfg]
+        return t["dram_bytes_per_cell"] * cells
+    except Exception:
+        return None
 
 
 # ------------------------------------------------------------------ clocks
@@ -191,17 +202,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2405_01713_b200 import parallel as PL
+    rank, world, local = PL.env_rank()
     cfg = args.config
     model, mech, n, L, dt, rtol, atol, desc = CONFIGS[cfg]
 
     if args.impl == "reference":
         if rank != 0:
             return
-        for _ in range(0):
-            pass
         m, times, thr = oracle_cells_per_s(cfg, budget_s=max(5.0, 60.0 / max(args.steps, 1)), steps=args.warmup +
                                            args.steps)
         times = times[args.warmup:] or times
@@ -227,7 +235,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    y0, rho, F, prog = make_inputs(cfg, rank, args.cells or None)
+    y0, rho, F, prog = make_inputs(cfg, rank, args.cells or None, world)
     N = y0.shape[1]
     b = P.Batch(N, n, rtol, atol, device=local)
     b.set_model(model)
@@ -261,19 +269,15 @@ def main():
             kern_ms.append(b.last_kernel_ms())
             stats.append(b.stats())
     step_ms = [a.elapsed_time(z) for a, z in ev]
-    total_ms = sum(step_ms)
-    if dist:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = PL.max_over_ranks(sum(step_ms), dist, dev)
     ms_per_step = total_ms / args.steps
-    value = N * world / (ms_per_step * 1e-3)
+    value = PL.job_throughput(N, world, ms_per_step * 1e-3)
 
     # roofline: algorithmic FP64 flops of the integrator kernel / its event-timed duration
     flops = [flop_model(cfg, s) for s in stats]
     achieved = statistics.mean(f / (k * 1e-3) for f, k in zip(flops, kern_ms)) / 1e12
     peak = SMS * FP64_FMA_PER_SM_CLK * 2 * SM_MAX_MHZ * 1e6 / 1e12
-    probe = C_double = None
+    probe = None
     try:
         import ctypes as C
         tf, sm = C.c_double(), C.c_int32()
@@ -282,7 +286,8 @@ def main():
     except Exception:
         pass
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "integrate_kernel<ModelMech<%s>>" % (mech or model),
+            "traffic": traffic_per_launch(cfg, N),
+            "kernel": ("integrate_group_kernel<ModelMech<%s>>" % mech) if mech else "integrate_kernel<%s>" % model,
             "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
             "fp64_probe_tflops": probe, "kernel_ms": statistics.mean(kern_ms),
             "flops_per_launch": statistics.mean(flops)}
@@ -306,11 +311,7 @@ def main():
         z.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(a.elapsed_time(z))
-    e2e_total = sum(e2e_ms)
-    if dist:
-        t = torch.tensor([e2e_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
+    e2e_total = PL.max_over_ranks(sum(e2e_ms), dist, dev)
     h2d = y0.nbytes + (0 if F is None else F.nbytes) + (0 if rho is None else rho.nbytes)
 
     cpu = None
@@ -319,7 +320,7 @@ def main():
         cpu = {"value": m / times[0], "unit": UNIT, "cores": thr, "kind": "oracle",
                "sample": f"{m} stratified cells of the {cfg} workload (same recipe and seed), one pass"}
 
-    s = stats[-1]
+    s = PL.reduce_stats(stats[-1], dist, dev)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",

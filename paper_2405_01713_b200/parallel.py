@@ -1,0 +1,58 @@
+"""Multi-GPU plumbing for the per-cell path (one process per GPU).
+
+Cells are independent, so ranks integrate disjoint slabs with
+no collective on the data path (weak scaling).  The only communication is
+host-side plumbing over torch.distributed: a barrier around the timed region,
+the max over ranks of the timed duration, and the sum of the aggregate
+integrator statistics.  (The global-norm mode's WRMS allreduce is the one
+collective that belongs to the method; it is not part of this module.)
+"""
+from __future__ import annotations
+
+import os
+
+STAT_SUM = ("n_cells", "n_failed", "nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn")
+STAT_MAX = ("nst_max", "nfe_max")
+
+
+def env_rank():
+    """(rank, world_size, local_rank) from the torchrun environment (defaults: single process)."""
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def shard(rank: int, world: int, cells_per_rank: int):
+    """Global cell indices [start, stop) of `rank`'s slab (weak scaling: every rank
+    owns cells_per_rank cells of one seeded field of world * cells_per_rank cells)."""
+    if not (0 <= rank < world) or cells_per_rank < 1:
+        raise ValueError("bad shard request")
+    return rank * cells_per_rank, (rank + 1) * cells_per_rank
+
+
+def max_over_ranks(value: float, dist=None, device=None) -> float:
+    """Max of a per-rank scalar (timed durations are reported as the slowest rank)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_stats(stats: dict, dist=None, device=None) -> dict:
+    """Whole-job aggregate of bdfb_get_stats dictionaries (sums and maxima)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return dict(stats)
+    import torch
+    s = torch.tensor([float(stats[k]) for k in STAT_SUM], dtype=torch.float64, device=device)
+    m = torch.tensor([float(stats[k]) for k in STAT_MAX], dtype=torch.float64, device=device)
+    dist.all_reduce(s, op=dist.ReduceOp.SUM)
+    dist.all_reduce(m, op=dist.ReduceOp.MAX)
+    out = {k: int(v) for k, v in zip(STAT_SUM, s.tolist())}
+    out.update({k: int(v) for k, v in zip(STAT_MAX, m.tolist())})
+    return out
+
+
+def job_throughput(cells_per_rank: int, world: int, max_seconds_per_step: float) -> float:
+    """Whole-job cells/s: all ranks' cells over the slowest rank's time."""
+    return cells_per_rank * world / max_seconds_per_step
