@@ -15,6 +15,7 @@
  */
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 #include "oracle.h"
 
@@ -52,15 +53,33 @@ enum { FIRST_CALL, PREV_CONV_FAIL, PREV_ERR_FAIL };
 enum { CF_NONE, CF_BAD_J, CF_OTHER };
 enum { NLS_OK = 0, NLS_RECOVERABLE = 1, NLS_RHS_UNREC = 2 };
 
+/* storage of one cell (per-cell mode) */
+typedef struct {
+  double zn[ORC_QMAX + 1][ORC_NMAX];
+  double ewt[ORC_NMAX], acor[ORC_NMAX], y[ORC_NMAX], ftemp[ORC_NMAX], tmp[ORC_NMAX];
+  double ycor[ORC_NMAX], G[ORC_NMAX];
+  double J[ORC_NMAX * ORC_NMAX], M[ORC_NMAX * ORC_NMAX];
+  int piv[ORC_NMAX];
+  double Minv[ORC_NMAX];
+} cellbuf;
+
+/* The integrator state.  Per-cell mode: one cell, nt = n.  Global-norm mode
+ * (listing "Global-norm variant"; reading R14): the ncell cells of a
+ * batch form ONE system of nt = n*ncell components (cell-major inside the
+ * oracle), with one h, q and history; J is block diagonal (one n x n LU per
+ * cell); every norm is batch-wide.                                          */
 typedef struct {
   const orc_problem *p;
   const orc_opts *o;
-  int n, qmax;
-  double zn[ORC_QMAX + 1][ORC_NMAX];
-  double ewt[ORC_NMAX], acor[ORC_NMAX], y[ORC_NMAX], ftemp[ORC_NMAX], tmp[ORC_NMAX];
-  double J[ORC_NMAX * ORC_NMAX], M[ORC_NMAX * ORC_NMAX];
-  int piv[ORC_NMAX];
-  double Minv[ORC_NMAX];           /* CVDiag */
+  int n, qmax, global;
+  long ncell, nt;
+  const double *rho_all;           /* global: [ncell] */
+  const double *fext_all;          /* global: [ncell][n] (cell-major) or NULL */
+  double *zn[ORC_QMAX + 1];
+  double *ewt, *acor, *y, *ftemp, *tmp, *ycor, *G;
+  double *J, *M;                   /* [ncell][n][n] */
+  int *piv;                        /* [ncell][n] */
+  double *Minv;                    /* CVDiag */
   double gammasv;                  /* CVDiag */
   double tn, h, hscale, hprime, eta, etamax;
   double tau[ORC_QMAX + 2], l[ORC_QMAX + 1], tq[6];
@@ -117,18 +136,43 @@ double orc_root(double x, int L)
   return ldexp(t * ROOT_C[L][r], k);
 }
 
-static double wrms(cell *c, const double *v) { return orc_wrms(c->n, v, c->ewt, c->o->group); }
+/* WRMS norm (Eq. 3).  Global mode: N = nt (reading R14) and the batch sum is
+ * formed in a specified order (reading R15): per-cell sums in the group order,
+ * accumulated sequentially over blocks of ORC_GBLK consecutive cells, block
+ * partials accumulated sequentially.                                       */
+static double wrms(cell *c, const double *v)
+{
+  if (!c->global) return orc_wrms(c->n, v, c->ewt, c->o->group);
+  double S = 0.0;
+  for (long b = 0; b < c->ncell; b += ORC_GBLK) {
+    double P = 0.0;
+    long e = b + ORC_GBLK < c->ncell ? b + ORC_GBLK : c->ncell;
+    for (long k = b; k < e; ++k) P = P + orc_wrms_sum(c->n, v + k * c->n, c->ewt + k * c->n, c->o->group);
+    S = S + P;
+  }
+  return sqrt(S / (double)c->nt);
+}
 
 /* Eq. 3 weights: w_i = 1/(rtol |y_i| + atol_i) */
 static void set_ewt(cell *c, const double *y)
 {
-  for (int i = 0; i < c->n; ++i) c->ewt[i] = 1.0 / (c->o->rtol * fabs(y[i]) + c->o->atol[i]);
+  for (long i = 0; i < c->nt; ++i) c->ewt[i] = 1.0 / (c->o->rtol * fabs(y[i]) + c->o->atol[i % c->n]);
 }
 
 static int f_eval(cell *c, double t, const double *y, double *f)
 {
   c->st.nfe++;
-  return orc_rhs(c->p, t, y, f);
+  if (!c->global) return orc_rhs(c->p, t, y, f);
+  int rv = 0;                      /* any cell's failure is the batch's (R18) */
+  for (long k = 0; k < c->ncell; ++k) {
+    orc_problem q = *c->p;
+    q.rho = c->rho_all ? c->rho_all[k] : q.rho;
+    q.fext = c->fext_all ? c->fext_all + k * c->n : NULL;
+    int r = orc_rhs(&q, t, y + k * c->n, f + k * c->n);
+    if (r < 0) return r;
+    if (r > 0) rv = r;
+  }
+  return rv;
 }
 
 /* RESCALE: zn[j] *= eta^j; h = hscale*eta; hscale = h (cvRescale) */
@@ -136,7 +180,7 @@ static void rescale(cell *c)
 {
   double r = c->eta;
   for (int j = 1; j <= c->q; ++j) {
-    for (int i = 0; i < c->n; ++i) c->zn[j][i] = r * c->zn[j][i];
+    for (long i = 0; i < c->nt; ++i) c->zn[j][i] = r * c->zn[j][i];
     r = r * c->eta;
   }
   c->h = c->hscale * c->eta;
@@ -150,7 +194,7 @@ static void predict(cell *c, double tf)
   if ((c->tn - tf) * c->h > 0.0) c->tn = tf;          /* never pass tf (R11) */
   for (int k = 1; k <= c->q; ++k)
     for (int j = c->q; j >= k; --j)
-      for (int i = 0; i < c->n; ++i) c->zn[j - 1][i] = c->zn[j - 1][i] + c->zn[j][i];
+      for (long i = 0; i < c->nt; ++i) c->zn[j - 1][i] = c->zn[j - 1][i] + c->zn[j][i];
 }
 
 /* RESTORE: undo PREDICT (cvRestore) */
@@ -159,7 +203,7 @@ static void restore(cell *c, double saved_t)
   c->tn = saved_t;
   for (int k = 1; k <= c->q; ++k)
     for (int j = c->q; j >= k; --j)
-      for (int i = 0; i < c->n; ++i) c->zn[j - 1][i] = c->zn[j - 1][i] - c->zn[j][i];
+      for (long i = 0; i < c->nt; ++i) c->zn[j - 1][i] = c->zn[j - 1][i] - c->zn[j][i];
 }
 
 /* SET_BDF: cvSetBDF + cvSetTqBDF (listing) */
@@ -227,9 +271,9 @@ static void increase_bdf(cell *c)
   }
   double A1 = (-alpha0 - alpha1) / prod;
   int Lq = c->q + 1;
-  for (int i = 0; i < c->n; ++i) c->zn[Lq][i] = A1 * c->zn[c->qmax][i];
+  for (long i = 0; i < c->nt; ++i) c->zn[Lq][i] = A1 * c->zn[c->qmax][i];
   for (int j = 2; j <= c->q; ++j)
-    for (int i = 0; i < c->n; ++i) c->zn[j][i] = l[j] * c->zn[Lq][i] + c->zn[j][i];
+    for (long i = 0; i < c->nt; ++i) c->zn[j][i] = l[j] * c->zn[Lq][i] + c->zn[j][i];
 }
 
 /* ADJUST_ORDER(-1): cvDecreaseBDF */
@@ -245,7 +289,7 @@ static void decrease_bdf(cell *c)
     for (int i = j + 2; i >= 2; --i) l[i] = l[i] * xi + l[i - 1];
   }
   for (int j = 2; j < c->q; ++j)
-    for (int i = 0; i < c->n; ++i) c->zn[j][i] = -l[j] * c->zn[c->q][i] + c->zn[j][i];
+    for (long i = 0; i < c->nt; ++i) c->zn[j][i] = -l[j] * c->zn[c->q][i] + c->zn[j][i];
 }
 
 static void adjust_order(cell *c, int dq)
@@ -257,10 +301,10 @@ static void adjust_order(cell *c, int dq)
 /* residual G = (rl1 zn[1] + ycor) - gamma f(tn, zn[0] + ycor)  (cvNlsResidual) */
 static int residual(cell *c, const double *ycor, double *G)
 {
-  for (int i = 0; i < c->n; ++i) c->y[i] = c->zn[0][i] + ycor[i];
+  for (long i = 0; i < c->nt; ++i) c->y[i] = c->zn[0][i] + ycor[i];
   int r = f_eval(c, c->tn, c->y, c->ftemp);
   if (r) return r;
-  for (int i = 0; i < c->n; ++i) {
+  for (long i = 0; i < c->nt; ++i) {
     double t = c->rl1 * c->zn[1][i] + ycor[i];
     G[i] = -c->gamma * c->ftemp[i] + t;
   }
@@ -281,16 +325,26 @@ static int lsetup(cell *c, int convfail, int *jcur)
       c->st.nje++;
       c->nstlj = c->st.nst;
       *jcur = 1;
-      int jr = orc_jac(c->p, c->tn, c->y, c->J);
-      if (jr) rv = -1;
+      for (long k = 0; k < c->ncell && rv == 0; ++k) {     /* block-diagonal J */
+        orc_problem q = *c->p;
+        if (c->global) {
+          q.rho = c->rho_all ? c->rho_all[k] : q.rho;
+          q.fext = c->fext_all ? c->fext_all + k * n : NULL;
+        }
+        if (orc_jac(&q, c->tn, c->y + k * n, c->J + k * n * n)) rv = -1;
+      }
     } else {
       *jcur = 0;
     }
     if (rv == 0) {
-      for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j)
-          c->M[i * n + j] = (i == j ? 1.0 : 0.0) - c->gamma * c->J[i * n + j];
-      if (orc_lu_factor(n, c->M, c->piv)) rv = 1;   /* zero pivot: recoverable */
+      for (long k = 0; k < c->ncell; ++k) {
+        double *Mk = c->M + k * n * n;
+        const double *Jk = c->J + k * n * n;
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j)
+            Mk[i * n + j] = (i == j ? 1.0 : 0.0) - c->gamma * Jk[i * n + j];
+        if (orc_lu_factor(n, Mk, c->piv + k * n)) rv = 1;   /* zero pivot: recoverable (R18) */
+      }
     }
   } else {
     /* CVDiagSetup: diagonal difference-quotient J, M = I - gamma J */
@@ -330,10 +384,10 @@ static int lsolve(cell *c, double *b)
 {
   int n = c->n;
   if (c->o->ls == ORC_LS_DENSE) {
-    orc_lu_solve(n, c->M, c->piv, b);
+    for (long k = 0; k < c->ncell; ++k) orc_lu_solve(n, c->M + k * n * n, c->piv + k * n, b + k * n);
     if (c->gamrat != 1.0) {
       double s = 2.0 / (1.0 + c->gamrat);
-      for (int i = 0; i < n; ++i) b[i] = s * b[i];
+      for (long i = 0; i < c->nt; ++i) b[i] = s * b[i];
     }
     return 0;
   }
@@ -353,14 +407,14 @@ static int lsolve(cell *c, double *b)
 /* NEWTON(nflag): cvNls + SUNNonlinSol_Newton + cvNlsConvTest (Eq. 4) */
 static int newton(cell *c, int nflag)
 {
-  int n = c->n;
+  long n = c->nt;
   int convfail = (nflag == FIRST_CALL || nflag == PREV_ERR_FAIL) ? CF_NONE : CF_OTHER;
   int setup = (nflag == PREV_CONV_FAIL) || (nflag == PREV_ERR_FAIL) || (c->st.nst == 0) ||
               (c->st.nst >= c->nstlp + MSBP) || (fabs(c->gamrat - 1.0) > DGMAX);
-  double ycor[ORC_NMAX], G[ORC_NMAX];
+  double *ycor = c->ycor, *G = c->G;
   double tol = c->tq[4];
   int jcur = 0;
-  for (int i = 0; i < n; ++i) ycor[i] = 0.0;
+  for (long i = 0; i < n; ++i) ycor[i] = 0.0;
   for (;;) {
     int rv = residual(c, ycor, G);                               /* N4 */
     if (rv < 0) return NLS_RHS_UNREC;
@@ -374,16 +428,16 @@ static int newton(cell *c, int nflag)
       int m = 0;
       for (;;) {                                                  /* N6 */
         c->st.nni++;
-        for (int i = 0; i < n; ++i) G[i] = -G[i];
+        for (long i = 0; i < n; ++i) G[i] = -G[i];
         rv = lsolve(c, G);
         if (rv) break;
-        for (int i = 0; i < n; ++i) ycor[i] = ycor[i] + G[i];
+        for (long i = 0; i < n; ++i) ycor[i] = ycor[i] + G[i];
         double del = wrms(c, G);
         if (m > 0) c->crate = fmax(CRDOWN * c->crate, del / dprev);     /* Eq. 4 rate */
         double dcon = del * fmin(1.0, c->crate) / tol;
         if (dcon <= 1.0) {                                                /* Eq. 4 test */
           c->acnrm = (m == 0) ? del : wrms(c, ycor);
-          for (int i = 0; i < n; ++i) c->acor[i] = ycor[i];
+          for (long i = 0; i < n; ++i) c->acor[i] = ycor[i];
           return NLS_OK;
         }
         if (m >= 1 && del > RDIV * dprev) { rv = 1; break; }
@@ -399,7 +453,7 @@ static int newton(cell *c, int nflag)
     if (rv > 0 && !jcur) {
       setup = 1;
       convfail = CF_BAD_J;
-      for (int i = 0; i < n; ++i) ycor[i] = 0.0;
+      for (long i = 0; i < n; ++i) ycor[i] = 0.0;
       continue;
     }
     return NLS_RECOVERABLE;
@@ -422,7 +476,7 @@ static void set_eta(cell *c)
 /* PREPARE_NEXT (cvPrepareNextStep + cvChooseEta) */
 static void prepare_next(cell *c, double dsm)
 {
-  int n = c->n;
+  long n = c->nt;
   if (c->etamax == 1.0) {
     c->qwait = c->qwait > 2 ? c->qwait : 2;
     c->qprime = c->q;
@@ -448,7 +502,7 @@ static void prepare_next(cell *c, double dsm)
     double pw = 1.0;
     for (int k = 0; k < c->L; ++k) pw = pw * hr;
     double cquot = (c->tq[5] / c->saved_tq5) * pw;
-    for (int i = 0; i < n; ++i) c->tmp[i] = -cquot * c->zn[c->qmax][i] + c->acor[i];
+    for (long i = 0; i < n; ++i) c->tmp[i] = -cquot * c->zn[c->qmax][i] + c->acor[i];
     double dup = wrms(c, c->tmp) * c->tq[3];
     etaqp1 = 1.0 / (orc_root(BIAS3 * dup, c->L + 1) + ADDON);
   }
@@ -465,7 +519,7 @@ static void prepare_next(cell *c, double dsm)
   } else {
     c->eta = etaqp1;
     c->qprime = c->q + 1;
-    for (int i = 0; i < n; ++i) c->zn[c->qmax][i] = c->acor[i];
+    for (long i = 0; i < n; ++i) c->zn[c->qmax][i] = c->acor[i];
   }
   set_eta(c);
 }
@@ -473,13 +527,13 @@ static void prepare_next(cell *c, double dsm)
 /* cvHin: initial step estimate (reading R9) */
 static int hin(cell *c, double t0, double tf, double *h0)
 {
-  int n = c->n;
+  long n = c->nt;
   double tdist = tf - t0;
   double tround = UROUND * fmax(fabs(t0), fabs(tf));
   double hlb = 100.0 * tround;
   /* cvUpperBoundH0 */
   double hub_inv = 0.0;
-  for (int i = 0; i < n; ++i) {
+  for (long i = 0; i < n; ++i) {
     double d = HUB_FACTOR * fabs(c->zn[0][i]) + 1.0 / c->ewt[i];
     double r = fabs(c->zn[1][i]) / d;
     if (r > hub_inv) hub_inv = r;
@@ -494,13 +548,13 @@ static int hin(cell *c, double t0, double tf, double *h0)
     double yddnrm = 0.0;
     for (int count2 = 1; count2 <= HIN_ITERS; ++count2) {
       /* cvYddNorm: ydd = (f(t0+hg, y0 + hg f0) - f0) * (1/hg) */
-      double yt[ORC_NMAX], ft[ORC_NMAX];
-      for (int i = 0; i < n; ++i) yt[i] = hg * c->zn[1][i] + c->zn[0][i];
+      double *yt = c->ycor, *ft = c->G;     /* scratch (not yet in use) */
+      for (long i = 0; i < n; ++i) yt[i] = hg * c->zn[1][i] + c->zn[0][i];
       int r = f_eval(c, t0 + hg, yt, ft);
       if (r < 0) return -1;
       if (r == 0) {
         double ih = 1.0 / hg;
-        for (int i = 0; i < n; ++i) ft[i] = (ft[i] - c->zn[1][i]) * ih;
+        for (long i = 0; i < n; ++i) ft[i] = (ft[i] - c->zn[1][i]) * ih;
         yddnrm = wrms(c, ft);
         ok = 1;
         break;
@@ -530,7 +584,7 @@ static int hin(cell *c, double t0, double tf, double *h0)
 /* STEP: one accepted step of cvStep.  Returns ORC_OK or a failure status. */
 static int step(cell *c, double tf)
 {
-  int n = c->n;
+  long n = c->nt;
   double saved_t = c->tn;
   int ncf = 0, nef = 0, nflag = FIRST_CALL;
   if (c->st.nst > 0 && c->hprime != c->h) {
@@ -598,7 +652,7 @@ static int step(cell *c, double tf)
     int fr = f_eval(c, c->tn, c->zn[0], c->tmp);
     if (fr < 0) return ORC_RHS_FAIL;
     if (fr > 0) return ORC_RHS_FAIL;
-    for (int i = 0; i < n; ++i) c->zn[1][i] = c->h * c->tmp[i];
+    for (long i = 0; i < n; ++i) c->zn[1][i] = c->h * c->tmp[i];
   }
 
   /* DONE: cvCompleteStep */
@@ -607,10 +661,10 @@ static int step(cell *c, double tf)
   if (c->q == 1 && c->st.nst > 1) c->tau[2] = c->tau[1];
   c->tau[1] = c->h;
   for (int j = 0; j <= c->q; ++j)
-    for (int i = 0; i < n; ++i) c->zn[j][i] = c->l[j] * c->acor[i] + c->zn[j][i];
+    for (long i = 0; i < n; ++i) c->zn[j][i] = c->l[j] * c->acor[i] + c->zn[j][i];
   c->qwait--;
   if (c->qwait == 1 && c->q != c->qmax) {
-    for (int i = 0; i < n; ++i) c->zn[c->qmax][i] = c->acor[i];
+    for (long i = 0; i < n; ++i) c->zn[c->qmax][i] = c->acor[i];
     c->saved_tq5 = c->tq[5];
   }
   prepare_next(c, dsm);
@@ -618,26 +672,26 @@ static int step(cell *c, double tf)
   return ORC_OK;
 }
 
-int orc_integrate(const orc_problem *p, const orc_opts *o, double t0, double tf,
-                  double *y, orc_stats *st, orc_trace *tr)
+/* INIT + LOOP (O1-O5) on an initialised cell c; y: [nt] in/out */
+static void run(cell *c, double t0, double tf, double *y, orc_trace *tr)
 {
-  cell C;
-  cell *c = &C;
-  memset(c, 0, sizeof(*c));
-  int n = p->n;
-  c->p = p; c->o = o; c->n = n;
-  c->qmax = o->qmax < 1 ? 1 : (o->qmax > ORC_QMAX ? ORC_QMAX : o->qmax);
+  const orc_opts *o = c->o;
+  long n = c->nt;
   c->st.status = ORC_OK;
   c->st.t_reached = t0;
-
-  for (int i = 0; i < n; ++i)
+  for (long i = 0; i < n; ++i)
     if (!isfinite(y[i])) { c->st.status = ORC_NONFINITE_INPUT; goto out; }
-  if (p->fext)
-    for (int i = 0; i < n; ++i)
-      if (!isfinite(p->fext[i])) { c->st.status = ORC_NONFINITE_INPUT; goto out; }
+  if (!c->global && c->p->fext) {
+    for (int i = 0; i < c->n; ++i)
+      if (!isfinite(c->p->fext[i])) { c->st.status = ORC_NONFINITE_INPUT; goto out; }
+  }
+  if (c->global && c->fext_all) {
+    for (long i = 0; i < n; ++i)
+      if (!isfinite(c->fext_all[i])) { c->st.status = ORC_NONFINITE_INPUT; goto out; }
+  }
 
   /* INIT */
-  for (int i = 0; i < n; ++i) c->zn[0][i] = y[i];
+  for (long i = 0; i < n; ++i) c->zn[0][i] = y[i];
   set_ewt(c, y);
   c->tn = t0;
   if (f_eval(c, t0, y, c->zn[1])) { c->st.status = ORC_RHS_FAIL; goto out; }
@@ -647,7 +701,7 @@ int orc_integrate(const orc_problem *p, const orc_opts *o, double t0, double tf,
   }
   if (h0 > tf - t0) h0 = tf - t0;
   if (o->hmax > 0.0 && h0 > o->hmax) h0 = o->hmax;
-  for (int i = 0; i < n; ++i) c->zn[1][i] = h0 * c->zn[1][i];
+  for (long i = 0; i < n; ++i) c->zn[1][i] = h0 * c->zn[1][i];
   c->h = c->hscale = c->hprime = h0;
   c->q = c->qprime = 1;
   c->L = 2;
@@ -670,19 +724,82 @@ int orc_integrate(const orc_problem *p, const orc_opts *o, double t0, double tf,
       int k = tr->count++;
       tr->tn[k] = c->tn; tr->h[k] = c->h; tr->q[k] = c->q;
       for (int j = 0; j <= ORC_QMAX; ++j)
-        for (int i = 0; i < n; ++i) tr->zn[(k * (ORC_QMAX + 1) + j) * n + i] = c->zn[j][i];
+        for (long i = 0; i < n; ++i) tr->zn[(k * (ORC_QMAX + 1) + j) * n + i] = c->zn[j][i];
     }
     if (fabs(c->tn - tf) <= 100.0 * UROUND * (fabs(c->tn) + fabs(c->h))) {   /* O5 */
       c->tn = tf;
       break;
     }
   }
-  for (int i = 0; i < n; ++i) y[i] = c->zn[0][i];
+  for (long i = 0; i < n; ++i) y[i] = c->zn[0][i];
   c->st.t_reached = c->tn;
 out:
   c->st.q_last = c->q;
   c->st.h_last = c->h;
+}
+
+int orc_integrate(const orc_problem *p, const orc_opts *o, double t0, double tf,
+                  double *y, orc_stats *st, orc_trace *tr)
+{
+  cellbuf B;
+  cell C;
+  cell *c = &C;
+  memset(c, 0, sizeof(*c));
+  memset(&B, 0, sizeof(B));
+  c->p = p; c->o = o; c->n = p->n;
+  c->ncell = 1; c->nt = p->n; c->global = 0;
+  c->qmax = o->qmax < 1 ? 1 : (o->qmax > ORC_QMAX ? ORC_QMAX : o->qmax);
+  for (int j = 0; j <= ORC_QMAX; ++j) c->zn[j] = B.zn[j];
+  c->ewt = B.ewt; c->acor = B.acor; c->y = B.y; c->ftemp = B.ftemp; c->tmp = B.tmp;
+  c->ycor = B.ycor; c->G = B.G; c->J = B.J; c->M = B.M; c->piv = B.piv; c->Minv = B.Minv;
+  run(c, t0, tf, y, tr);
   *st = c->st;
+  return c->st.status;
+}
+
+/* Global-norm mode (listing "Global-norm variant"): the N cells
+ * of a YC field y[k*N + c] integrated as ONE system -- one h, q, history and
+ * batch-wide WRMS norms (N_tot = n*N, reading R14); block-diagonal J with one
+ * LU per cell; any cell's zero pivot or RHS failure is the batch's
+ * recoverable failure (R18).  Dense solver only.                          */
+int orc_integrate_global(const orc_problem *proto, const orc_opts *o, double t0, double tf, int64_t N,
+                         double *y, const double *fext, const double *rho, orc_stats *st)
+{
+  int n = proto->n;
+  long nt = (long)n * N;
+  cell C;
+  cell *c = &C;
+  memset(c, 0, sizeof(*c));
+  c->p = proto; c->o = o; c->n = n;
+  c->ncell = N; c->nt = nt; c->global = 1;
+  c->qmax = o->qmax < 1 ? 1 : (o->qmax > ORC_QMAX ? ORC_QMAX : o->qmax);
+  double *mem = calloc((size_t)nt * (ORC_QMAX + 1 + 7) + (size_t)nt * n * 2 + (fext ? nt : 0), sizeof(double));
+  int *piv = calloc((size_t)nt, sizeof(int));
+  double *ycm = calloc((size_t)nt, sizeof(double));
+  if (!mem || !piv || !ycm) { free(mem); free(piv); free(ycm); return -1; }
+  double *q = mem;
+  for (int j = 0; j <= ORC_QMAX; ++j) { c->zn[j] = q; q += nt; }
+  c->ewt = q; q += nt; c->acor = q; q += nt; c->y = q; q += nt; c->ftemp = q; q += nt;
+  c->tmp = q; q += nt; c->ycor = q; q += nt; c->G = q; q += nt;
+  c->J = q; q += nt * n; c->M = q; q += nt * n;
+  double *fcm = NULL;
+  if (fext) { fcm = q; q += nt; }
+  c->piv = piv;
+  c->Minv = NULL;
+  c->rho_all = rho;
+  /* YC -> cell-major */
+  for (long k = 0; k < N; ++k)
+    for (int i = 0; i < n; ++i) {
+      ycm[k * n + i] = y[(long)i * N + k];
+      if (fext) fcm[k * n + i] = fext[(long)i * N + k];
+    }
+  c->fext_all = fcm;
+  run(c, t0, tf, ycm, NULL);
+  if (c->st.status != ORC_NONFINITE_INPUT)
+    for (long k = 0; k < N; ++k)
+      for (int i = 0; i < n; ++i) y[(long)i * N + k] = ycm[k * n + i];
+  *st = c->st;
+  free(mem); free(piv); free(ycm);
   return c->st.status;
 }
 

@@ -18,6 +18,12 @@
  */
 double orc_wrms(int n, const double *v, const double *w, int group)
 {
+  return sqrt(orc_wrms_sum(n, v, w, group) / (double)n);
+}
+
+/* the sum S of Eq. 3 before the division by N and the square root */
+double orc_wrms_sum(int n, const double *v, const double *w, int group)
+{
   double s[64];
   int G = group < 1 ? 1 : group;
   for (int l = 0; l < G; ++l) {
@@ -33,7 +39,7 @@ double orc_wrms(int n, const double *v, const double *w, int group)
     for (int l = 0; l < G; ++l) t[l] = s[l] + s[l ^ off];
     for (int l = 0; l < G; ++l) s[l] = t[l];
   }
-  return sqrt(s[0] / (double)n);
+  return s[0];
 }
 
 /*

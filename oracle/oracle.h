@@ -127,8 +127,11 @@ typedef struct {
   double *zn;            /* [cap][ORC_QMAX+1][n] */
 } orc_trace;
 
+#define ORC_GBLK 256        /* global-norm mode: cells per partial sum (R15) */
+
 /* ---- primitives -------------------------------------------------------- */
 double orc_wrms(int n, const double *v, const double *w, int group);
+double orc_wrms_sum(int n, const double *v, const double *w, int group);
 int orc_lu_factor(int n, double *M /* row-major n*n, in/out */, int *piv);
 void orc_lu_solve(int n, const double *LU, const int *piv, double *b);
 
@@ -154,6 +157,12 @@ void orc_set_bdf(int q, double h, const double *tau /* [7], tau[1..6] */,
 /* Integrate one cell from t0 to tf in place (y: [n]).  Returns status.   */
 int orc_integrate(const orc_problem *p, const orc_opts *o, double t0,
                   double tf, double *y, orc_stats *st, orc_trace *tr);
+
+/* Global-norm mode: the N cells of a YC field integrated as one system with
+ * batch-wide norms (see bdf.c).  fext YC or NULL, rho [N] or NULL.          */
+int orc_integrate_global(const orc_problem *proto, const orc_opts *o, double t0, double tf,
+                         int64_t N, double *y, const double *fext, const double *rho,
+                         orc_stats *st);
 
 /* Batch driver over cells [c0, c1) of a YC (component-major) field:
  * y[k*N + c], fext[k*N + c] (or NULL), rho[c] (or NULL).  Stats written

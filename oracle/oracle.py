@@ -107,6 +107,9 @@ def lib():
             L.orc_integrate.restype = C.c_int
             L.orc_integrate.argtypes = [C.POINTER(Problem), C.POINTER(Opts), C.c_double, C.c_double, dp,
                                         C.POINTER(Stats), C.POINTER(Trace)]
+            L.orc_integrate_global.restype = C.c_int
+            L.orc_integrate_global.argtypes = [C.POINTER(Problem), C.POINTER(Opts), C.c_double, C.c_double,
+                                               C.c_int64, dp, dp, dp, C.POINTER(Stats)]
             L.orc_integrate_batch.restype = None
             L.orc_integrate_batch.argtypes = [C.POINTER(Problem), C.POINTER(Opts), C.c_double, C.c_double,
                                               C.c_int64, C.c_int64, C.c_int64, dp, dp, dp, C.POINTER(Stats)]
@@ -345,6 +348,21 @@ def integrate(model, y0, t0, tf, rtol, atol, rho=1.0, fext=None, trace=0, ls=Non
         c = trp.count
         tr = {k: v[:c] for k, v in tr.items()}
     return y, st.as_dict(), tr
+
+
+def integrate_global(model, y_yc, t0, tf, rtol, atol, rho=None, fext_yc=None, group=1, **kw):
+    """Global-norm mode (lockstep batch, batch-wide WRMS): returns (y [n, N], stats dict)."""
+    y = np.array(y_yc, dtype=np.float64, copy=True, order="C")
+    n, N = y.shape
+    fe = None if fext_yc is None else np.ascontiguousarray(fext_yc, dtype=np.float64)
+    rh = None if rho is None else np.ascontiguousarray(rho, dtype=np.float64)
+    p = model.problem(1.0, None)
+    o = make_opts(n, rtol, atol, ls=LS_DENSE, group=group, **kw)
+    st = Stats()
+    lib().orc_integrate_global(C.byref(p), C.byref(o), float(t0), float(tf), N, _dp(y),
+                               _dp(fe) if fe is not None else None, _dp(rh) if rh is not None else None,
+                               C.byref(st))
+    return y, st.as_dict()
 
 
 STAT_FIELDS = ["status", "nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn", "q_last", "h_last", "t_reached"]

@@ -149,3 +149,43 @@ def test_batch_driver_matches_single_cell(oracle):
     for c in (0, 17, 63):
         y1, s1, _ = oracle.integrate(m, Y[:, c], 0.0, 40.0, 1e-6, 1e-10)
         assert np.array_equal(y1, yb[:, c]) and s1["nst"] == st["nst"][c]
+
+
+# ---------------------------------------------------------------- global-norm mode
+def test_global_mode_identical_cells_reproduce_single_cell(oracle):
+    """SPEC AC7: k identical cells integrated as one lockstep batch reproduce the
+    single-cell run with the identical step count (batch WRMS of identical blocks = cell WRMS)."""
+    m = oracle.Model.robertson()
+    y1, s1, _ = oracle.integrate(m, [1.0, 0.0, 0.0], 0.0, 40.0, 1e-6, 1e-10)
+    for k in (1, 64, 300):
+        Y = np.tile(np.array([[1.0], [0.0], [0.0]]), (1, k))
+        yg, sg = oracle.integrate_global(m, Y, 0.0, 40.0, 1e-6, 1e-10)
+        assert sg["status"] == 0
+        assert sg["nst"] == s1["nst"] and sg["netf"] == s1["netf"] and sg["nje"] == s1["nje"], (k, sg, s1)
+        # the only difference is the rounding of the batch sum (k partial sums): ~1e-12 relative
+        np.testing.assert_allclose(yg, np.tile(y1[:, None], (1, k)), rtol=1e-11, atol=1e-300)
+
+
+def test_global_mode_linear_closed_form(oracle):
+    lam = np.array([-1.0, -5.0, -25.0, -125.0])
+    m = oracle.Model.linear([-1.0])
+    # a batch of 4 one-component cells with different rates is not expressible with one
+    # model, so use a 4-component linear cell and a batch of 3 copies with different y0
+    m = oracle.Model.linear(lam)
+    Y = np.stack([np.linspace(1.0, 2.0, 3)] * 4)
+    yg, sg = oracle.integrate_global(m, Y, 0.0, 1.0, 1e-7, 1e-12)
+    exact = Y * np.exp(lam[:, None])
+    assert sg["status"] == 0
+    assert np.all(np.abs(yg - exact) <= 20 * (1e-7 * np.abs(exact) + 1e-12))
+
+
+def test_global_mode_lockstep_costs_more_than_per_cell(oracle):
+    """in lockstep the effort is dictated by the most difficult cells: the batch takes at
+    least as many steps as its hardest cell, and each step advances every cell."""
+    from synth import robertson_field
+    Y = robertson_field(32)
+    _, st = oracle.integrate_batch(oracle.Model.robertson(), Y, 0.0, 40.0, 1e-6, 1e-10)
+    yg, sg = oracle.integrate_global(oracle.Model.robertson(), Y, 0.0, 40.0, 1e-6, 1e-10)
+    assert sg["status"] == 0
+    assert sg["nst"] >= 0.5 * st["nst"].max()
+    assert np.abs(yg.sum(axis=0) - 1.0).max() <= 1e-14       # conservation per cell
