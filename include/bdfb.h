@@ -131,6 +131,15 @@ int bdfb_create(bdfb_batch **out, int64_t n_cells, int32_t n, double rtol,
  * parameters (copied), or NULL for defaults.                               */
 int bdfb_set_model(bdfb_batch *b, int32_t model_id, const void *params, size_t bytes);
 
+/* Global-norm mode across ranks (one lockstep batch over all GPUs): create
+ * the library's NCCL communicator.  nccl_unique_id: host pointer to the 128
+ * bytes of an ncclUniqueId created on rank 0 and broadcast by the caller;
+ * ncells_total: the batch size summed over ranks (the N of Eq. 3, R14; each
+ * rank's n_cells should be a multiple of 256 so the reduction order matches
+ * the single-GPU order).  Only valid for BDFB_MODE_GLOBAL_NORM handles.      */
+int bdfb_set_comm(bdfb_batch *b, const void *nccl_unique_id, int32_t nranks, int32_t rank,
+                  int64_t ncells_total);
+
 /* Attach (or detach with NULL) caller-owned per-cell statistics arrays that
  * the next bdfb_integrate fills.  The struct is copied.                     */
 int bdfb_set_cell_stats(bdfb_batch *b, const bdfb_cell_stats *cs);
@@ -144,7 +153,11 @@ int bdfb_set_cell_stats(bdfb_batch *b, const bdfb_cell_stats *cs);
  *          MECH_*), or NULL when the model needs none.
  * Per-cell mode enqueues asynchronously; results are valid when `stream`
  * completes.  Returns 0 on enqueue, < 0 on an argument or launch error.
- * Failed cells are counted by bdfb_get_stats (they are not an error here). */
+ * Failed cells are counted by bdfb_get_stats (they are not an error here).
+ * Global-norm mode (group models only: MECH_H2, MECH_DRM19) runs the
+ * integrator's control loop on the host and returns when done; its
+ * statistics are batch counters (one step count for the whole batch) and a
+ * failure fails every cell of the batch (R18).                              */
 int bdfb_integrate(bdfb_batch *b, double t0, double tf, double *y, const double *f_ext,
                    const double *aux, int32_t layout, void *stream);
 

@@ -19,7 +19,9 @@ import numpy as np
 
 from . import _lib as L
 
-__all__ = ["Batch", "MODELS", "eval_rhs", "eval_jac", "lu_factor_solve", "version", "library_path"]
+MODE_PER_CELL, MODE_GLOBAL_NORM = L.MODE_PER_CELL, L.MODE_GLOBAL_NORM
+
+__all__ = ["Batch", "MODE_PER_CELL", "MODE_GLOBAL_NORM", "MODELS", "eval_rhs", "eval_jac", "lu_factor_solve", "version", "library_path"]
 
 MODELS = {"linear": (L.MODEL_LINEAR, 1), "robertson": (L.MODEL_ROBERTSON, 3), "nyx_kwh": (L.MODEL_NYX_KWH, 1),
           "h2": (L.MODEL_MECH_H2, 10), "drm19": (L.MODEL_MECH_DRM19, 22)}
@@ -102,6 +104,13 @@ class Batch:
             self._params_keep = p
         _check(self._L.bdfb_set_model(self.h, mid, buf, size), self.h)
         self.model = model
+
+    def set_comm(self, unique_id: bytes, nranks: int, rank: int, ncells_total: int):
+        """Global-norm mode across ranks: NCCL communicator from a 128-byte ncclUniqueId
+        (created on rank 0, broadcast by the caller, e.g. with torch.distributed)."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(self._L.bdfb_set_comm(self.h, C.cast(buf, C.c_void_p), int(nranks), int(rank), int(ncells_total)),
+               self.h)
 
     def attach_cell_stats(self, device="cuda"):
         """Allocate per-cell statistics tensors that each integrate fills; returns the dict."""

@@ -19,7 +19,7 @@ MODE_PER_CELL, MODE_GLOBAL_NORM = 0, 1
 SYMBOLS = ["bdfb_default_options", "bdfb_create", "bdfb_set_model", "bdfb_set_cell_stats", "bdfb_integrate",
            "bdfb_integrate_host", "bdfb_get_stats", "bdfb_last_launch_count", "bdfb_last_kernel_ms",
            "bdfb_destroy", "bdfb_last_error", "bdfb_version", "bdfb_eval_rhs", "bdfb_eval_jac",
-           "bdfb_lu_factor_solve", "bdfb_probe_fp64"]
+           "bdfb_lu_factor_solve", "bdfb_probe_fp64", "bdfb_set_comm"]
 
 
 class Options(C.Structure):
@@ -90,6 +90,8 @@ def lib():
     L.bdfb_eval_jac.argtypes = [vp, dp, vp, vp, vp, vp]
     L.bdfb_lu_factor_solve.restype = C.c_int
     L.bdfb_lu_factor_solve.argtypes = [i32, i64, vp, vp, vp, vp, vp]
+    L.bdfb_set_comm.restype = C.c_int
+    L.bdfb_set_comm.argtypes = [vp, vp, i32, i32, i64]
     L.bdfb_probe_fp64.restype = C.c_int
     L.bdfb_probe_fp64.argtypes = [i32, dp, C.POINTER(C.c_double), C.POINTER(C.c_int32)]
     _lib = L

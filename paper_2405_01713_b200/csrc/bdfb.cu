@@ -16,6 +16,7 @@
 #include "../../include/bdfb.h"
 #include "bdf_cell.cuh"
 #include "bdf_group.cuh"
+#include "global_host.cuh"
 #include "gen/mech_drm19_class.cuh"
 #include "gen/mech_h2_lidryer.cuh"
 #include "mech_model.cuh"
@@ -38,6 +39,8 @@ struct bdfb_batch {
   unsigned long long* d_counter = nullptr;
   Agg* d_agg = nullptr;
   double *d_y = nullptr, *d_f = nullptr, *d_aux = nullptr;   // host-API staging
+  GlobalBuffers gb;            // global-norm mode workspace
+  Agg gagg{};                  // global-norm mode: statistics of the last integrate (host)
   CellStatsPtrs cs{};
   cudaStream_t last_stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -98,7 +101,7 @@ int bdfb_create(bdfb_batch** out, int64_t n_cells, int32_t n, double rtol, const
   if (opt) o = *opt;
   if (o.qmax < 1 || o.qmax > 5) return fail(nullptr, BDFB_EINVAL, "qmax must be in 1..5");
   if (o.mxstep < 1) return fail(nullptr, BDFB_EINVAL, "mxstep must be >= 1");
-  if (o.mode != BDFB_MODE_PER_CELL) return fail(nullptr, BDFB_EUNSUPPORTED, "global-norm mode not in this build");
+  if (o.mode != BDFB_MODE_PER_CELL && o.mode != BDFB_MODE_GLOBAL_NORM) return fail(nullptr, BDFB_EINVAL, "bad mode");
   if (o.h0 < 0.0 || o.hmin < 0.0 || o.hmax < 0.0) return fail(nullptr, BDFB_EINVAL, "h0/hmin/hmax must be >= 0");
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
@@ -119,6 +122,28 @@ int bdfb_create(bdfb_batch** out, int64_t n_cells, int32_t n, double rtol, const
     bdfb_destroy(b);
     return cuda_fail(nullptr, e, "create");
   }
+  if (o.mode == BDFB_MODE_GLOBAL_NORM) {   // all workspace once: vectors, J, LU, reductions
+    GlobalBuffers& g = b->gb;
+    const size_t M = (size_t)n * n_cells, nb = (size_t)(n_cells + GM_BLK - 1) / GM_BLK;
+    bool ok = true;
+    auto A = [&](void** p, size_t bytes) { if (ok && cudaMalloc(p, bytes) != cudaSuccess) ok = false; };
+    for (int j = 0; j <= QMAX; ++j) A((void**)&g.v.zn[j], sizeof(double) * M);
+    A((void**)&g.v.ewt, sizeof(double) * M); A((void**)&g.v.acor, sizeof(double) * M);
+    A((void**)&g.v.yq, sizeof(double) * M); A((void**)&g.v.fy, sizeof(double) * M);
+    A((void**)&g.v.del, sizeof(double) * M); A((void**)&g.v.tmp, sizeof(double) * M);
+    A((void**)&g.v.f, sizeof(double) * M);
+    A((void**)&g.J, sizeof(double) * M * n); A((void**)&g.LU, sizeof(double) * M * n);
+    A((void**)&g.invd, sizeof(double) * M); A((void**)&g.pos, sizeof(int) * M); A((void**)&g.perm, sizeof(int) * M);
+    A((void**)&g.s, sizeof(double) * n_cells); A((void**)&g.P, sizeof(double) * nb);
+    A((void**)&g.sum, sizeof(double)); A((void**)&g.gath, sizeof(double) * 1024);
+    A((void**)&g.flag, sizeof(int)); A((void**)&g.igath, sizeof(int) * 1024);
+    A((void**)&g.ubuf, sizeof(unsigned long long));
+    g.ncells_total = n_cells;
+    if (!ok) {
+      bdfb_destroy(b);
+      return fail(nullptr, BDFB_ENOMEM, "global-norm workspace does not fit in device memory");
+    }
+  }
   *out = b;
   return BDFB_OK;
 }
@@ -132,6 +157,15 @@ void bdfb_destroy(bdfb_batch* b) {
   if (b->d_y) cudaFree(b->d_y);
   if (b->d_f) cudaFree(b->d_f);
   if (b->d_aux) cudaFree(b->d_aux);
+  {
+    GlobalBuffers& g = b->gb;
+    for (int j = 0; j <= QMAX; ++j) cudaFree(g.v.zn[j]);
+    cudaFree(g.v.ewt); cudaFree(g.v.acor); cudaFree(g.v.yq); cudaFree(g.v.fy); cudaFree(g.v.del);
+    cudaFree(g.v.tmp); cudaFree(g.v.f); cudaFree(g.J); cudaFree(g.LU); cudaFree(g.invd); cudaFree(g.pos);
+    cudaFree(g.perm); cudaFree(g.s); cudaFree(g.P); cudaFree(g.sum); cudaFree(g.gath); cudaFree(g.flag);
+    cudaFree(g.igath); cudaFree(g.ubuf);
+    if (g.comm) ncclCommDestroy(g.comm);
+  }
   if (b->ev0) cudaEventDestroy(b->ev0);
   if (b->ev1) cudaEventDestroy(b->ev1);
   delete b;
@@ -241,6 +275,83 @@ static int launch_integrate(bdfb_batch* b, const Opts& o, double* y, const doubl
   return BDFB_OK;
 }
 
+__global__ void gk_fill_stats(CellStatsPtrs cs, long long N, int status, int nst, int nfe, int nje, int nsetups,
+                              int nni, int netf, int ncfn, int q, double h, double tn) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  if (cs.status) cs.status[c] = status;
+  if (cs.nst) cs.nst[c] = nst;
+  if (cs.nfe) cs.nfe[c] = nfe;
+  if (cs.nje) cs.nje[c] = nje;
+  if (cs.nsetups) cs.nsetups[c] = nsetups;
+  if (cs.nni) cs.nni[c] = nni;
+  if (cs.netf) cs.netf[c] = netf;
+  if (cs.ncfn) cs.ncfn[c] = ncfn;
+  if (cs.q_last) cs.q_last[c] = q;
+  if (cs.h_last) cs.h_last[c] = h;
+  if (cs.t_reached) cs.t_reached[c] = tn;
+}
+
+// global-norm mode: host control loop over device kernels (global_host.cuh)
+template <class Model>
+static int run_global(bdfb_batch* b, const Opts& o, double* y, const double* fext, const double* aux,
+                      cudaStream_t st) {
+  if constexpr (Model::G > 1) {
+    typename Model::Params prm;
+    memcpy(&prm, b->params, sizeof(prm));
+    auto* kr = gk_rhs<Model>;
+    auto* ks = gk_setup<Model>;
+    auto* kv = gk_solve<Model>;
+    const int smem = (int)(sizeof(double) * GMK<Model>::PG * GMK<Model>::GPB);
+    if (smem > 48 * 1024) {
+      cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    }
+    cudaEventRecord(b->ev0, st);
+    GlobalRunner<Model> R(b->gb, o, prm, st, b->n, b->ncells, b->d_atol, fext, aux);
+    const GlobalResult r = R.run(y);
+    cudaEventRecord(b->ev1, st);
+    const long long N = b->ncells;
+    gk_fill_stats<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(b->cs, N, r.status, (int)r.nst, (int)r.nfe,
+                                                                 (int)r.nje, (int)r.nsetups, (int)r.nni, (int)r.netf,
+                                                                 (int)r.ncfn, r.q, r.h, r.tn);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(b, e, "global-norm integrate");
+    Agg& a = b->gagg;
+    a = Agg{};
+    a.cells_done = (unsigned long long)N;
+    a.n_failed = r.status == ST_OK ? 0ull : (unsigned long long)N;
+    a.nst = r.nst; a.nfe = r.nfe; a.nje = r.nje; a.nsetups = r.nsetups; a.nni = r.nni; a.netf = r.netf;
+    a.ncfn = r.ncfn; a.nst_max = r.nst; a.nfe_max = r.nfe;
+    b->timed = true;
+    b->launches = -1;
+    return BDFB_OK;
+  } else {
+    return fail(b, BDFB_EUNSUPPORTED, "global-norm mode is implemented for the group models (MECH_H2, MECH_DRM19)");
+  }
+}
+
+extern "C" int bdfb_set_comm(bdfb_batch* b, const void* nccl_unique_id, int32_t nranks, int32_t rank,
+                             int64_t ncells_total) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (b->opt.mode != BDFB_MODE_GLOBAL_NORM) return fail(b, BDFB_EINVAL, "set_comm needs a GLOBAL_NORM handle");
+  if (!nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks || nranks > 1024 || ncells_total < b->ncells)
+    return fail(b, BDFB_EINVAL, "bad communicator arguments");
+  cudaSetDevice(b->device);
+  if (b->gb.comm) { ncclCommDestroy(b->gb.comm); b->gb.comm = nullptr; }
+  if (nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&b->gb.comm, nranks, id, rank);
+    if (r != ncclSuccess) return fail(b, BDFB_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  b->gb.nranks = nranks;
+  b->gb.rank = rank;
+  b->gb.ncells_total = ncells_total;
+  return BDFB_OK;
+}
+
 extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, const double* f_ext,
                               const double* aux, int32_t layout, void* stream) {
   if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
@@ -265,6 +376,14 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
   o.ncells = b->ncells;
   cudaStream_t st = (cudaStream_t)stream;
   b->last_stream = st;
+  if (b->opt.mode == BDFB_MODE_GLOBAL_NORM) {
+    if (layout != BDFB_LAYOUT_YC) return fail(b, BDFB_EUNSUPPORTED, "global-norm mode takes the YC layout");
+    switch (b->model) {
+      case BDFB_MODEL_MECH_H2: return run_global<ModelH2>(b, o, y, f_ext, aux, st);
+      case BDFB_MODEL_MECH_DRM19: return run_global<ModelDRM19>(b, o, y, f_ext, aux, st);
+      default: return fail(b, BDFB_EUNSUPPORTED, "global-norm mode: group models only (MECH_H2, MECH_DRM19)");
+    }
+  }
   switch (b->model) {
     case BDFB_MODEL_LINEAR: return launch_integrate<ModelLinear>(b, o, y, f_ext, aux, st);
     case BDFB_MODEL_ROBERTSON: return launch_integrate<ModelRobertson>(b, o, y, f_ext, aux, st);
@@ -314,8 +433,11 @@ extern "C" int64_t bdfb_get_stats(bdfb_batch* b, bdfb_stats* agg) {
   cudaError_t e = cudaStreamSynchronize(b->last_stream);
   if (e != cudaSuccess) return cuda_fail(b, e, "stream synchronize");
   Agg h{};
-  if ((e = cudaMemcpy(&h, b->d_agg, sizeof(Agg), cudaMemcpyDeviceToHost)) != cudaSuccess)
+  if (b->opt.mode == BDFB_MODE_GLOBAL_NORM) {
+    h = b->gagg;
+  } else if ((e = cudaMemcpy(&h, b->d_agg, sizeof(Agg), cudaMemcpyDeviceToHost)) != cudaSuccess) {
     return cuda_fail(b, e, "stats copy");
+  }
   if (agg) {
     agg->n_cells = (int64_t)h.cells_done;
     agg->n_failed = (int64_t)h.n_failed;

@@ -245,3 +245,26 @@ def test_full_size_c3_sampled(oracle):
     yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho, fext_yc=F,
                                     group=G, threads=8, cells=idx)
     end_state_check(yg[:, idx], yo, 1e-6, 1e-10)
+
+
+# ------------------------------------------------------------------ global-norm mode (row a12)
+@pytest.mark.parametrize("name,L,dt", [("h2", 4, 1e-5), ("drm19", 4, 1e-6), ("drm19", 8, 1e-5)])
+def test_global_norm_mode_parity(oracle, name, L, dt):
+    """The paper's lockstep batch: one h, q for all cells, batch-wide WRMS (R14, R15 order:
+    per-cell sums, 256-cell block partials in order).  GPU (host control loop + device kernels)
+    vs the oracle's global-norm variant on identical inputs."""
+    mech, n, G = MECH[name]
+    y0, rho, F, prog = flame_field(mech, L, dt=dt)
+    N = y0.shape[1]
+    b = P.Batch(N, n, 1e-6, 1e-10, mode=P.MODE_GLOBAL_NORM)
+    b.set_model(name)
+    cs = b.attach_cell_stats()
+    y = cu(y0)
+    b.integrate(0.0, dt, y, f_ext=cu(F), aux=cu(rho))
+    st = b.stats()
+    yo, so = oracle.integrate_global(oracle.Model.mechanism(mech), y0, 0.0, dt, 1e-6, 1e-10, rho=rho, fext_yc=F)
+    assert so["status"] == 0 and st["n_failed"] == 0
+    print(f"global {name} N={N}: gpu nst={st['nst']} nfe={st['nfe']} | oracle nst={so['nst']} nfe={so['nfe']}")
+    assert st["nst"] == so["nst"] and st["nfe"] == so["nfe"] and st["netf"] == so["netf"]
+    end_state_check(y.cpu().numpy(), yo, 1e-6, 1e-10)
+    assert np.all(cs["nst"].cpu().numpy() == so["nst"])
