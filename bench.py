@@ -43,7 +43,13 @@ CONFIGS = {
            "C3 H2/air (9 species + T, n=10) flame field on 64^3 cells, dt_CFD 1e-5 s"),
     "C4": ("drm19", "drm19_class", 22, 256, 1e-5, 1e-6, 1e-10,
            "C4 DRM19-class CH4/air (21 species + T, n=22) flame field on 256^3 cells, dt_CFD 1e-5 s"),
+    # the paper's lockstep batch (row a12).  C5's 53-species mechanism is not available (R22) and the
+    # group kernel holds n <= 32, so the global-norm path is measured on the DRM19-class mechanism.
+    "G4": ("drm19", "drm19_class", 22, 64, 1e-5, 1e-6, 1e-10,
+           "G4 global-norm mode (lockstep batch, batch-wide WRMS) on the DRM19-class flame field, 64^3 cells, "
+           "dt_CFD 1e-5 s"),
 }
+GLOBAL_CFGS = {"G4"}
 METRIC = "cell ODE integrations/sec per outer step"
 UNIT = "cells/s"
 FP64_FMA_PER_SM_CLK = 64        # B200 FP64 units per SM (sm_100a): 148 x 64 x 2 x 1.965 GHz = 37.2 TF
@@ -84,8 +90,29 @@ def flop_model(cfg, st):
     f_lu = (2 * (n - 1) * n * (2 * n - 1)) // 6 + n * (n - 1) // 2 + n + 2 * n * n
     f_sol = 2 * n * n - n
     att = st["nst"] + st["netf"] + st["ncfn"]
-    return (st["nfe"] * f_rhs + st["nje"] * f_jac + st["nsetups"] * f_lu + st["nni"] * (f_sol + 9 * n) +
-            att * (6 * n + 20 * n + 60) + st["nst"] * (8 * n + 3 * n + 80))
+    f = (st["nfe"] * f_rhs + st["nje"] * f_jac + st["nsetups"] * f_lu + st["nni"] * (f_sol + 9 * n) +
+         att * (6 * n + 20 * n + 60) + st["nst"] * (8 * n + 3 * n + 80))
+    if cfg in GLOBAL_CFGS:      # batch counters: every batch step does the work for every cell
+        f *= st["n_cells"]
+    return f
+
+
+def hbm_bytes_global(cfg, st):
+    """Algorithmic HBM bytes of one global-norm-mode integrate: per Newton solve the
+    cell's LU (8 n^2) + pivots/1/U (16 n) + del, acor r/w, b (32 n); per RHS y, F in, f out (24 n + 8);
+    per setup J r/w + LU w (24 n^2); per norm 16 n; per step the Nordsieck updates (2 (q+1) 8 n, q ~ 3)."""
+    n = CONFIGS[cfg][2]
+    per_cell = (st["nni"] * (8 * n * n + 16 * n + 32 * n) + st["nfe"] * (24 * n + 8) +
+                st["nsetups"] * 24 * n * n + (st["nni"] + st["nst"]) * 16 * n + st["nst"] * 64 * n)
+    return per_cell * st["n_cells"]
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
+    except Exception:
+        return 7700.0, "fallback: B200 nominal HBM3e 7.7 TB/s"
 
 
 def traffic_per_launch(cfg, cells):
@@ -153,6 +180,20 @@ def oracle_cells_per_s(cfg, budget_s=15.0, threads=None, rank_cells=None, steps=
     from synth.fields import stratified_sample
     model, mech, n, L, dt, rtol, atol, _ = CONFIGS[cfg]
     threads = threads or os.cpu_count() or 1
+    if cfg in GLOBAL_CFGS:
+        # the lockstep batch is one system: the oracle's global variant on a contiguous sub-batch, 1 thread
+        from synth import flame_field
+        om = O.Model.mechanism(mech)
+
+        def runb(m):
+            y, rho, F, _ = flame_field(mech, L, cells=np.arange(m), dt=dt)
+            t = time.perf_counter()
+            O.integrate_global(om, y, 0.0, dt, rtol, atol, rho=rho, fext_yc=F)
+            return time.perf_counter() - t
+
+        tp = runb(256)
+        m = int(max(256, min(L ** 3, 256 * budget_s / max(tp, 1e-6))) // 256 * 256)
+        return m, [runb(m) for _ in range(steps)], 1
     if cfg == "C1":
         y, rho, F, prog = make_inputs(cfg)
         om, G, idx = O.Model.robertson(), 1, np.arange(y.shape[1])
@@ -220,7 +261,9 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": {"workload": desc, "sample_cells_per_step": m},
                 "cpu_baseline": {"value": val, "unit": UNIT, "cores": thr, "kind": "oracle",
-                                 "sample": f"{m} stratified cells of the {cfg} workload per step"},
+                                 "sample": (f"first {m} cells of the {cfg} field as one lockstep batch per step"
+                                            if cfg in GLOBAL_CFGS else
+                                            f"{m} stratified cells of the {cfg} workload per step")},
                 "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -237,8 +280,15 @@ def main():
 
     y0, rho, F, prog = make_inputs(cfg, rank, args.cells or None, world)
     N = y0.shape[1]
-    b = P.Batch(N, n, rtol, atol, device=local)
+    glob_mode = cfg in GLOBAL_CFGS
+    b = P.Batch(N, n, rtol, atol, device=local, mode=P.MODE_GLOBAL_NORM if glob_mode else P.MODE_PER_CELL)
     b.set_model(model)
+    if glob_mode and world > 1:
+        # one lockstep system across ranks: the library's own NCCL communicator carries the norms
+        uid = torch.cuda.nccl.unique_id() if rank == 0 else None
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        b.set_comm(obj[0], world, rank, N * world)
     y_pristine = torch.tensor(y0, device=dev)
     y = torch.empty_like(y_pristine)
     Fd = None if F is None else torch.tensor(F, device=dev)
@@ -291,6 +341,15 @@ def main():
             "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
             "fp64_probe_tflops": probe, "kernel_ms": statistics.mean(kern_ms),
             "flops_per_launch": statistics.mean(flops)}
+    if glob_mode:
+        # lockstep batch: the state, J and LU stream through HBM every stage -> HBM roofline
+        hb = [hbm_bytes_global(cfg, s) for s in stats]
+        gbs = statistics.mean(x / (k * 1e-3) for x, k in zip(hb, kern_ms)) / 1e9
+        hpk, src = hbm_peak()
+        roof = {"bound": "hbm", "achieved": gbs, "peak": hpk, "unit": "GB/s", "frac": gbs / hpk,
+                "traffic": traffic_per_launch(cfg, N), "kernel": "global-norm kernel sequence (gk_*)",
+                "peak_source": src, "kernel_ms": statistics.mean(kern_ms),
+                "bytes_per_integrate": statistics.mean(hb), "fp64_tflops": achieved, "alu_frac": achieved / peak}
 
     # e2e through the host-buffer C-ABI call (pinned host memory; H2D + integrate + D2H timed)
     yh0 = torch.tensor(y0).pin_memory()
@@ -317,8 +376,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         m, times, thr = oracle_cells_per_s(cfg, budget_s=15.0)
-        cpu = {"value": m / times[0], "unit": UNIT, "cores": thr, "kind": "oracle",
-               "sample": f"{m} stratified cells of the {cfg} workload (same recipe and seed), one pass"}
+        smp = (f"first {m} cells of the {cfg} field integrated as one lockstep batch (orc_integrate_global), one pass"
+               if glob_mode else f"{m} stratified cells of the {cfg} workload (same recipe and seed), one pass")
+        cpu = {"value": m / times[0], "unit": UNIT, "cores": thr, "kind": "oracle", "sample": smp}
 
     s = PL.reduce_stats(stats[-1], dist, dev)
     if rank == 0:
@@ -327,7 +387,9 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": desc, "cells_per_gpu": N, "n": n, "rtol": rtol,
                            "atol": atol if np.isscalar(atol) else list(atol), "dt_CFD": dt,
-                           "mode": "per-cell", "parallelism": f"dp{world} (cells sharded, no collective)",
+                           "mode": "global-norm" if glob_mode else "per-cell",
+                           "parallelism": (f"dp{world} (cells sharded; NCCL allgather of the batch norms)"
+                                           if glob_mode else f"dp{world} (cells sharded, no collective)"),
                            "l2": "inputs larger than L2 (state %.2f GB per GPU); pristine field restored "
                                  "untimed before each step" % (y0.nbytes / 1e9),
                            "mechanism": mech},

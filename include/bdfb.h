@@ -174,11 +174,14 @@ int bdfb_integrate_host(bdfb_batch *b, double t0, double tf, double *y_host, con
  * or < 0 on error.                                                          */
 int64_t bdfb_get_stats(bdfb_batch *b, bdfb_stats *agg);
 
-/* Kernel launches made by the last bdfb_integrate (for bench accounting). */
+/* Kernel launches made by the last bdfb_integrate (for bench accounting):
+ * 1 in PER_CELL mode (one persistent kernel); in GLOBAL_NORM mode every
+ * device kernel the host control loop issued (NCCL's own kernels excluded). */
 int32_t bdfb_last_launch_count(const bdfb_batch *b);
 
 /* Device time in milliseconds of the last integrate's main kernel, measured
- * with CUDA events on the launch stream (synchronises that stream).       */
+ * with CUDA events on the launch stream (synchronises that stream).  In
+ * GLOBAL_NORM mode: the whole host-driven kernel sequence.                 */
 double bdfb_last_kernel_ms(bdfb_batch *b);
 
 /* Free everything owned by the handle (NULL is a no-op). */

@@ -325,7 +325,7 @@ static int run_global(bdfb_batch* b, const Opts& o, double* y, const double* fex
     a.nst = r.nst; a.nfe = r.nfe; a.nje = r.nje; a.nsetups = r.nsetups; a.nni = r.nni; a.netf = r.netf;
     a.ncfn = r.ncfn; a.nst_max = r.nst; a.nfe_max = r.nfe;
     b->timed = true;
-    b->launches = -1;
+    b->launches = (int)(r.launches + 1);  // + gk_fill_stats
     return BDFB_OK;
   } else {
     return fail(b, BDFB_EUNSUPPORTED, "global-norm mode is implemented for the group models (MECH_H2, MECH_DRM19)");

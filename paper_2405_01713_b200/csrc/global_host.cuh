@@ -28,6 +28,7 @@ struct GlobalResult {
   long long nst, nfe, nje, nsetups, nni, netf, ncfn;
   int q;
   double h, tn;
+  long long launches;
 };
 
 template <class Model>
@@ -43,6 +44,7 @@ struct GlobalRunner {
   const double* atol;
   const double* fext;
   const double* aux;
+  long long launches = 0;
   // scalar state (the listing's)
   double tn = 0, h = 0, hscale = 0, hprime = 0, eta = 1, etamax = ETAMX1, saved_t = 0;
   double tau[QMAX + 2] = {0}, l[QMAX + 1] = {0}, tq[6] = {0};
@@ -98,10 +100,10 @@ struct GlobalRunner {
 
   // WRMS over the whole batch (Eq. 3 with N = n * N_total, R14; order R15)
   double wrms(const double* x) {
-    gk_cellsum<<<gridc(), 128, 0, st>>>(x, B.v.ewt, B.s, n, N);
+    ++launches; gk_cellsum<<<gridc(), 128, 0, st>>>(x, B.v.ewt, B.s, n, N);
     const long long nb = (N + GM_BLK - 1) / GM_BLK;
-    gk_blocksum<<<(unsigned)((nb + 127) / 128), 128, 0, st>>>(B.s, B.P, N);
-    gk_finalsum<<<1, 1, 0, st>>>(B.P, nb, B.sum);
+    ++launches; gk_blocksum<<<(unsigned)((nb + 127) / 128), 128, 0, st>>>(B.s, B.P, N);
+    ++launches; gk_finalsum<<<1, 1, 0, st>>>(B.P, nb, B.sum);
     double S = 0.0;
     cudaMemcpyAsync(&S, B.sum, sizeof(double), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
@@ -111,7 +113,7 @@ struct GlobalRunner {
 
   int rhs(double t, const double* yin, double* fout) {
     cudaMemsetAsync(B.flag, 0, sizeof(int), st);
-    gk_rhs<Model><<<gridg(), 128, smemg(), st>>>(prm, N, t, yin, fext, aux, fout, B.flag);
+    ++launches; gk_rhs<Model><<<gridg(), 128, smemg(), st>>>(prm, N, t, yin, fext, aux, fout, B.flag);
     nfe++;
     int fl = 0;
     cudaMemcpyAsync(&fl, B.flag, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -119,20 +121,20 @@ struct GlobalRunner {
     return allor(fl);
   }
 
-  void ewt_from(const double* y) { gk_ewt<<<gride(), 256, 0, st>>>(B.v.ewt, y, atol, o.rtol, n, N); }
+  void ewt_from(const double* y) { ++launches; gk_ewt<<<gride(), 256, 0, st>>>(B.v.ewt, y, atol, o.rtol, n, N); }
   void rescale() {
-    gk_rescale<<<gridc(), 128, 0, st>>>(B.v, n, N, q, eta);
+    ++launches; gk_rescale<<<gridc(), 128, 0, st>>>(B.v, n, N, q, eta);
     h = hscale * eta;
     hscale = h;
   }
   void predict() {
     tn = tn + h;
     if ((tn - o.tf) * h > 0.0) tn = o.tf;
-    gk_predict<<<gridc(), 128, 0, st>>>(B.v, n, N, q);
+    ++launches; gk_predict<<<gridc(), 128, 0, st>>>(B.v, n, N, q);
   }
   void restore() {
     tn = saved_t;
-    gk_restore<<<gridc(), 128, 0, st>>>(B.v, n, N, q);
+    ++launches; gk_restore<<<gridc(), 128, 0, st>>>(B.v, n, N, q);
   }
 
   void set_bdf() {
@@ -195,7 +197,7 @@ struct GlobalRunner {
         }
       }
       const double A1 = (-alpha0 - alpha1) / prod;
-      gk_increase<<<gridc(), 128, 0, st>>>(B.v, n, N, q, qmax, A1, lc);
+      ++launches; gk_increase<<<gridc(), 128, 0, st>>>(B.v, n, N, q, qmax, A1, lc);
     } else {
       lc.c[2] = 1.0;
       double hsum = 0.0;
@@ -204,7 +206,7 @@ struct GlobalRunner {
         const double xi = hsum / hscale;
         for (int i = j + 2; i >= 2; --i) lc.c[i] = lc.c[i] * xi + lc.c[i - 1];
       }
-      gk_decrease<<<gridc(), 128, 0, st>>>(B.v, n, N, q, lc);
+      ++launches; gk_decrease<<<gridc(), 128, 0, st>>>(B.v, n, N, q, lc);
     }
   }
 
@@ -221,10 +223,10 @@ struct GlobalRunner {
 
   // residual at ycor = acor: yq = zn0 + acor; f = R(tn, yq); del = -gamma f + (rl1 zn1 + acor)
   int residual() {
-    gk_axpby<<<gride(), 256, 0, st>>>(B.v.yq, 1.0, B.v.zn[0], 1.0, B.v.acor, M);
+    ++launches; gk_axpby<<<gride(), 256, 0, st>>>(B.v.yq, 1.0, B.v.zn[0], 1.0, B.v.acor, M);
     const int r = rhs(tn, B.v.yq, B.v.f);
     if (r) return r;
-    gk_residual<<<gride(), 256, 0, st>>>(B.v, M, gamma, rl1);
+    ++launches; gk_residual<<<gride(), 256, 0, st>>>(B.v, M, gamma, rl1);
     return 0;
   }
 
@@ -240,7 +242,7 @@ struct GlobalRunner {
       jcur = 0;
     }
     cudaMemsetAsync(B.flag, 0, sizeof(int), st);
-    gk_setup<Model><<<gridg(), 128, smemg(), st>>>(prm, N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.pos,
+    ++launches; gk_setup<Model><<<gridg(), 128, smemg(), st>>>(prm, N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.pos,
                                                    B.perm, B.invd, B.flag);
     int fl = 0;
     cudaMemcpyAsync(&fl, B.flag, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -273,7 +275,7 @@ struct GlobalRunner {
         for (;;) {
           nni++;
           const double sc2 = (gamrat != 1.0) ? 2.0 / (1.0 + gamrat) : 1.0;
-          gk_solve<Model><<<gridg(), 128, smemg(), st>>>(N, sc2, B.LU, B.pos, B.perm, B.invd, B.v.del, B.v.acor,
+          ++launches; gk_solve<Model><<<gridg(), 128, smemg(), st>>>(N, sc2, B.LU, B.pos, B.perm, B.invd, B.v.del, B.v.acor,
                                                          B.v.tmp);
           const double del = wrms(B.v.tmp);
           if (m > 0) crate = fmax(CRDOWN * crate, del / dprev);
@@ -326,7 +328,7 @@ struct GlobalRunner {
       double pw = 1.0;
       for (int k = 0; k < L; ++k) pw = pw * hr;
       const double cquot = (tq[5] / saved_tq5) * pw;
-      gk_axpby<<<gride(), 256, 0, st>>>(B.v.tmp, -cquot, B.v.zn[qmax], 1.0, B.v.acor, M);
+      ++launches; gk_axpby<<<gride(), 256, 0, st>>>(B.v.tmp, -cquot, B.v.zn[qmax], 1.0, B.v.acor, M);
       const double dup = wrms(B.v.tmp) * tq[3];
       etaqp1 = 1.0 / (root_host(BIAS3 * dup, L + 1) + ADDON);
     }
@@ -343,7 +345,7 @@ struct GlobalRunner {
     } else {
       eta = etaqp1;
       qprime = q + 1;
-      gk_axpby<<<gride(), 256, 0, st>>>(B.v.zn[qmax], 1.0, B.v.acor, 0.0, nullptr, M);
+      ++launches; gk_axpby<<<gride(), 256, 0, st>>>(B.v.zn[qmax], 1.0, B.v.acor, 0.0, nullptr, M);
     }
     set_eta();
   }
@@ -353,7 +355,7 @@ struct GlobalRunner {
     const double tround = UROUND * fmax(fabs(o.t0), fabs(o.tf));
     const double hlb = 100.0 * tround;
     cudaMemsetAsync(B.ubuf, 0, sizeof(unsigned long long), st);
-    gk_hubinv<<<gride(), 256, 0, st>>>(B.v, M, B.ubuf);
+    ++launches; gk_hubinv<<<gride(), 256, 0, st>>>(B.v, M, B.ubuf);
     unsigned long long bits = 0;
     cudaMemcpyAsync(&bits, B.ubuf, sizeof(bits), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
@@ -369,13 +371,13 @@ struct GlobalRunner {
       int ok = 0;
       double ydd = 0.0;
       for (int count2 = 1; count2 <= HIN_ITERS; ++count2) {
-        gk_axpby<<<gride(), 256, 0, st>>>(B.v.yq, hg, B.v.zn[1], 1.0, B.v.zn[0], M);
+        ++launches; gk_axpby<<<gride(), 256, 0, st>>>(B.v.yq, hg, B.v.zn[1], 1.0, B.v.zn[0], M);
         const int r = rhs(o.t0 + hg, B.v.yq, B.v.f);
         if (r == 0) {
           const double ih = 1.0 / hg;
           // tmp = (f - f0) * (1/hg)
-          gk_axpby<<<gride(), 256, 0, st>>>(B.v.tmp, 1.0, B.v.f, -1.0, B.v.zn[1], M);
-          gk_axpby<<<gride(), 256, 0, st>>>(B.v.tmp, ih, B.v.tmp, 0.0, nullptr, M);
+          ++launches; gk_axpby<<<gride(), 256, 0, st>>>(B.v.tmp, 1.0, B.v.f, -1.0, B.v.zn[1], M);
+          ++launches; gk_axpby<<<gride(), 256, 0, st>>>(B.v.tmp, ih, B.v.tmp, 0.0, nullptr, M);
           ydd = wrms(B.v.tmp);
           ok = 1;
           break;
@@ -497,7 +499,7 @@ struct GlobalRunner {
       hscale = h;
       qwait = LONG_WAIT;
       if (rhs(tn, B.v.zn[0], B.v.f)) return ST_RHS_FAIL;
-      gk_axpby<<<gride(), 256, 0, st>>>(B.v.zn[1], h, B.v.f, 0.0, nullptr, M);
+      ++launches; gk_axpby<<<gride(), 256, 0, st>>>(B.v.zn[1], h, B.v.f, 0.0, nullptr, M);
     }
     nst++;
     for (int i = q; i >= 2; --i) tau[i] = tau[i - 1];
@@ -507,7 +509,7 @@ struct GlobalRunner {
     const int save = (qwait == 1 && q != qmax);
     GCoef lco{};
     for (int j = 0; j <= QMAX; ++j) lco.c[j] = l[j];
-    gk_complete<<<gridc(), 128, 0, st>>>(B.v, n, N, q, lco, save, qmax);
+    ++launches; gk_complete<<<gridc(), 128, 0, st>>>(B.v, n, N, q, lco, save, qmax);
     if (save) saved_tq5 = tq[5];
     prepare_next(dsm);
     etamax = ETAMX2;
@@ -520,8 +522,8 @@ struct GlobalRunner {
     res.tn = o.t0;
     // non-finite input anywhere -> the batch is not integrated
     cudaMemsetAsync(B.flag, 0, sizeof(int), st);
-    gk_finite<<<gride(), 256, 0, st>>>(y, M, B.flag);
-    if (fext) gk_finite<<<gride(), 256, 0, st>>>(fext, M, B.flag);
+    ++launches; gk_finite<<<gride(), 256, 0, st>>>(y, M, B.flag);
+    if (fext) { ++launches; gk_finite<<<gride(), 256, 0, st>>>(fext, M, B.flag); }
     int fl = 0;
     cudaMemcpyAsync(&fl, B.flag, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
@@ -539,7 +541,7 @@ struct GlobalRunner {
     if (status == ST_OK) {
       if (h0 > o.tf - o.t0) h0 = o.tf - o.t0;
       if (o.hmax > 0.0 && h0 > o.hmax) h0 = o.hmax;
-      gk_axpby<<<gride(), 256, 0, st>>>(B.v.zn[1], h0, B.v.zn[1], 0.0, nullptr, M);
+      ++launches; gk_axpby<<<gride(), 256, 0, st>>>(B.v.zn[1], h0, B.v.zn[1], 0.0, nullptr, M);
       h = hscale = hprime = h0;
       q = qprime = 1;
       L = 2;
@@ -566,7 +568,7 @@ struct GlobalRunner {
     cudaStreamSynchronize(st);
     res.status = status;
     res.nst = nst; res.nfe = nfe; res.nje = nje; res.nsetups = nsetups; res.nni = nni; res.netf = netf;
-    res.ncfn = ncfn; res.q = q; res.h = h; res.tn = tn;
+    res.ncfn = ncfn; res.q = q; res.h = h; res.tn = tn; res.launches = launches;
     return res;
   }
 };
