@@ -1,0 +1,37 @@
+"""Aggregate an ncu cuda,sass source export of bdf_tpc.cuh by function line ranges (plus whole other files)."""
+import csv, sys, collections, bisect
+csv.field_size_limit(1 << 30)
+path = sys.argv[1]
+ranges = [(97, "tpc_factor"), (171, "tpc_solve"), (206, "coop_factor"), (275, "wrms"), (286, "restore"),
+          (305, "set_bdf"), (351, "increase_bdf"), (377, "decrease_bdf"), (394, "adjust/set_eta/rescale"),
+          (420, "prepare_next"), (458, "idx/req_res"), (477, "consume"), (560, "hin/start/setup_done/decide"),
+          (610, "solve"), (650, "nfail"), (671, "errtest"), (765, "step_top"), (789, "attempt"), (845, "store"),
+          (876, "load"), (927, "ts_of/ws_of"), (933, "trip"), (941, "SETUP_J stage"), (974, "SETUP_LU stage"),
+          (1010, "trip tail"), (1040, "kernel")]
+starts = [r[0] for r in ranges]
+agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0])
+fname = None; hdr = None
+with open(path, newline="") as f:
+    for r in csv.reader(f):
+        if not r: continue
+        if r[0] == "File Path": fname = r[1].split("/")[-1]; continue
+        if r[0] == "Line No": hdr = r; continue
+        if hdr is None: continue
+        try: line = int(r[0])
+        except ValueError: continue
+        d = dict(zip(hdr, r))
+        def num(k):
+            try:
+                return float(d.get(k, 0) or 0)
+            except ValueError:
+                return 0.0
+        smp, ie, te = num("Warp Stall Sampling (All Samples)"), num("Instructions Executed"), num("Thread Instructions Executed")
+        if fname == "bdf_tpc.cuh":
+            i = bisect.bisect_right(starts, line) - 1
+            key = "tpc:" + (ranges[i][1] if i >= 0 else "head")
+        else:
+            key = fname
+        a = agg[key]; a[0] += smp; a[1] += ie; a[2] += te
+ts = sum(a[0] for a in agg.values()) or 1; ti = sum(a[1] for a in agg.values()) or 1
+for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"{k:34s} samples {100*a[0]/ts:5.1f}%  inst {100*a[1]/ti:5.1f}% ({a[1]:.3e})  thr/inst {a[2]/max(a[1],1):5.1f}")

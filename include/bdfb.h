@@ -76,6 +76,13 @@ extern "C" {
 #define BDFB_MODE_PER_CELL 0
 #define BDFB_MODE_GLOBAL_NORM 1
 
+/* per-cell kernel organisation for the mechanism models (bdfb_set_kernel) */
+#define BDFB_KERNEL_AUTO 0     /* = THREAD                                              */
+#define BDFB_KERNEL_THREAD 1   /* one cell per thread, straight-line generated RHS/J,
+                                  per-thread-slot device workspace (csrc/bdf_tpc.cuh)    */
+#define BDFB_KERNEL_GROUP 2    /* one cell per group of 16/32 lanes, state in shared
+                                  memory (csrc/bdf_group.cuh; round-1 design)           */
+
 typedef struct bdfb_batch bdfb_batch;
 
 /* Nyx KWH96-form heating/cooling constants. */
@@ -139,6 +146,22 @@ int bdfb_set_model(bdfb_batch *b, int32_t model_id, const void *params, size_t b
  * the single-GPU order).  Only valid for BDFB_MODE_GLOBAL_NORM handles.      */
 int bdfb_set_comm(bdfb_batch *b, const void *nccl_unique_id, int32_t nranks, int32_t rank,
                   int64_t ncells_total);
+
+/* Choose the per-cell kernel organisation (BDFB_KERNEL_*) for the mechanism
+ * models; other models ignore it.  May be called before or after
+ * bdfb_set_model; the THREAD kernel's workspace (about 8 (12 n + 2 n^2)
+ * bytes per resident thread: Nordsieck history, weights, J, LU) is
+ * allocated here or in bdfb_set_model, never in bdfb_integrate.
+ * Both kernels run the same algorithm; they differ in the WRMS summation
+ * order (reading R15, see bdfb_wrms_group) and hence in rounding.
+ * Returns BDFB_EINVAL for an unknown id, BDFB_ENOMEM.                       */
+int bdfb_set_kernel(bdfb_batch *b, int32_t kernel);
+
+/* The lane-group size G whose WRMS summation order (reading R15: lane l sums
+ * components i = l (mod G) in increasing i, then an xor butterfly G/2..1)
+ * the selected model/kernel uses; 1 = plain sequential sum.  0 if no model
+ * is set.  The oracle reproduces the order from this value.                */
+int32_t bdfb_wrms_group(const bdfb_batch *b);
 
 /* Attach (or detach with NULL) caller-owned per-cell statistics arrays that
  * the next bdfb_integrate fills.  The struct is copied.                     */
@@ -209,7 +232,9 @@ int bdfb_eval_jac(bdfb_batch *b, double t, const double *y, const double *aux, d
 
 /* Batched LU with partial pivoting + solve, the integrator's own routine
  * (listing LU_FACTOR / LU_SOLVE).  For each of N systems of size
- * n (n in 1..32): M[(i*n + j)*N + c] (device, in/out: the LU factors in
+ * n (n in 1..32; n >= 5 runs the thread-per-cell routine of the mechanism
+ * integrator, n <= 4 the shared-memory routine of the small models):
+ * M[(i*n + j)*N + c] (device, in/out: the LU factors in
  * LAPACK getrf form, rows in pivoted order), piv[k*N + c] (device int32,
  * getrf pivot indices), b[i*N + c] (device, in/out: the solution),
  * info[c] (device int32: 0, or k+1 when pivot k is exactly zero).           */

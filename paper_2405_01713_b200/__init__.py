@@ -105,6 +105,16 @@ class Batch:
         _check(self._L.bdfb_set_model(self.h, mid, buf, size), self.h)
         self.model = model
 
+    def set_kernel(self, kernel):
+        """Per-cell kernel for the mechanism models: "thread" (default) or "group" (bdfb_set_kernel)."""
+        kid = {"auto": L.KERNEL_AUTO, "thread": L.KERNEL_THREAD, "group": L.KERNEL_GROUP}[kernel]
+        _check(self._L.bdfb_set_kernel(self.h, kid), self.h)
+
+    @property
+    def wrms_group(self):
+        """Lane-group size of the WRMS summation order (reading R15) the selected kernel uses."""
+        return int(self._L.bdfb_wrms_group(self.h))
+
     def set_comm(self, unique_id: bytes, nranks: int, rank: int, ncells_total: int):
         """Global-norm mode across ranks: NCCL communicator from a 128-byte ncclUniqueId
         (created on rank 0, broadcast by the caller, e.g. with torch.distributed)."""

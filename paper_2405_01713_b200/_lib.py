@@ -14,12 +14,13 @@ LIB_PATH = os.environ.get("BDFB_LIB") or os.path.join(PKG, "libbdfb.so")   # BDF
 MODEL_LINEAR, MODEL_ROBERTSON, MODEL_NYX_KWH, MODEL_MECH_H2, MODEL_MECH_DRM19 = 0, 1, 2, 3, 4
 LAYOUT_YC, LAYOUT_CY = 0, 1
 MODE_PER_CELL, MODE_GLOBAL_NORM = 0, 1
+KERNEL_AUTO, KERNEL_THREAD, KERNEL_GROUP = 0, 1, 2
 
 # every symbol include/bdfb.h declares
 SYMBOLS = ["bdfb_default_options", "bdfb_create", "bdfb_set_model", "bdfb_set_cell_stats", "bdfb_integrate",
            "bdfb_integrate_host", "bdfb_get_stats", "bdfb_last_launch_count", "bdfb_last_kernel_ms",
            "bdfb_destroy", "bdfb_last_error", "bdfb_version", "bdfb_eval_rhs", "bdfb_eval_jac",
-           "bdfb_lu_factor_solve", "bdfb_probe_fp64", "bdfb_set_comm"]
+           "bdfb_lu_factor_solve", "bdfb_probe_fp64", "bdfb_set_comm", "bdfb_set_kernel", "bdfb_wrms_group"]
 
 
 class Options(C.Structure):
@@ -92,6 +93,10 @@ def lib():
     L.bdfb_lu_factor_solve.argtypes = [i32, i64, vp, vp, vp, vp, vp]
     L.bdfb_set_comm.restype = C.c_int
     L.bdfb_set_comm.argtypes = [vp, vp, i32, i32, i64]
+    L.bdfb_set_kernel.restype = C.c_int
+    L.bdfb_set_kernel.argtypes = [vp, i32]
+    L.bdfb_wrms_group.restype = i32
+    L.bdfb_wrms_group.argtypes = [vp]
     L.bdfb_probe_fp64.restype = C.c_int
     L.bdfb_probe_fp64.argtypes = [i32, dp, C.POINTER(C.c_double), C.POINTER(C.c_int32)]
     _lib = L

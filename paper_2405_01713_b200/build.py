@@ -19,32 +19,49 @@ LIB = os.path.join(PKG, "libbdfb.so")
 CSRC = os.path.join(PKG, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "--shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-lnccl"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+UNITS = ["bdfb.cu", "tpc.cu"]          # translation units, compiled in parallel
 
 
 def sources():
     return (glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
             glob.glob(os.path.join(REPO, "include", "*.h")) + glob.glob(os.path.join(REPO, "mechanisms", "*.json")) +
-            [os.path.join(PKG, "codegen", "gen_mech.py"), __file__])
+            [os.path.join(PKG, "codegen", "gen_mech.py"), os.path.join(PKG, "codegen", "gen_tpc.py"), __file__])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     sys.path.insert(0, REPO)
-    from paper_2405_01713_b200.codegen import gen_mech
+    from paper_2405_01713_b200.codegen import gen_mech, gen_tpc
     gen_mech.main([])
+    gen_tpc.main([])
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(s) <= t for s in sources()):
             return LIB
-    cmd = [NVCC] + ARCH + FLAGS + ["-o", LIB + ".tmp", os.path.join(CSRC, "bdfb.cu")]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    objs, procs = [], []
+    for u in UNITS:
+        obj = os.path.join(PKG, "build", u.replace(".cu", ".o"))
+        os.makedirs(os.path.dirname(obj), exist_ok=True)
+        objs.append(obj)
+        procs.append(subprocess.Popen([NVCC] + ARCH + FLAGS + ["-c", "-o", obj, os.path.join(CSRC, u)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    info, err = [], None
+    for u, p in zip(UNITS, procs):
+        out, e = p.communicate()
+        info.append(f"==== {u}\n{out}{e}")
+        if p.returncode != 0:
+            err = f"nvcc failed on {u}:\n" + e[-4000:]
     with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-        f.write(r.stdout + r.stderr)
+        f.write("".join(info))
+    if err:
+        raise RuntimeError(err)
+    r = subprocess.run([NVCC] + ARCH + ["--shared", "-o", LIB + ".tmp"] + objs + ["-lnccl"], capture_output=True,
+                       text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stderr[-4000:])
+        raise RuntimeError("link failed:\n" + r.stderr[-4000:])
     os.replace(LIB + ".tmp", LIB)
     if verbose:
-        print(r.stderr)
+        print("".join(info))
     return LIB
 
 

@@ -1,17 +1,39 @@
-"""Straight-line, thread-per-cell RHS for a mechanism table (experimental).
+"""Mechanism table (mechanisms/<name>.json) -> straight-line, thread-per-cell
+RHS and analytic Jacobian (paper_2405_01713_b200/csrc/gen/tpc_<name>.cuh).
 
-Emits csrc/gen/tpc_<name>.cuh with
-    __device__ int tpc_rhs_<name>(const double* y, double rho, double* f)
-where y, f are per-thread arrays of N doubles (registers after inlining):
-every constant (Arrhenius parameters, NASA-7 coefficients, stoichiometry,
-efficiencies) is folded into the code, so a warp evaluates 32 cells with
-no index arithmetic or table loads.  Same physics as csrc/mech_model.cuh.
+Build-time only.  The paper's chemistry Jacobians are "generated offline,
+mechanism-specific"; here every constant of the mechanism
+(Arrhenius parameters, NASA-7 coefficients, stoichiometry, third-body
+efficiencies, Troe parameters) is folded into generated code, so one thread
+evaluates one cell with no table loads and no index arithmetic, and a warp
+evaluates 32 cells in lock step (the per-cell integrator of csrc/bdf_tpc.cuh).
+
+Physics (the paper's 0-D reactor "assumed constant internal
+energy"; split form P:196-201) -- the same as csrc/mech_model.cuh:
+  C_k = rho Y_k / W_k;  k_f = exp(ln A + beta ln T - Ea/(R_c T));
+  [M] = sum_k alpha_k C_k;  Lindemann / Troe falloff;
+  1/K_c = prod_reac e^{-g/RT} / prod_prod e^{-g/RT} * (R T / p_atm)^{dnu};
+  q = k_f (prod_reac C - prod_prod C / K_c)  (times [M] for third body);
+  wdot_k = sum_r nu_rk q_r;  dY_k/dt = W_k wdot_k / rho;
+  dT/dt = -sum_k u_k wdot_k / (rho cv),  u_k = (h_k/RT - 1) R T.
+
+Emitted device functions (struct Tpc_<name>):
+  rhs(y[N], rho, f[N]) -> 0, or 1 if T <= 0 (recoverable RHS failure)
+      y, f: per-thread register arrays after inlining.
+  jac<SS>(y, rho, J, sc, Srt) -> same status (element stride S = SS, or Srt if SS = 0)
+      y: N doubles at y[k*S]; J: row-major N x N at J[(i*N+j)*S];
+      sc: scratch (NSC doubles at sc[m*S]), here the LU area that the matrix
+      setup overwrites right after.  S = the workspace slot stride.
+      Column-wise: pass 1 stores per-reaction kf, kr, dq/dT (and dq/d[M]);
+      pass 2 builds one column of dwdot/dC in registers per species and
+      the temperature row from it (chain rule through u_k and cv).
 """
 from __future__ import annotations
 
 import json
 import math
 import os
+import struct
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -20,53 +42,142 @@ REPO = os.path.dirname(PKG)
 RC = 1.98720425864083
 RU = 8.31446261815324e7
 PATM = 1013250.0
+LN10 = 2.302585092994045684
 
 
-def d(x):
-    return repr(float(x))
+def lit(x):
+    x = float(x)
+    return repr(x) if math.isfinite(x) else ("1e308" if x > 0 else "-1e308")
+
+
+class Pool:
+    """Floating constants of the generated code.  Values exactly representable in fp32
+    are emitted as literals (SASS encodes them as immediates); every other constant
+    goes to a __constant__ table, so FP64 instructions take it as a constant-bank
+    operand instead of materialising it with two uniform-register moves."""
+
+    def __init__(self, name):
+        self.name = name
+        self.vals = []
+        self.idx = {}
+
+    def __call__(self, x):
+        x = float(x)
+        if not math.isfinite(x) or struct.unpack("f", struct.pack("f", x))[0] == x:
+            return lit(x)
+        key = struct.pack("d", x)
+        if key not in self.idx:
+            self.idx[key] = len(self.vals)
+            self.vals.append(x)
+        return f"kc_{self.name}[{self.idx[key]}]"
+
+    def table(self):
+        body = ",\n  ".join(repr(v) for v in self.vals) or "0.0"
+        return f"__constant__ double kc_{self.name}[{max(1, len(self.vals))}] = {{\n  {body}}};\n"
+
+
+d = lit   # rebound per mechanism in generate()
+
+
+def _nasa(A, tab, tm, body):
+    """Emit `body(k, coeffs, indent)` for both NASA-7 ranges (all Tmid equal)."""
+    A(f"  if (T < {d(tm)}) {{\n")
+    for k, s in enumerate(tab["species"]):
+        body(k, s["nasa"]["low"])
+    A("  } else {\n")
+    for k, s in enumerate(tab["species"]):
+        body(k, s["nasa"]["high"])
+    A("  }\n")
+
+
+def _rate(x, lnT="lnT", invT="invT", low=False):
+    p = x["low"] if low else x
+    if not low and x["b"] == 0 and x["Ea"] == 0:
+        return d(x["A"])
+    return f"fexp({d(math.log(p['A']))} + {d(p['b'])} * {lnT} - {d(p['Ea'] / RC)} * {invT})"
+
+
+def _prod(names):
+    return " * ".join(names) if names else "1.0"
 
 
 def generate(name, out_dir):
+    global d
+    d = Pool(name)
     tab = json.load(open(os.path.join(REPO, "mechanisms", name + ".json")))
     sp = [s["name"] for s in tab["species"]]
     idx = {s: i for i, s in enumerate(sp)}
     K = len(sp)
     N = K + 1
+    W = [s["W"] for s in tab["species"]]
+    rx = tab["reactions"]
+    NR = len(rx)
+    tmids = {s["nasa"]["Tmid"] for s in tab["species"]}
+    assert len(tmids) == 1, "generator assumes one common Tmid"
+    tm = tmids.pop()
+    tb = [r for r, x in enumerate(rx) if x["type"] != "elementary"]
+    NTB = len(tb)
+    # scratch layout of jac(): kf[NR], kr[NR], dqdT[NR], dqdM[NTB], h[K], cvk[K]
+    O_KF, O_KR, O_DT, O_DM = 0, NR, 2 * NR, 3 * NR
+    O_H = 3 * NR + NTB
+    O_CV = O_H + K
+    NSC = O_CV + K
+    assert NSC <= N * N, "jac scratch must fit in the LU area"
+    nu = []
+    for x in rx:
+        v = {}
+        for s in x["reactants"]:
+            v[idx[s]] = v.get(idx[s], 0) - 1
+        for s in x["products"]:
+            v[idx[s]] = v.get(idx[s], 0) + 1
+        nu.append({k: c for k, c in v.items() if c != 0})
+
     L = []
     A = L.append
-    A(f"// GENERATED by codegen/gen_tpc.py from mechanisms/{name}.json -- do not edit.\n#pragma once\n")
-    A("namespace bdfb {\n")
-    A(f"__device__ __forceinline__ int tpc_rhs_{name}(const double* y, double rho, double* f) {{\n")
-    A(f"  const double T = y[{K}];\n  if (!(T > 0.0)) return 1;\n")
-    A("  const double lnT = log(T), invT = 1.0 / T, T2 = T * T, T3 = T2 * T, T4 = T3 * T;\n")
-    A(f"  const double cRT = {d(RU / PATM)} * T, icRT = 1.0 / cRT;\n")
-    for k, s in enumerate(tab["species"]):
-        A(f"  const double C{k} = rho * y[{k}] * {d(1.0 / s['W'])};\n")
-    # g/RT and e^{-g/RT}: all Tmid equal in our tables -> one branch
-    tmids = {s["nasa"]["Tmid"] for s in tab["species"]}
-    assert len(tmids) == 1
-    tm = tmids.pop()
-    for k in range(K):
-        A(f"  double eg{k};\n")
-    for branch, key in (("if (T < %s) {" % d(tm), "low"), ("} else {", "high")):
-        A(f"  {branch}\n")
-        for k, s in enumerate(tab["species"]):
-            a = s["nasa"][key]
-            # g/RT = a0 (1 - lnT) - a1 T/2 - a2 T^2/6 - a3 T^3/12 - a4 T^4/20 + a5/T - a6
-            A(f"    eg{k} = exp(-({d(a[0])} * (1.0 - lnT) + {d(-a[1] / 2)} * T + {d(-a[2] / 6)} * T2 + "
-              f"{d(-a[3] / 12)} * T3 + {d(-a[4] / 20)} * T4 + {d(a[5])} * invT - {d(a[6])}));\n")
-    A("  }\n")
-    for k in range(K):
-        A(f"  double w{k} = 0.0;\n")
-    for r, x in enumerate(tab["reactions"]):
+    A(f"// GENERATED by codegen/gen_tpc.py from mechanisms/{name}.json -- do not edit.\n")
+    A(f"// {tab.get('provenance', '')}\n#pragma once\n#include \"../fexp.cuh\"\nnamespace bdfb {{\n")
+    A("@@TABLE@@")
+    A(f"struct Tpc_{name} {{\n")
+    A(f"  static constexpr int K = {K}, N = {N}, NR = {NR}, NTB = {NTB}, NSC = {NSC};\n")
+    A(f"  static constexpr const char* NAME = \"{name}\";\n")
+
+    def thermo_common(A):
+        A(f"  const double T = y{K};\n  if (!(T > 0.0)) return 1;\n")
+        A("  const double lnT = log(T), invT = 1.0 / T, T2 = T * T, T3 = T2 * T, T4 = T3 * T;\n")
+        A(f"  const double cRT = T * {d(RU / PATM)}, icRT = {d(PATM / RU)} * invT;\n")
+        for k in range(K):
+            A(f"  const double C{k} = rho * y{k} * {d(1.0 / W[k])};\n")
+        for k in range(K):
+            A(f"  double eg{k};\n")
+
+    def eg_body(k, a):
+        # -g/RT = -(h/RT - s/R) = a0 (lnT - 1) + a1 T/2 + a2 T^2/6 + a3 T^3/12 + a4 T^4/20 - a5/T + a6
+        A(f"    eg{k} = fexp({d(a[0])} * (lnT - 1.0) + {d(a[1] / 2)} * T + {d(a[2] / 6)} * T2 + {d(a[3] / 12)} * T3 + "
+          f"{d(a[4] / 20)} * T4 - {d(a[5])} * invT + {d(a[6])});\n")
+
+    def reaction(A, r, x, deriv):
+        """Emit the rate of progress q of reaction r (and its derivative data if deriv)."""
         reac = [idx[s] for s in x["reactants"]]
         prod = [idx[s] for s in x["products"]]
         typ = x["type"]
-        A(f"  {{ // {x['equation']}\n")
-        if x["b"] == 0 and x["Ea"] == 0:
-            A(f"    double k = {d(x['A'])};\n")
+        dn = len(prod) - len(reac)
+        A(f"  {{ // R{r}: {x['equation']}\n")
+        A(f"    const double kinf = {_rate(x)};\n")
+        const = x["b"] == 0 and x["Ea"] == 0
+        A(f"    const double Cf = {_prod([f'C{i}' for i in reac])}, Cr = {_prod([f'C{i}' for i in prod])};\n")
+        fac = {0: "", 1: " * cRT", -1: " * icRT", 2: " * (cRT * cRT)", -2: " * (icRT * icRT)"}[dn]
+        if x["reversible"]:
+            A(f"    const double invKc = ({_prod([f'eg{i}' for i in reac])}) / ({_prod([f'eg{i}' for i in prod])}){fac};\n")
         else:
-            A(f"    double k = exp({d(math.log(x['A']))} + {d(x['b'])} * lnT - {d(x['Ea'] / RC)} * invT);\n")
+            A("    const double invKc = 0.0;\n")
+        A("    const double net = Cf - Cr * invKc;\n")
+        if deriv:
+            A(f"    const double dlnkinf = {'0.0' if const else f'({d(x['b'])} + {d(x['Ea'] / RC)} * invT) * invT'};\n")
+            if x["reversible"]:
+                hs = " + ".join([f"sc[{O_H + i}*S]" for i in prod]) + " - " + " - ".join([f"sc[{O_H + i}*S]" for i in reac])
+                A(f"    const double dlnKc = ({hs} - {d(dn)}) * invT;\n")
+            else:
+                A("    const double dlnKc = 0.0;\n")
         if typ != "elementary":
             eff = x["efficiencies"]
             terms = []
@@ -77,65 +188,218 @@ def generate(name, out_dir):
                 elif e != 0.0:
                     terms.append(f"{d(e)} * C{idx[s]}")
             A(f"    const double M = {' + '.join(terms)};\n")
-            if typ == "three_body":
-                A("    k *= M;\n")
-            else:
-                lo = x["low"]
-                A(f"    const double k0 = exp({d(math.log(lo['A']))} + {d(lo['b'])} * lnT - {d(lo['Ea'] / RC)} * invT);\n")
-                A("    const double Pr = k0 * M / k;\n")
-                if typ == "troe":
-                    t = x["troe"]
-                    fc = f"{d(1 - t[0])} * exp(-T * {d(1 / t[1])}) + {d(t[0])} * exp(-T * {d(1 / t[2])})"
+        if typ in ("elementary", "three_body"):
+            Mf = "M * " if typ == "three_body" else ""
+            A(f"    const double kf = {Mf}kinf;\n")
+            if deriv:
+                A(f"    const double dkdT = kinf * dlnkinf;\n")
+                if typ == "three_body":
+                    A(f"    sc[{O_DM + tb.index(r)}*S] = kinf * net;\n")
+                A(f"    sc[{O_DT + r}*S] = {'M * ' if typ == 'three_body' else ''}(dkdT * net + kinf * Cr * invKc * dlnKc);\n")
+        else:
+            lo = x["low"]
+            A(f"    const double k0 = {_rate(x, low=True)};\n")
+            A("    const double Pr = k0 * M / kinf;\n")
+            A("    const double Pr1 = 1.0 / (1.0 + Pr);\n")
+            if typ == "troe":
+                t = x["troe"]
+                A(f"    const double e3 = fexp(-T * {d(1.0 / t[1])}), e1 = fexp(-T * {d(1.0 / t[2])});\n")
+                fc = f"{d(1 - t[0])} * e3 + {d(t[0])} * e1"
+                if len(t) == 4:
+                    A(f"    const double e2 = fexp({d(-t[3])} * invT);\n")
+                    fc += " + e2"
+                A(f"    const double Fc = {fc};\n")
+                A("    const double lFc = log10(Fc);\n")
+                A(f"    const double cc = {d(-0.4)} - {d(0.67)} * lFc, nn = 0.75 - {d(1.27)} * lFc;\n")
+                A("    const double xx = log10(Pr) + cc;\n")
+                A(f"    const double den = 1.0 / (nn - {d(0.14)} * xx);\n")
+                A("    const double f1 = xx * den;\n")
+                A("    const double q1 = 1.0 / (1.0 + f1 * f1);\n")
+                A(f"    const double F = fexp(lFc * q1 * {d(LN10)});\n")
+                if deriv:
+                    dfc = f"-({d((1 - t[0]) / t[1])}) * e3 - ({d(t[0] / t[2])}) * e1"
                     if len(t) == 4:
-                        fc += f" + exp({d(-t[3])} * invT)"
-                    A(f"    const double lFc = log10({fc});\n")
-                    A("    const double cc = -0.4 - 0.67 * lFc, nn = 0.75 - 1.27 * lFc;\n")
-                    A("    const double xx = log10(Pr) + cc;\n")
-                    A("    const double f1 = xx / (nn - 0.14 * xx);\n")
-                    A("    const double F = exp(2.302585092994045684 * lFc / (1.0 + f1 * f1));\n")
-                    A("    k = k * (Pr / (1.0 + Pr)) * F;\n")
-                else:
-                    A("    k = k * (Pr / (1.0 + Pr));\n")
-        cf = " * ".join(f"C{i}" for i in reac)
-        cr = " * ".join(f"C{i}" for i in prod)
-        er = " * ".join(f"eg{i}" for i in reac)
-        ep = " * ".join(f"eg{i}" for i in prod)
-        dn = len(prod) - len(reac)
-        fac = {0: "", 1: " * cRT", -1: " * icRT", 2: " * cRT * cRT", -2: " * icRT * icRT"}[dn]
-        A(f"    const double q = k * ({cf} - {cr} * (({er}) / ({ep})){fac});\n")
-        net = {}
-        for i in reac:
-            net[i] = net.get(i, 0) - 1
-        for i in prod:
-            net[i] = net.get(i, 0) + 1
-        for i, v in sorted(net.items()):
+                        dfc += f" + ({d(t[3])}) * invT * invT * e2"
+                    A(f"    const double dFc = {dfc};\n")
+                    A("    const double dlFdlPr = -lFc * 2.0 * f1 * (nn * den * den) * q1 * q1;\n")
+                    A(f"    const double df1dlFc = ({d(-0.67)} * (nn - {d(0.14)} * xx) - xx * {d(-1.27 + 0.14 * 0.67)}) * den * den;\n")
+                    A("    const double dlFdlFc = q1 - lFc * 2.0 * f1 * df1dlFc * q1 * q1;\n")
+                    A(f"    const double dFdT = F * {d(LN10)} * dlFdlFc * (dFc / (Fc * {d(LN10)}));\n")
+            else:
+                A("    const double F = 1.0;\n")
+                if deriv:
+                    A("    const double dlFdlPr = 0.0, dFdT = 0.0;\n")
+            A("    const double k = kinf * (Pr * Pr1 * F);\n")
+            A("    const double kf = k;\n")
+            if deriv:
+                A("    const double dgdPr = F * Pr1 * Pr1 + Pr1 * F * dlFdlPr;\n")
+                A(f"    const double dlnk0 = ({d(lo['b'])} + {d(lo['Ea'] / RC)} * invT) * invT;\n")
+                A("    const double dkdT = k * dlnkinf + kinf * dgdPr * Pr * (dlnk0 - dlnkinf) + kinf * Pr * Pr1 * dFdT;\n")
+                A(f"    sc[{O_DM + tb.index(r)}*S] = k0 * dgdPr * net;\n")
+                A(f"    sc[{O_DT + r}*S] = dkdT * net + k * Cr * invKc * dlnKc;\n")
+        A("    const double q = kf * net;\n")
+        if deriv:
+            A(f"    sc[{O_KF + r}*S] = kf;\n    sc[{O_KR + r}*S] = kf * invKc;\n")
+        for i, v in sorted(nu[r].items()):
             if v == 1:
                 A(f"    w{i} += q;\n")
             elif v == -1:
                 A(f"    w{i} -= q;\n")
-            elif v != 0:
-                A(f"    w{i} += {d(v)} * q;\n")
+            else:
+                A(f"    w{i} = fma({d(v)}, q, w{i});\n")
         A("  }\n")
-    # outputs and temperature equation (cv and u recomputed from the polynomials)
+
+    # ------------------------------------------------------------------ rhs
+    A(f"  __device__ __forceinline__ static int rhs(const double (&yv)[{N}], double rho, double (&f)[{N}]) {{\n")
+    for k in range(N):
+        A(f"  const double y{k} = yv[{k}];\n")
+    thermo_common(A)
+    _nasa(A, tab, tm, eg_body)
+    for k in range(K):
+        A(f"  double w{k} = 0.0;\n")
+    for r, x in enumerate(rx):
+        reaction(A, r, x, False)
     A("  double cv = 0.0, su = 0.0;\n")
-    for branch, key in (("if (T < %s) {" % d(tm), "low"), ("} else {", "high")):
-        A(f"  {branch}\n")
-        for k, s in enumerate(tab["species"]):
-            a = s["nasa"][key]
-            A(f"    cv += y[{k}] * ({d(a[0] - 1)} + {d(a[1])} * T + {d(a[2])} * T2 + {d(a[3])} * T3 + "
-              f"{d(a[4])} * T4) * {d(RU / s['W'])};\n")
-            A(f"    su += ({d(a[0] - 1)} + {d(a[1] / 2)} * T + {d(a[2] / 3)} * T2 + {d(a[3] / 4)} * T3 + "
-              f"{d(a[4] / 5)} * T4 + {d(a[5])} * invT) * w{k};\n")
-    A("  }\n")
-    for k, s in enumerate(tab["species"]):
-        A(f"  f[{k}] = {d(s['W'])} * w{k} / rho;\n")
-    A(f"  f[{K}] = -su * {d(RU)} * T / (rho * cv);\n  return 0;\n}}\n}}  // namespace\n")
+
+    def tail_body(k, a):
+        A(f"    cv = fma(y{k} * {d(RU / W[k])}, {d(a[0] - 1)} + T * ({d(a[1])} + T * ({d(a[2])} + T * ({d(a[3])} + T * {d(a[4])}))), cv);\n")
+        A(f"    su = fma({d(a[0] - 1)} + T * ({d(a[1] / 2)} + T * ({d(a[2] / 3)} + T * ({d(a[3] / 4)} + T * {d(a[4] / 5)}))) + "
+          f"{d(a[5])} * invT, w{k}, su);\n")
+    _nasa(A, tab, tm, tail_body)
+    A("  const double irho = 1.0 / rho;\n")
+    for k in range(K):
+        A(f"  f[{k}] = {d(W[k])} * w{k} * irho;\n")
+    A(f"  f[{K}] = -su * {d(RU)} * T / (rho * cv);\n  return 0;\n  }}\n\n")
+
+    # ------------------------------------------------------------------ jac
+    A("  template <long long SS>  // compile-time element stride (0: runtime Srt)\n")
+    A("  __device__ __noinline__ static int jac(const double* __restrict__ yp, double rho, double* __restrict__ J, "
+      "double* __restrict__ sc, long long Srt) {\n")
+    A("  const long long S = SS ? SS : Srt;\n")
+    for k in range(N):
+        A(f"  const double y{k} = yp[{k}*S];\n")
+    thermo_common(A)
+
+    def jac_thermo(k, a):
+        eg_body(k, a)
+        # h/RT into scratch (for dlnKc), cv_k = (cp_k/R - 1) R / W_k, u_k/W_k, dcp_k/dT
+        A(f"    sc[{O_H + k}*S] = {d(a[0])} + T * ({d(a[1] / 2)} + T * ({d(a[2] / 3)} + T * ({d(a[3] / 4)} + T * {d(a[4] / 5)}))) + {d(a[5])} * invT;\n")
+        A(f"    sc[{O_CV + k}*S] = ({d(a[0] - 1)} + T * ({d(a[1])} + T * ({d(a[2])} + T * ({d(a[3])} + T * {d(a[4])})))) * {d(RU / W[k])};\n")
+    _nasa(A, tab, tm, jac_thermo)
+    for k in range(K):
+        A(f"  double w{k} = 0.0;\n")
+    for r, x in enumerate(rx):
+        reaction(A, r, x, True)
+    # cv, su, scw, dcv; uoW_k (registers for pass 2)
+    A("  double cv = 0.0, su = 0.0, scw = 0.0, dcv = 0.0;\n")
+    for k in range(K):
+        A(f"  double uoW{k};\n")
+
+    def jac_tail(k, a):
+        A(f"    {{ const double hk = sc[{O_H + k}*S], cvk = sc[{O_CV + k}*S];\n")
+        A(f"      uoW{k} = (hk - 1.0) * {d(RU)} * T * {d(1.0 / W[k])};\n")
+        A(f"      cv = fma(y{k}, cvk, cv);\n")
+        A(f"      su = fma(uoW{k} * {d(W[k])}, w{k}, su);\n")
+        A(f"      scw = fma(cvk * {d(W[k])}, w{k}, scw);\n")
+        A(f"      dcv = fma(y{k} * {d(RU / W[k])}, {d(a[1])} + T * ({d(2 * a[2])} + T * ({d(3 * a[3])} + T * {d(4 * a[4])})), dcv); }}\n")
+    _nasa(A, tab, tm, jac_tail)
+    A("  const double icv = 1.0 / cv, irho = 1.0 / rho;\n")
+    A("  const double fT0 = -su * irho * icv;\n")
+    # pass 2: species columns
+    for j in range(K):
+        A(f"  {{ // column {j} ({sp[j]})\n")
+        rows = {}
+        terms = []
+        for r, x in enumerate(rx):
+            reac = [idx[s] for s in x["reactants"]]
+            prod = [idx[s] for s in x["products"]]
+            parts = []
+            for o in range(len(reac)):
+                if reac[o] == j:
+                    others = reac[:o] + reac[o + 1:]
+                    parts.append(" * ".join([f"sc[{O_KF + r}*S]"] + [f"C{i}" for i in others]))
+            pparts = []
+            if x["reversible"]:
+                for o in range(len(prod)):
+                    if prod[o] == j:
+                        others = prod[:o] + prod[o + 1:]
+                        pparts.append(" * ".join([f"sc[{O_KR + r}*S]"] + [f"C{i}" for i in others]))
+            tbterm = None
+            if x["type"] != "elementary":
+                e = x["efficiencies"].get(sp[j], 1.0)
+                if e != 0.0:
+                    tbterm = f"sc[{O_DM + tb.index(r)}*S]" + ("" if e == 1.0 else f" * {d(e)}")
+            if not parts and not pparts and tbterm is None:
+                continue
+            if not nu[r]:
+                continue
+            expr = " + ".join(parts) if parts else "0.0"
+            for pp in pparts:
+                expr += f" - {pp}"
+            if tbterm:
+                expr += f" + {tbterm}"
+            terms.append((r, expr))
+            for i in nu[r]:
+                rows[i] = True
+        for i in sorted(rows):
+            A(f"    double c{i} = 0.0;\n")
+        for r, expr in terms:
+            A(f"    {{ const double dq = {expr};\n")
+            for i, v in sorted(nu[r].items()):
+                if v == 1:
+                    A(f"      c{i} += dq;\n")
+                elif v == -1:
+                    A(f"      c{i} -= dq;\n")
+                else:
+                    A(f"      c{i} = fma({d(v)}, dq, c{i});\n")
+            A("    }\n")
+        A("    double s = 0.0;\n")
+        for i in range(K):
+            if i in rows:
+                A(f"    {{ const double v = c{i} * {d(W[i] / W[j])}; J[{i * N + j}*S] = v; s = fma(uoW{i}, v, s); }}\n")
+            else:
+                A(f"    J[{i * N + j}*S] = 0.0;\n")
+        A(f"    J[{K * N + j}*S] = -s * icv - fT0 * sc[{O_CV + j}*S] * icv;\n")
+        A("  }\n")
+    # temperature column
+    A("  {\n")
+    rowsT = {}
+    for r in range(NR):
+        for i in nu[r]:
+            rowsT.setdefault(i, []).append(r)
+    A("    double s = 0.0;\n")
+    for i in range(K):
+        if i in rowsT:
+            A("    { double c = 0.0;\n")
+            for r in rowsT[i]:
+                v = nu[r][i]
+                if v == 1:
+                    A(f"      c += sc[{O_DT + r}*S];\n")
+                elif v == -1:
+                    A(f"      c -= sc[{O_DT + r}*S];\n")
+                else:
+                    A(f"      c = fma({d(v)}, sc[{O_DT + r}*S], c);\n")
+            A(f"      const double v = {d(W[i])} * c * irho; J[{i * N + K}*S] = v; s = fma(uoW{i}, v, s); }}\n")
+        else:
+            A(f"    J[{i * N + K}*S] = 0.0;\n")
+    A(f"    J[{K * N + K}*S] = -scw * irho * icv - s * icv - fT0 * dcv * icv;\n")
+    A("  }\n  return 0;\n  }\n};\n}  // namespace bdfb\n")
     os.makedirs(out_dir, exist_ok=True)
     p = os.path.join(out_dir, f"tpc_{name}.cuh")
-    open(p, "w").write("".join(L))
+    src = "".join(L).replace("@@TABLE@@", d.table())
+    if not os.path.exists(p) or open(p).read() != src:
+        open(p, "w").write(src)
     return p
 
 
+MECHANISMS = ["h2_lidryer", "drm19_class"]
+
+
+def main(argv=None):
+    out = os.path.join(PKG, "csrc", "gen")
+    for m in (argv or MECHANISMS):
+        print(generate(m, out))
+
+
 if __name__ == "__main__":
-    for m in (sys.argv[1:] or ["drm19_class", "h2_lidryer"]):
-        print(generate(m, os.path.join(PKG, "csrc", "gen")))
+    main(sys.argv[1:])

@@ -94,7 +94,7 @@ __constant__ double kRootCL[8] = {0, 0, 0x1.2bec333018867p-2, 0x1.a68056b0a470ep
                                   0x1.091cc94907b7fp-3, 0x1.bee0fc589f6b6p-4, 0x1.8227e72c5f2dbp-4};
 __constant__ double kInvL[8] = {0, 1.0 / 1, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7};
 
-__device__ __noinline__ double root_l(double x, int L) {
+static __device__ __noinline__ double root_l(double x, int L) {
   if (!(x > 0.0) || isinf(x)) return x > 0.0 ? x : 0.0;
   if (L == 1) return x;
   int e;

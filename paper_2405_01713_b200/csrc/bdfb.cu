@@ -21,6 +21,7 @@
 #include "gen/mech_h2_lidryer.cuh"
 #include "mech_model.cuh"
 #include "models_simple.cuh"
+#include "tpc_api.h"
 
 using namespace bdfb;
 
@@ -46,8 +47,15 @@ struct bdfb_batch {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
   int launches = 0;
+  int kernel = BDFB_KERNEL_AUTO;   // per-cell kernel organisation for the mechanism models
+  double* d_ws = nullptr;          // thread-per-cell workspace (bdf_tpc.cuh), sized for the resident grid
+  int* d_iws = nullptr;
+  long long ws_slots = 0;
   std::string err;
 };
+
+static bool is_mech(int model) { return model == BDFB_MODEL_MECH_H2 || model == BDFB_MODEL_MECH_DRM19; }
+static bool use_tpc(const bdfb_batch* b) { return is_mech(b->model) && b->kernel != BDFB_KERNEL_GROUP; }
 
 static std::string g_err;
 
@@ -69,6 +77,44 @@ static int model_n(int model) {
     case BDFB_MODEL_MECH_DRM19: return ModelDRM19::N;
   }
   return -1;
+}
+
+// ---- thread-per-cell mechanism kernel (csrc/tpc.cu): the per-slot workspace is
+// sized once for the resident grid (host setup, never in bdfb_integrate).
+static int prepare_kernel(bdfb_batch* b) {
+  if (b->opt.mode != BDFB_MODE_PER_CELL || !use_tpc(b)) return BDFB_OK;
+  long long slots = 0, dps = 0, ips = 0;
+  cudaError_t e = cudaSetDevice(b->device);
+  if (e == cudaSuccess) e = tpc_geometry(b->model, b->device, b->ncells, &slots, &dps, &ips);
+  if (e != cudaSuccess) return cuda_fail(b, e, "thread-per-cell geometry");
+  if (slots < 1) return fail(b, BDFB_ECUDA, "thread-per-cell kernel does not fit on an SM");
+  if (slots != b->ws_slots) {
+    if (b->d_ws) cudaFree(b->d_ws);
+    if (b->d_iws) cudaFree(b->d_iws);
+    b->d_ws = nullptr;
+    b->d_iws = nullptr;
+    b->ws_slots = 0;
+    if (cudaMalloc(&b->d_ws, sizeof(double) * (size_t)dps * slots) != cudaSuccess ||
+        cudaMalloc(&b->d_iws, sizeof(int) * (size_t)ips * slots) != cudaSuccess)
+      return fail(b, BDFB_ENOMEM, "thread-per-cell workspace");
+    b->ws_slots = slots;
+  }
+  return BDFB_OK;
+}
+
+static int launch_tpc(bdfb_batch* b, const Opts& o, double* y, const double* fext, const double* aux,
+                      cudaStream_t st) {
+  if (b->ws_slots < 1) return fail(b, BDFB_ENOMODEL, "thread-per-cell workspace not prepared");
+  cudaMemsetAsync(b->d_counter, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(b->d_agg, 0, sizeof(Agg), st);
+  cudaEventRecord(b->ev0, st);
+  cudaError_t e = tpc_integrate(b->model, o, y, fext, aux, b->d_atol, b->d_ws, b->d_iws, b->ws_slots, b->d_counter,
+                                b->d_agg, b->cs, st);
+  cudaEventRecord(b->ev1, st);
+  if (e != cudaSuccess) return cuda_fail(b, e, "integrate launch");
+  b->launches = 1;
+  b->timed = true;
+  return BDFB_OK;
 }
 
 extern "C" {
@@ -157,6 +203,8 @@ void bdfb_destroy(bdfb_batch* b) {
   if (b->d_y) cudaFree(b->d_y);
   if (b->d_f) cudaFree(b->d_f);
   if (b->d_aux) cudaFree(b->d_aux);
+  if (b->d_ws) cudaFree(b->d_ws);
+  if (b->d_iws) cudaFree(b->d_iws);
   {
     GlobalBuffers& g = b->gb;
     for (int j = 0; j <= QMAX; ++j) cudaFree(g.v.zn[j]);
@@ -206,7 +254,26 @@ int bdfb_set_model(bdfb_batch* b, int32_t model_id, const void* params, size_t b
     memcpy(b->params, params, bytes);
   }
   b->model = model_id;
-  return BDFB_OK;
+  return prepare_kernel(b);
+}
+
+int bdfb_set_kernel(bdfb_batch* b, int32_t kernel) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (kernel != BDFB_KERNEL_AUTO && kernel != BDFB_KERNEL_THREAD && kernel != BDFB_KERNEL_GROUP)
+    return fail(b, BDFB_EINVAL, "bad kernel id");
+  b->kernel = kernel;
+  return b->model >= 0 ? prepare_kernel(b) : BDFB_OK;
+}
+
+int32_t bdfb_wrms_group(const bdfb_batch* b) {
+  if (!b || b->model < 0) return 0;
+  if (b->opt.mode == BDFB_MODE_GLOBAL_NORM) return b->model == BDFB_MODEL_MECH_H2 ? ModelH2::G : ModelDRM19::G;
+  if (use_tpc(b)) return 1;
+  switch (b->model) {
+    case BDFB_MODEL_MECH_H2: return ModelH2::G;
+    case BDFB_MODEL_MECH_DRM19: return ModelDRM19::G;
+  }
+  return 1;
 }
 
 int bdfb_set_cell_stats(bdfb_batch* b, const bdfb_cell_stats* cs) {
@@ -388,8 +455,12 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
     case BDFB_MODEL_LINEAR: return launch_integrate<ModelLinear>(b, o, y, f_ext, aux, st);
     case BDFB_MODEL_ROBERTSON: return launch_integrate<ModelRobertson>(b, o, y, f_ext, aux, st);
     case BDFB_MODEL_NYX_KWH: return launch_integrate<ModelNyxKwh>(b, o, y, f_ext, aux, st);
-    case BDFB_MODEL_MECH_H2: return launch_integrate<ModelH2>(b, o, y, f_ext, aux, st);
-    case BDFB_MODEL_MECH_DRM19: return launch_integrate<ModelDRM19>(b, o, y, f_ext, aux, st);
+    case BDFB_MODEL_MECH_H2:
+      return use_tpc(b) ? launch_tpc(b, o, y, f_ext, aux, st)
+                        : launch_integrate<ModelH2>(b, o, y, f_ext, aux, st);
+    case BDFB_MODEL_MECH_DRM19:
+      return use_tpc(b) ? launch_tpc(b, o, y, f_ext, aux, st)
+                        : launch_integrate<ModelDRM19>(b, o, y, f_ext, aux, st);
   }
   return fail(b, BDFB_ENOMODEL, "unknown model");
 }
@@ -552,6 +623,12 @@ static int launch_eval(bdfb_batch* b, double t, const double* y, const double* f
   return BDFB_OK;
 }
 
+static int launch_eval_tpc(bdfb_batch* b, const double* y, const double* fext, const double* aux, double* f,
+                           int* status, double* J, cudaStream_t st) {
+  const cudaError_t e = tpc_eval(b->model, b->ncells, y, fext, aux, f, status, J, st);
+  return e == cudaSuccess ? BDFB_OK : cuda_fail(b, e, "eval launch");
+}
+
 extern "C" int bdfb_eval_rhs(bdfb_batch* b, double t, const double* y, const double* f_ext, const double* aux,
                              double* f, int32_t* status, void* stream) {
   if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
@@ -563,8 +640,12 @@ extern "C" int bdfb_eval_rhs(bdfb_batch* b, double t, const double* y, const dou
     case BDFB_MODEL_LINEAR: return launch_eval<ModelLinear>(b, t, y, f_ext, aux, f, status, nullptr, st);
     case BDFB_MODEL_ROBERTSON: return launch_eval<ModelRobertson>(b, t, y, f_ext, aux, f, status, nullptr, st);
     case BDFB_MODEL_NYX_KWH: return launch_eval<ModelNyxKwh>(b, t, y, f_ext, aux, f, status, nullptr, st);
-    case BDFB_MODEL_MECH_H2: return launch_eval<ModelH2>(b, t, y, f_ext, aux, f, status, nullptr, st);
-    case BDFB_MODEL_MECH_DRM19: return launch_eval<ModelDRM19>(b, t, y, f_ext, aux, f, status, nullptr, st);
+    case BDFB_MODEL_MECH_H2:
+      return use_tpc(b) ? launch_eval_tpc(b, y, f_ext, aux, f, status, nullptr, st)
+                        : launch_eval<ModelH2>(b, t, y, f_ext, aux, f, status, nullptr, st);
+    case BDFB_MODEL_MECH_DRM19:
+      return use_tpc(b) ? launch_eval_tpc(b, y, f_ext, aux, f, status, nullptr, st)
+                        : launch_eval<ModelDRM19>(b, t, y, f_ext, aux, f, status, nullptr, st);
   }
   return fail(b, BDFB_ENOMODEL, "unknown model");
 }
@@ -579,8 +660,12 @@ extern "C" int bdfb_eval_jac(bdfb_batch* b, double t, const double* y, const dou
   switch (b->model) {
     case BDFB_MODEL_LINEAR: return launch_eval<ModelLinear>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
     case BDFB_MODEL_ROBERTSON: return launch_eval<ModelRobertson>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
-    case BDFB_MODEL_MECH_H2: return launch_eval<ModelH2>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
-    case BDFB_MODEL_MECH_DRM19: return launch_eval<ModelDRM19>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
+    case BDFB_MODEL_MECH_H2:
+      return use_tpc(b) ? launch_eval_tpc(b, y, nullptr, aux, nullptr, nullptr, J, st)
+                        : launch_eval<ModelH2>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
+    case BDFB_MODEL_MECH_DRM19:
+      return use_tpc(b) ? launch_eval_tpc(b, y, nullptr, aux, nullptr, nullptr, J, st)
+                        : launch_eval<ModelDRM19>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
   }
   return fail(b, BDFB_ENOMODEL, "unknown model");
 }
@@ -656,6 +741,10 @@ __global__ void __launch_bounds__(128) lu_kernel(long long N, double* M, int* pi
 
 template <int NN>
 static int launch_lu(int64_t N, double* M, int32_t* piv, double* b, int32_t* info, cudaStream_t st) {
+  if constexpr (NN >= 5) {
+    const cudaError_t e = tpc_lu(NN, N, M, piv, b, info, st);
+    return e == cudaSuccess ? BDFB_OK : cuda_fail(nullptr, e, "lu launch");
+  }
   constexpr int G = NN <= 4 ? 1 : (NN <= 16 ? 16 : 32);
   constexpr int MAT = (G == 1 ? NN * NN * WS : NN * 34);
   const size_t smem = sizeof(double) * (MAT + 64) * 4;

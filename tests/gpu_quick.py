@@ -17,16 +17,18 @@ def report(name, yg, yo, rtol, atol, sg=None, so=None):
         msg += f" identical-stats frac {same:.3f} nst gpu/orc {sg['nst'].sum()}/{so['nst'].sum()}"
     print(msg, flush=True)
 
-def run(model, mname, n, y0, t1, rtol, atol, rho=None, F=None, group=1, ls=None):
+def run(model, mname, n, y0, t1, rtol, atol, rho=None, F=None, kernel="thread"):
     N = y0.shape[1]
     b = P.Batch(N, n, rtol, atol)
+    b.set_kernel(kernel)
     b.set_model(model)
+    group = b.wrms_group
     cs = b.attach_cell_stats()
     y = torch.tensor(y0, device=dev)
     b.integrate(0.0, t1, y, f_ext=None if F is None else torch.tensor(F, device=dev),
                 aux=None if rho is None else torch.tensor(rho, device=dev))
     st = b.stats()
-    print(model, st, "kernel ms", b.last_kernel_ms(), flush=True)
+    print(model, kernel, "G", group, st, "kernel ms", b.last_kernel_ms(), flush=True)
     sg = {k: v.cpu().numpy() for k, v in cs.items()}
     m = O.Model.mechanism(mname) if mname not in ("robertson", "kwh", "linear") else (
         O.Model.robertson() if mname == "robertson" else (O.Model.nyx_kwh() if mname == "kwh" else O.Model.linear([-1.0])))
@@ -62,9 +64,23 @@ for s in steps:
             run("nyx_kwh", "kwh", 1, e, 3e15, 1e-6, 1e-10, rho=rho, F=fe)
         if s == "h2":
             y, rho, F, prog = flame_field("h2_lidryer", 16)
-            run("h2", "h2_lidryer", 10, y, 1e-5, 1e-6, 1e-10, rho=rho, F=F, group=16)
+            for k in ("thread", "group"):
+                run("h2", "h2_lidryer", 10, y, 1e-5, 1e-6, 1e-10, rho=rho, F=F, kernel=k)
         if s == "drm":
             y, rho, F, prog = flame_field("drm19_class", 16)
-            run("drm19", "drm19_class", 22, y, 1e-5, 1e-6, 1e-10, rho=rho, F=F, group=32)
+            for k in ("thread", "group"):
+                run("drm19", "drm19_class", 22, y, 1e-5, 1e-6, 1e-10, rho=rho, F=F, kernel=k)
+        if s == "time":
+            L = int(os.environ.get("L", "64"))
+            y, rho, F, prog = flame_field("drm19_class", L)
+            for k in ("thread", "group", "thread"):
+                b = P.Batch(y.shape[1], 22, 1e-6, 1e-10)
+                b.set_kernel(k)
+                b.set_model("drm19")
+                yy = torch.tensor(y, device=dev)
+                b.integrate(0.0, 1e-5, yy, f_ext=torch.tensor(F, device=dev), aux=torch.tensor(rho, device=dev))
+                st = b.stats()
+                ms = b.last_kernel_ms()
+                print(f"time drm19 {k} L={L}: {ms:.1f} ms  {y.shape[1] / ms * 1e3:.3e} cells/s  {st}", flush=True)
     except Exception:
         traceback.print_exc()

@@ -21,7 +21,8 @@ from synth.fields import stratified_sample  # noqa: E402
 
 DEV = torch.device("cuda", 0)
 STAT_KEYS = ("nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn")
-MECH = {"h2": ("h2_lidryer", 10, 16), "drm19": ("drm19_class", 22, 32)}
+MECH = {"h2": ("h2_lidryer", 10), "drm19": ("drm19_class", 22)}
+KERNELS = ("thread", "group")   # per-cell kernel organisations of the mechanism models (bdfb_set_kernel)
 
 
 def cu(a):
@@ -35,14 +36,18 @@ def end_state_check(yg, yo, rtol, atol, frac_min=0.0):
     assert ok.all(), f"{(~ok.all(axis=0)).sum()} cells outside 10 tol; worst {np.max(err / tol):.3g}"
 
 
-def run_gpu(model, n, y0, t1, rtol, atol, rho=None, F=None, layout="YC", **kw):
+def run_gpu(model, n, y0, t1, rtol, atol, rho=None, F=None, layout="YC", kernel="thread", **kw):
+    """Integrate on the GPU; st carries the aggregate stats plus "group", the WRMS lane-group
+    size (reading R15) of the kernel used, which the oracle reproduces."""
     N = y0.shape[1]
     b = P.Batch(N, n, rtol, atol, **kw)
+    b.set_kernel(kernel)
     b.set_model(model)
     cs = b.attach_cell_stats()
     y = cu(y0 if layout == "YC" else y0.T)
     b.integrate(0.0, t1, y, f_ext=cu(F if (F is None or layout == "YC") else F.T), aux=cu(rho), layout=layout)
     st = b.stats()
+    st["group"] = b.wrms_group
     yy = y.cpu().numpy()
     return (yy if layout == "YC" else yy.T), {k: v.cpu().numpy() for k, v in cs.items()}, st
 
@@ -93,11 +98,13 @@ def oracle_model(oracle, name):
     return oracle.Model.mechanism(MECH[name][0])
 
 
-@pytest.mark.parametrize("name", ["robertson", "nyx_kwh", "h2", "drm19"])
-def test_rhs_parity(oracle, name):
+@pytest.mark.parametrize("name,kernel", [("robertson", "thread"), ("nyx_kwh", "thread"), ("h2", "thread"),
+                                         ("h2", "group"), ("drm19", "thread"), ("drm19", "group")])
+def test_rhs_parity(oracle, name, kernel):
     y, rho, F = model_states(name, 32768)
     n, N = y.shape
     b = P.Batch(N, n, 1e-6, 1e-10)
+    b.set_kernel(kernel)
     b.set_model(name)
     f, st = P.eval_rhs(b, cu(y), f_ext=cu(F), aux=cu(rho))
     f, st = f.cpu().numpy(), st.cpu().numpy()
@@ -117,11 +124,13 @@ def test_rhs_parity(oracle, name):
     print(f"{name}: worst |df|/S = {worst:.3g}")
 
 
-@pytest.mark.parametrize("name", ["robertson", "h2", "drm19"])
-def test_jacobian_parity(oracle, name):
+@pytest.mark.parametrize("name,kernel", [("robertson", "thread"), ("h2", "thread"), ("h2", "group"),
+                                         ("drm19", "thread"), ("drm19", "group")])
+def test_jacobian_parity(oracle, name, kernel):
     y, rho, F = model_states(name, 4096)
     n, N = y.shape
     b = P.Batch(N, n, 1e-6, 1e-10)
+    b.set_kernel(kernel)
     b.set_model(name)
     J = P.eval_jac(b, cu(y), aux=cu(rho)).cpu().numpy()
     m = oracle_model(oracle, name)
@@ -164,59 +173,62 @@ def test_nyx_c2_parity(oracle):
     print(f"C2: identical per-cell stats {same:.4f}")
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("name,dt", [("h2", 1e-5), ("h2", 1e-6), ("drm19", 1e-5), ("drm19", 1e-6)])
-def test_flame_parity(oracle, name, dt):
-    mech, n, G = MECH[name]
+def test_flame_parity(oracle, name, dt, kernel):
+    mech, n = MECH[name]
     y0, rho, F, prog = flame_field(mech, 16, dt=dt)
-    yg, sg, st = run_gpu(name, n, y0, dt, 1e-6, 1e-10, rho=rho, F=F)
+    yg, sg, st = run_gpu(name, n, y0, dt, 1e-6, 1e-10, rho=rho, F=F, kernel=kernel)
     yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, dt, 1e-6, 1e-10, rho=rho, fext_yc=F,
-                                    group=G, threads=8)
+                                    group=st["group"], threads=8)
     assert st["n_failed"] == 0
     end_state_check(yg, yo, 1e-6, 1e-10)
     same = np.mean([all(sg[k][c] == so[k][c] for k in STAT_KEYS) for c in range(y0.shape[1])])
-    print(f"{name} dt={dt}: identical per-cell stats {same:.4f}")
+    print(f"{name} dt={dt} {kernel}: identical per-cell stats {same:.4f}")
     assert same > 0.95
 
 
 def test_mass_conservation_both_sides(oracle):
     """F_Y = 0 (only F_T forcing): sum_k Y_k is conserved to round-off on both sides."""
     y0, rho, F, prog = flame_field("drm19_class", 8, dt=1e-5)
-    yg, _, _ = run_gpu("drm19", 22, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    yg, _, st = run_gpu("drm19", 22, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
     yo, _ = oracle.integrate_batch(oracle.Model.mechanism("drm19_class"), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho,
-                                   fext_yc=F, group=32, threads=8)
+                                   fext_yc=F, group=st["group"], threads=8)
     s0 = y0[:-1].sum(axis=0)
     assert np.abs(yg[:-1].sum(axis=0) - s0).max() <= 1e-13
     assert np.abs(yo[:-1].sum(axis=0) - s0).max() <= 1e-13
 
 
 # ------------------------------------------------------------------ edge cases
-def test_edge_cases(oracle):
-    y0, rho, F, prog = flame_field("h2_lidryer", 4)        # 64 cells, 2 cells per warp (G=16)
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_edge_cases(oracle, kernel):
+    y0, rho, F, prog = flame_field("h2_lidryer", 4)        # 64 cells
     y0 = y0[:, :61].copy()                                    # ragged tail
     rho, F = rho[:61].copy(), F[:, :61].copy()
     y0[0, 3] = np.nan                                         # non-finite input
     F[5, 9] = np.inf
-    yg, sg, st = run_gpu("h2", 10, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    yg, sg, st = run_gpu("h2", 10, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F, kernel=kernel)
+    G = st["group"]
     assert sg["status"][3] == 5 and sg["status"][9] == 5
     assert np.isnan(yg[0, 3]) and np.array_equal(yg[:, 9], y0[:, 9])
     ok = np.ones(61, bool)
     ok[[3, 9]] = False
     yo, so = oracle.integrate_batch(oracle.Model.mechanism("h2_lidryer"), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho,
-                                    fext_yc=F, group=16)
+                                    fext_yc=F, group=G)
     assert np.array_equal(so["status"], sg["status"])
     end_state_check(yg[:, ok], yo[:, ok], 1e-6, 1e-10)
     assert st["n_failed"] == 2
     # too much work: mxstep = 3
-    yg2, sg2, st2 = run_gpu("h2", 10, y0[:, ok], 1e-5, 1e-6, 1e-10, rho=rho[ok], F=F[:, ok], mxstep=3)
+    yg2, sg2, st2 = run_gpu("h2", 10, y0[:, ok], 1e-5, 1e-6, 1e-10, rho=rho[ok], F=F[:, ok], mxstep=3, kernel=kernel)
     tmw = sg2["status"] == 1
     assert tmw.any() and np.all(sg2["t_reached"][tmw] < 1e-5) and np.all(sg2["nst"][tmw] == 3)
     assert np.all(sg2["status"][~tmw] == 0) and np.all(sg2["nst"][~tmw] <= 3)
     yo2, so2 = oracle.integrate_batch(oracle.Model.mechanism("h2_lidryer"), y0[:, ok], 0.0, 1e-5, 1e-6, 1e-10,
-                                      rho=rho[ok], fext_yc=F[:, ok], group=16, mxstep=3)
+                                      rho=rho[ok], fext_yc=F[:, ok], group=G, mxstep=3)
     assert np.array_equal(so2["status"], sg2["status"])
     end_state_check(yg2, yo2, 1e-6, 1e-10)
     # CY layout == YC layout, bit for bit
-    ycy, _, _ = run_gpu("h2", 10, y0[:, ok], 1e-5, 1e-6, 1e-10, rho=rho[ok], F=F[:, ok], layout="CY")
+    ycy, _, _ = run_gpu("h2", 10, y0[:, ok], 1e-5, 1e-6, 1e-10, rho=rho[ok], F=F[:, ok], layout="CY", kernel=kernel)
     assert np.array_equal(ycy, yg[:, ok])
     # single cell
     y1, s1, _ = run_gpu("robertson", 3, np.array([[1.0], [0.0], [0.0]]), 40.0, 1e-6, 1e-10)
@@ -224,22 +236,24 @@ def test_edge_cases(oracle):
     assert np.array_equal(y1[:, 0], yo1)
 
 
-def test_sharding_invariance_bitwise():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_sharding_invariance_bitwise(kernel):
     """Cells are independent: integrating any subset (what a rank does) gives bit-identical results."""
     y0, rho, F, prog = flame_field("drm19_class", 8, dt=1e-5)
-    yall, _, _ = run_gpu("drm19", 22, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    yall, _, _ = run_gpu("drm19", 22, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F, kernel=kernel)
     for r in range(3):
         sub = np.arange(r, y0.shape[1], 3)
-        ys, _, _ = run_gpu("drm19", 22, y0[:, sub], 1e-5, 1e-6, 1e-10, rho=rho[sub], F=F[:, sub])
+        ys, _, _ = run_gpu("drm19", 22, y0[:, sub], 1e-5, 1e-6, 1e-10, rho=rho[sub], F=F[:, sub], kernel=kernel)
         assert np.array_equal(ys, yall[:, sub])
 
 
 def test_full_size_c3_sampled(oracle):
     """C3 at its BASELINE size (64^3 cells), launch configuration as in bench.py; parity on a
     stratified sample of cells the oracle integrates one by one."""
-    mech, n, G = MECH["h2"]
+    mech, n = MECH["h2"]
     y0, rho, F, prog = flame_field(mech, 64, dt=1e-5)
     yg, sg, st = run_gpu("h2", n, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    G = st["group"]
     assert st["n_failed"] == 0 and st["n_cells"] == 64 ** 3
     idx = stratified_sample(prog, 300)
     yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho, fext_yc=F,
@@ -253,7 +267,7 @@ def test_global_norm_mode_parity(oracle, name, L, dt):
     """The paper's lockstep batch: one h, q for all cells, batch-wide WRMS (R14, R15 order:
     per-cell sums, 256-cell block partials in order).  GPU (host control loop + device kernels)
     vs the oracle's global-norm variant on identical inputs."""
-    mech, n, G = MECH[name]
+    mech, n = MECH[name]
     y0, rho, F, prog = flame_field(mech, L, dt=dt)
     N = y0.shape[1]
     b = P.Batch(N, n, 1e-6, 1e-10, mode=P.MODE_GLOBAL_NORM)
