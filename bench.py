@@ -228,7 +228,7 @@ def oracle_cells_per_s(cfg, budget_s=15.0, threads=None, rank_cells=None, steps=
     return m, times, threads
 
 
-CONFIGS_G = {"C3": 16, "C4": 32}
+CONFIGS_G = {"C3": 1, "C4": 1}     # WRMS summation group of the default (thread-per-cell) kernel, R15
 
 
 # ------------------------------------------------------------------ main
@@ -241,6 +241,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cells", type=int, default=0, help="override cells per rank (debug)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--kernel", default=None, choices=["thread", "group", "split"],
+                    help="per-cell kernel organisation of the mechanism models (default: the library's)")
     args = ap.parse_args()
 
     from paper_2405_01713_b200 import parallel as PL
@@ -282,6 +284,8 @@ def main():
     N = y0.shape[1]
     glob_mode = cfg in GLOBAL_CFGS
     b = P.Batch(N, n, rtol, atol, device=local, mode=P.MODE_GLOBAL_NORM if glob_mode else P.MODE_PER_CELL)
+    if args.kernel and mech:
+        b.set_kernel(args.kernel)
     b.set_model(model)
     if glob_mode and world > 1:
         # one lockstep system across ranks: the library's own NCCL communicator carries the norms
@@ -337,7 +341,8 @@ def main():
         pass
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic_per_launch(cfg, N),
-            "kernel": ("integrate_group_kernel<ModelMech<%s>>" % mech) if mech else "integrate_kernel<%s>" % model,
+            "kernel": (("integrate_tpc_kernel<Tpc_%s>" if b.wrms_group == 1 else "integrate_group_kernel<ModelMech<%s>>")
+                       % mech) if mech else "integrate_kernel<%s>" % model,
             "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
             "fp64_probe_tflops": probe, "kernel_ms": statistics.mean(kern_ms),
             "flops_per_launch": statistics.mean(flops)}

@@ -77,11 +77,15 @@ extern "C" {
 #define BDFB_MODE_GLOBAL_NORM 1
 
 /* per-cell kernel organisation for the mechanism models (bdfb_set_kernel) */
-#define BDFB_KERNEL_AUTO 0     /* = THREAD                                              */
+#define BDFB_KERNEL_AUTO 0     /* = SPLIT                                               */
 #define BDFB_KERNEL_THREAD 1   /* one cell per thread, straight-line generated RHS/J,
                                   per-thread-slot device workspace (csrc/bdf_tpc.cuh)    */
 #define BDFB_KERNEL_GROUP 2    /* one cell per group of 16/32 lanes, state in shared
                                   memory (csrc/bdf_group.cuh; round-1 design)           */
+#define BDFB_KERNEL_SPLIT 3    /* slot pool in HBM, two kernels per trip: group-per-cell
+                                  control (Newton, LU, error test, step/order) and
+                                  thread-per-cell generated RHS (csrc/bdf_split.cuh);
+                                  bdfb_integrate is synchronous (host launch loop)      */
 
 typedef struct bdfb_batch bdfb_batch;
 

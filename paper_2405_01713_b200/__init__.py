@@ -106,8 +106,9 @@ class Batch:
         self.model = model
 
     def set_kernel(self, kernel):
-        """Per-cell kernel for the mechanism models: "thread" (default) or "group" (bdfb_set_kernel)."""
-        kid = {"auto": L.KERNEL_AUTO, "thread": L.KERNEL_THREAD, "group": L.KERNEL_GROUP}[kernel]
+        """Per-cell kernel for the mechanism models: "split" (= "auto", default), "thread" or "group" (bdfb_set_kernel)."""
+        kid = {"auto": L.KERNEL_AUTO, "thread": L.KERNEL_THREAD, "group": L.KERNEL_GROUP,
+               "split": L.KERNEL_SPLIT}[kernel]
         _check(self._L.bdfb_set_kernel(self.h, kid), self.h)
 
     @property

@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("BDFB_LIB") or os.path.join(PKG, "libbdfb.so")   # BDF
 MODEL_LINEAR, MODEL_ROBERTSON, MODEL_NYX_KWH, MODEL_MECH_H2, MODEL_MECH_DRM19 = 0, 1, 2, 3, 4
 LAYOUT_YC, LAYOUT_CY = 0, 1
 MODE_PER_CELL, MODE_GLOBAL_NORM = 0, 1
-KERNEL_AUTO, KERNEL_THREAD, KERNEL_GROUP = 0, 1, 2
+KERNEL_AUTO, KERNEL_THREAD, KERNEL_GROUP, KERNEL_SPLIT = 0, 1, 2, 3
 
 # every symbol include/bdfb.h declares
 SYMBOLS = ["bdfb_default_options", "bdfb_create", "bdfb_set_model", "bdfb_set_cell_stats", "bdfb_integrate",

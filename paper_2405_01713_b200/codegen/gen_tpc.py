@@ -272,6 +272,7 @@ def generate(name, out_dir):
     A(f"  f[{K}] = -su * {d(RU)} * T / (rho * cv);\n  return 0;\n  }}\n\n")
 
     # ------------------------------------------------------------------ jac
+    jac_start = len(L)
     A("  template <long long SS>  // compile-time element stride (0: runtime Srt)\n")
     A("  __device__ __noinline__ static int jac(const double* __restrict__ yp, double rho, double* __restrict__ J, "
       "double* __restrict__ sc, long long Srt) {\n")
@@ -383,7 +384,24 @@ def generate(name, out_dir):
         else:
             A(f"    J[{i * N + K}*S] = 0.0;\n")
     A(f"    J[{K * N + K}*S] = -scw * irho * icv - s * icv - fT0 * dcv * icv;\n")
-    A("  }\n  return 0;\n  }\n};\n}  // namespace bdfb\n")
+    A("  }\n  return 0;\n  }\n")
+    # jac_cm: the same body with y at yp[k * SY] (e.g. a warp-blocked SoA state), J column-major and
+    # contiguous (J(i, j) at J[j * N + i], the split kernel's per-cell record) and contiguous scratch
+    import re
+    body = "".join(L[jac_start:])
+    body = body.replace("  template <long long SS>  // compile-time element stride (0: runtime Srt)\n",
+                        "  template <long long SY>  // element stride of y; J column-major, contiguous\n")
+    body = body.replace("static int jac(const double* __restrict__ yp, double rho, double* __restrict__ J, "
+                        "double* __restrict__ sc, long long Srt) {\n",
+                        "static int jac_cm(const double* __restrict__ yp, double rho, double* __restrict__ J, "
+                        "double* __restrict__ sc) {\n")
+    body = body.replace("  const long long S = SS ? SS : Srt;\n", "")
+    body = re.sub(r"yp\[(\d+)\*S\]", lambda m: f"yp[{m.group(1)}*SY]", body)
+    body = re.sub(r"J\[(\d+)\*S\]", lambda m: f"J[{(int(m.group(1)) % N) * N + int(m.group(1)) // N}]", body)
+    body = re.sub(r"sc\[(\d+)\*S\]", lambda m: f"sc[{m.group(1)}]", body)
+    assert "*S]" not in body, "unconverted stride in jac_cm"
+    A(body)
+    A("};\n}  // namespace bdfb\n")
     os.makedirs(out_dir, exist_ok=True)
     p = os.path.join(out_dir, f"tpc_{name}.cuh")
     src = "".join(L).replace("@@TABLE@@", d.table())

@@ -123,7 +123,7 @@ enum : int { X_LOAD = 0, X_STEP_TOP, X_ATTEMPT, X_REQ_RES, X_SOLVE, X_NFAIL, X_E
              X_HIN_FINISH, X_SETUP, X_COMPLETE, X_PREPARE, X_PREP_FINISH, X_ORDER_DOWN, X_RESCALE, X_RETURN };
 
 // ---- leader-lane scalar logic (out of line, pointer arguments only) ----------
-__device__ __noinline__ void gl_set_bdf(GS* s) {
+static __device__ __noinline__ void gl_set_bdf(GS* s) {
   const int q = s->q;
   const double h = s->h;
   double xi_inv = 1.0, xistar_inv = 1.0, alpha0 = -1.0, alpha0_hat = -1.0, hsum = h;
@@ -169,7 +169,7 @@ __device__ __noinline__ void gl_set_bdf(GS* s) {
 }
 
 // cvIncreaseBDF coefficients: lc[2..q], A1 (vector part applied by all lanes)
-__device__ __noinline__ void gl_increase_coef(GS* s) {
+static __device__ __noinline__ void gl_increase_coef(GS* s) {
   double* l = s->lc;
   for (int i = 0; i <= QMAX; ++i) l[i] = 0.0;
   double alpha1 = 1.0, prod = 1.0, xiold = 1.0, alpha0 = -1.0, hsum = s->hscale;
@@ -189,7 +189,7 @@ __device__ __noinline__ void gl_increase_coef(GS* s) {
 }
 
 // cvDecreaseBDF coefficients lc[2..q-1]
-__device__ __noinline__ void gl_decrease_coef(GS* s) {
+static __device__ __noinline__ void gl_decrease_coef(GS* s) {
   double* l = s->lc;
   for (int i = 0; i <= QMAX; ++i) l[i] = 0.0;
   l[2] = 1.0;
@@ -201,7 +201,7 @@ __device__ __noinline__ void gl_decrease_coef(GS* s) {
   }
 }
 
-__device__ __forceinline__ void gl_set_eta(GS* s, const Opts* o) {
+static __device__ __forceinline__ void gl_set_eta(GS* s, const Opts* o) {
   if (s->eta < THRESH) {
     s->eta = 1.0;
     s->hprime = s->h;
@@ -213,7 +213,7 @@ __device__ __forceinline__ void gl_set_eta(GS* s, const Opts* o) {
 }
 
 // Error test and, on success, cvCompleteStep's scalar part.  Sets s->act.
-__device__ __noinline__ void gl_errtest(GS* s, const Opts* o) {
+static __device__ __noinline__ void gl_errtest(GS* s, const Opts* o) {
   const double dsm = s->acnrm * s->tq[2];
   s->dsm = dsm;
   if (dsm <= 1.0) {
@@ -234,7 +234,7 @@ __device__ __noinline__ void gl_errtest(GS* s, const Opts* o) {
 }
 
 // after RESTORE on an error-test failure: choose eta / order (sets s->act)
-__device__ __noinline__ void gl_errfail(GS* s, const Opts* o) {
+static __device__ __noinline__ void gl_errfail(GS* s, const Opts* o) {
   s->tn = s->saved_t;
   if (fabs(s->h) <= o->hmin * (1.0 + UROUND) || s->nef == MXNEF) {
     s->status = ST_ERR_FAILURE;
@@ -265,7 +265,7 @@ __device__ __noinline__ void gl_errfail(GS* s, const Opts* o) {
 }
 
 // PREPARE_NEXT, first part: does the order selection need the two norms?
-__device__ __noinline__ void gl_prepare_a(GS* s, const Opts* o) {
+static __device__ __noinline__ void gl_prepare_a(GS* s, const Opts* o) {
   if (s->etamax == 1.0) {
     s->qwait = s->qwait > 2 ? s->qwait : 2;
     s->qprime = s->q;
@@ -298,7 +298,7 @@ __device__ __noinline__ void gl_prepare_a(GS* s, const Opts* o) {
 }
 
 // PREPARE_NEXT, second part (cvChooseEta + cvSetEta); s->flag = 1 -> zn[qmax] = acor
-__device__ __noinline__ void gl_prepare_b(GS* s, const Opts* o, double ddn, double dup) {
+static __device__ __noinline__ void gl_prepare_b(GS* s, const Opts* o, double ddn, double dup) {
   const double etaq = s->A1;
   double etaqm1 = 0.0, etaqp1 = 0.0;
   if (s->q > 1) etaqm1 = 1.0 / (root_l(BIAS1 * (ddn * s->tq[1]), s->q) + ADDON);
@@ -323,7 +323,7 @@ __device__ __noinline__ void gl_prepare_b(GS* s, const Opts* o, double ddn, doub
 }
 
 // outer-loop top (O2, O3 and the STEP prologue); sets s->act / s->flag
-__device__ __noinline__ void gl_step_top(GS* s, const Opts* o) {
+static __device__ __noinline__ void gl_step_top(GS* s, const Opts* o) {
   if ((s->tn + s->hprime - o->tf) * s->h > 0.0) {
     s->hprime = o->tf - s->tn;
     s->eta = s->hprime / s->h;
@@ -347,7 +347,7 @@ __device__ __noinline__ void gl_step_top(GS* s, const Opts* o) {
 }
 
 // after PREDICT: SET_BDF, gamma, Newton prologue
-__device__ __noinline__ void gl_attempt(GS* s, const Opts* o) {
+static __device__ __noinline__ void gl_attempt(GS* s, const Opts* o) {
   s->tn = s->tn + s->h;
   if ((s->tn - o->tf) * s->h > 0.0) s->tn = o->tf;
   gl_set_bdf(s);
@@ -363,7 +363,7 @@ __device__ __noinline__ void gl_attempt(GS* s, const Opts* o) {
 }
 
 // Newton convergence test (Eq. 4) after a solve; sets s->act
-__device__ __forceinline__ void gl_newton_test(GS* s, double del) {
+static __device__ __forceinline__ void gl_newton_test(GS* s, double del) {
   s->nni++;
   if (s->m > 0) s->crate = fmax(CRDOWN * s->crate, del / s->dprev);
   const double dcon = del * fmin(1.0, s->crate) / s->tol;

@@ -1,0 +1,422 @@
+// bdf_split.cuh -- the SPLIT organisation of the per-cell BDF integrator for
+// the reacting-flow mechanism models (B200 / sm_100a).
+//
+// Semantics: the listing SURVEY.md §8(c).2 (CVODE's fixed-leading-coefficient
+// Nordsieck BDF), executed by the same
+// thread-per-cell state machine as bdf_tpc.cuh (TpcIntegrator: one cell per
+// lane, identical stages, constants and operation order; WRMS order R15 with
+// G = 1; LU bit-identical to LU_FACTOR, reading R16).
+//
+// Why split (ncu, profiles/r1): one persistent kernel that holds a cell's
+// whole life -- RHS, Jacobian, LU and control -- keeps only 8 warps per SM
+// resident (its straight-line RHS needs 255 registers), serialises the
+// block's LU work onto one warp behind __syncthreads (barrier stalls), and
+// re-reads every L entry of its factorisations from L2/HBM (long-scoreboard
+// stalls): FP64 pipe < 5%, IPC 0.27.  Here a pool of S cell SLOTS lives in
+// HBM between launches and every trip of the listing runs as five kernels,
+// each with its own register budget, occupancy and memory pattern:
+//
+//   K_ctl (pass A, thread per slot, all slots): consume the RHS value;
+//     cvHin; decide the matrix setup.  A cell that needs no setup continues
+//     (Newton solve with its LU, error test, step/order selection, order
+//     change, predictor) to its next RHS request; one that needs a setup
+//     stops and joins the setup list (and the Jacobian list if J is stale).
+//     A finished cell is stored and the slot loads the next cell from the
+//     device work counter, so the pool stays full until the counter runs out
+//     (per-cell adaptive stepping: a stiff cell holds its slot for more trips).
+//   K_jac (thread per listed slot): analytic Jacobian, generated straight-line
+//     code (gen/tpc_<mech>.cuh jac_cm), into the slot's J record.
+//   K_lu (one cell per group of G lanes): M = I - gamma J, LU with partial
+//     pivoting in registers (coop_factor: lane i holds row i), factors stored
+//     column-major in pivoted row order with 1/U_kk and the permutation.
+//   K_ctl (pass B, thread per listed slot): the rest of the trip after the
+//     setup, to the next RHS request.
+//   K_rhs (thread per slot with a request): f = R(yq) + F, generated
+//     straight-line RHS -- the transcendental-heavy FP64 work on full warps.
+//
+// HBM records per slot s (all allocated once, sized for the pool):
+//   VEC  warp-blocked SoA: element e of slot s at vec[((s/32) D + e) 32 + s%32]
+//        (zn[0..5], ewt, acor, yq, del, fext, 1/U_kk (unused), fr): a warp of
+//        consecutive slots reads one element as one 256-byte line;
+//   TS   the scalar state (struct TS), one record per slot, block-contiguous
+//        (K_ctl copies its block's records through shared memory);
+//   J    column-major n x n (LUREC stride);
+//   LU   column-major n x n factors in pivoted row order | 1/U_kk[n] | perm[n]
+//        (ints): the Newton solve of a thread streams its own record with
+//        16-byte loads, column by column in the order of the substitutions.
+#pragma once
+#include "bdf_tpc.cuh"
+
+namespace bdfb {
+
+#ifndef BDFB_SPLIT_BLOCK
+#define BDFB_SPLIT_BLOCK 128
+#endif
+#ifndef BDFB_SPLIT_CTL_MINB
+#define BDFB_SPLIT_CTL_MINB 3
+#endif
+
+struct SplitBufs {
+  double* vec;                 // S/32 * D * 32
+  double* ts;                  // S * TS_STRIDE
+  double* J;                   // S * JREC
+  double* LU;                  // S * LUREC
+  int* rv;                     // S: RHS status of the last request
+  int* slist;                  // setup list (slots)
+  int* jlist;                  // Jacobian list (slots)
+  unsigned* cnt;               // [0] setup count, [1] Jacobian count
+  unsigned long long* live;    // [2]: live slots after the K_ctl of iteration it (it & 1)
+  long long slots;             // S (multiple of 32)
+};
+
+template <class Mech, class GM>
+struct Split {
+  static constexpr int N = Mech::N;
+  using I = TpcIntegrator<Mech, GM, 32, false>;
+  using W = typename I::W;
+  static constexpr int D = W::DOUBLES;
+  static constexpr int JREC = (N * N + 3) / 4 * 4;
+  static constexpr int LU_INVD = N * N, LU_PERM = N * N + N;     // perm: ints at double offset LU_PERM
+  static constexpr int LUREC = (N * N + N + (N + 1) / 2 + 3) / 4 * 4;
+  static_assert(N % 2 == 0, "16-byte column loads need an even n");
+  static_assert(sizeof(TS) <= sizeof(double) * TS_STRIDE, "TS record");
+
+  __device__ static W ws(const SplitBufs& b, long long slot) {
+    return W{b.vec + ((slot >> 5) * D) * 32 + (slot & 31), nullptr};
+  }
+  __device__ static TS* ts(const SplitBufs& b, long long slot) {
+    return reinterpret_cast<TS*>(b.ts + slot * TS_STRIDE);
+  }
+
+  // SOLVE with the slot's LU record (listing LU_SOLVE, reading R16): the
+  // same operations in the same order as tpc_solve, then the stale-gamma
+  // scaling, ycor update and the Newton test of TpcIntegrator::solve.
+  __device__ static int solve(TS& s, const W& w, const double* __restrict__ lu) {
+    s.nni++;
+    double b[N];
+    const int* perm = reinterpret_cast<const int*>(lu + LU_PERM);
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[i] = -w.del(perm[i]);
+    const double2* col = reinterpret_cast<const double2*>(lu);
+#pragma unroll
+    for (int k = 0; k < N - 1; ++k) {           // unit-L forward substitution, column k
+      double c[N];
+#pragma unroll
+      for (int h = (k + 1) / 2; h < N / 2; ++h) {
+        const double2 v = col[(k * N) / 2 + h];
+        c[2 * h] = v.x;
+        c[2 * h + 1] = v.y;
+      }
+#pragma unroll
+      for (int i = k + 1; i < N; ++i) b[i] = fma(-c[i], b[k], b[i]);
+    }
+    const double2* inv2 = reinterpret_cast<const double2*>(lu + LU_INVD);
+    double inv[N];
+#pragma unroll
+    for (int h = 0; h < N / 2; ++h) {
+      const double2 v = inv2[h];
+      inv[2 * h] = v.x;
+      inv[2 * h + 1] = v.y;
+    }
+#pragma unroll
+    for (int k = N - 1; k > 0; --k) {           // back substitution, column k, reciprocal diagonal
+      b[k] = b[k] * inv[k];
+      double c[N];
+#pragma unroll
+      for (int h = 0; h < (k + 1) / 2; ++h) {
+        const double2 v = col[(k * N) / 2 + h];
+        c[2 * h] = v.x;
+        c[2 * h + 1] = v.y;
+      }
+#pragma unroll
+      for (int i = 0; i < k; ++i) b[i] = fma(-c[i], b[k], b[i]);
+    }
+    b[0] = b[0] * inv[0];
+    if (s.gamrat != 1.0) {
+      const double sc = 2.0 / (1.0 + s.gamrat);
+#pragma unroll
+      for (int i = 0; i < N; ++i) b[i] = sc * b[i];
+    }
+    double acc = 0.0, acc2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double a = w.acor(i) + b[i];
+      w.acor(i) = a;
+      const double e = w.ewt(i);
+      const double p = b[i] * e;
+      acc = acc + p * p;
+      const double p2 = a * e;
+      acc2 = acc2 + p2 * p2;
+      b[i] = a;
+    }
+    const double del = sqrt(acc / (double)N);
+    if (s.m > 0) s.crate = fmax(CRDOWN * s.crate, del / s.dprev);
+    const double dcon = del * fmin(1.0, s.crate) / s.tol;
+    if (dcon <= 1.0) {
+      s.acnrm = (s.m == 0) ? del : sqrt(acc2 / (double)N);
+      return I::A_ERRTEST;
+    }
+    if (s.m >= 1 && del > RDIV * s.dprev) return I::A_NFAIL;
+    s.dprev = del;
+    s.m++;
+    if (s.m >= MAXCOR) return I::A_NFAIL;
+#pragma unroll
+    for (int i = 0; i < N; ++i) w.yq(i) = w.zn(0, i) + b[i];
+    s.tq_req = s.tn;
+    s.phase = PH_NRES;
+    return I::A_RET;
+  }
+
+  // the trip after the setup decision (both passes): SOLVE .. ATTEMPT, in the
+  // stage order of TpcIntegrator::trip.  Returns A_RET (RHS requested) or A_DONE.
+  __device__ static int finish(const Opts& o, TS& s, const W& w, int act, const double* lu, double* y,
+                               const double* fext, const double* aux, const double* atol,
+                               unsigned long long* counter, Agg& acc, const CellStatsPtrs& cs) {
+    if (act == I::A_SOLVE) act = solve(s, w, lu);
+    if (act == I::A_NFAIL) act = I::nfail(o, s, w);
+    if (act == I::A_ERRTEST) act = I::errtest(o, s, w);
+    if (act == I::A_STEP_TOP) act = I::step_top(o, s, w);
+    if (act == I::A_STORE) {
+      I::store(o, s, w, y, acc, cs);
+      act = I::A_LOAD;
+    }
+    if (act == I::A_LOAD) act = I::load(o, s, w, y, fext, aux, atol, counter, acc, cs);
+    if (act == I::A_ATTEMPT) act = I::attempt(o, s, w, atol);
+    return act;
+  }
+};
+
+// initialise the pool: every slot empty (phase DONE)
+template <class Mech, class GM>
+__global__ void split_init_kernel(SplitBufs b) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s == 0) {
+    b.live[0] = b.live[1] = 0;
+    b.cnt[0] = b.cnt[1] = 0;
+  }
+  if (s >= b.slots) return;
+  TS* t = Split<Mech, GM>::ts(b, s);
+  t->phase = PH_DONE;
+  t->flag = 0;
+  t->pend = 0;
+  b.rv[s] = 0;
+}
+
+// ------------------------------------------------------------------ K_ctl
+// one trip of every slot (slot = block * BLOCK + thread); the block's TS
+// records are copied through shared memory (coalesced).  A cell whose last
+// trip stopped at a matrix setup (phase PH_SETUP) resumes after it: the setup
+// kernels ran in between, so the trip costs the cell one extra iteration
+// (its RHS slot idles once) instead of a latency-bound second pass.
+constexpr int PH_SETUP = 6;
+template <class Mech, class GM>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_CTL_MINB)
+    split_ctl_kernel(Opts o, SplitBufs b, int it, double* y, const double* fext, const double* aux,
+                     const double* atol, unsigned long long* counter, Agg* agg, CellStatsPtrs cs) {
+  using SP = Split<Mech, GM>;
+  using I = typename SP::I;
+  constexpr int N = Mech::N;
+  extern __shared__ double smem[];           // TS records of the block's threads (TS_STRIDE each)
+  __shared__ double satol[N];
+  __shared__ Agg wacc[BDFB_SPLIT_BLOCK / 32];
+  __shared__ unsigned long long blive;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < N) satol[threadIdx.x] = atol[threadIdx.x];
+  if (lane == 0) wacc[warp] = Agg{};
+  if (threadIdx.x == 0) blive = 0;
+  const long long s0 = (long long)blockIdx.x * BDFB_SPLIT_BLOCK;
+  const long long nrec = (b.slots - s0 < BDFB_SPLIT_BLOCK ? b.slots - s0 : BDFB_SPLIT_BLOCK) * TS_STRIDE;
+  {
+    const double* src = b.ts + s0 * TS_STRIDE;
+    for (long long i = threadIdx.x; i < nrec; i += BDFB_SPLIT_BLOCK) smem[i] = src[i];
+  }
+  const long long slot = s0 + threadIdx.x;
+  const bool have = slot < b.slots;
+  __syncthreads();
+  TS& s = *reinterpret_cast<TS*>(smem + threadIdx.x * TS_STRIDE);
+  const typename SP::W w = SP::ws(b, have ? slot : 0);
+  const double* lu = b.LU + (have ? slot : 0) * SP::LUREC;
+  int act = I::A_DONE;
+  bool setup = false, jreq = false;
+  if (have) {
+    bool run = true;
+    if (s.phase == PH_DONE) {   // empty slot: live only while the work counter has cells left
+      const unsigned long long next = *reinterpret_cast<volatile unsigned long long*>(counter);
+      run = next < (unsigned long long)o.ncells;
+    }
+    if (run && s.phase == PH_SETUP) {   // resume after the setup kernels (TpcIntegrator::trip order)
+      act = s.pend;
+      if (act == I::A_SETUP_J) {
+        if (s.coop) {
+          I::setup_done(s);
+          act = I::A_NFAIL;
+        } else {
+          act = I::A_SETUP_LU;
+        }
+      }
+      if (act == I::A_SETUP_LU) {
+        I::setup_done(s);
+        act = s.coop ? I::A_NFAIL : I::A_SOLVE;
+      }
+      s.pend = 0;
+    } else if (run) {
+      double fr[N];
+      int rv = 0;
+      if (s.phase == PH_INIT || s.phase == PH_HIN || s.phase == PH_NRES || s.phase == PH_ETF3) {
+        rv = b.rv[slot];
+        s.nfe++;
+#pragma unroll
+        for (int i = 0; i < N; ++i) fr[i] = w.fr(i);
+      }
+      act = I::consume(o, s, w, rv, fr);
+      if (act == I::A_HIN_FINISH) act = I::hin_finish(o, s);
+      if (act == I::A_START) act = I::start(o, s, w);
+      if (act == I::A_SETUP) act = I::setup_decide(s);
+      if (act == I::A_SETUP_J || act == I::A_SETUP_LU) {
+        s.pend = act;
+        s.coop = 0;
+        s.phase = PH_SETUP;
+        setup = true;
+        jreq = act == I::A_SETUP_J;
+        act = I::A_RET;      // live; finish() passes A_RET through
+      }
+    }
+    // one call site: lanes that resumed and lanes that consumed an RHS value run the rest together
+    if (run) act = SP::finish(o, s, w, act, lu, y, fext, aux, satol, counter, wacc[warp], cs);
+  }
+  // setup / Jacobian lists: one atomic per warp and list
+  {
+    const unsigned bs = __ballot_sync(0xffffffffu, setup), bj = __ballot_sync(0xffffffffu, jreq);
+    unsigned os = 0, oj = 0;
+    if (lane == 0) {
+      if (bs) os = atomicAdd(&b.cnt[0], __popc(bs));
+      if (bj) oj = atomicAdd(&b.cnt[1], __popc(bj));
+    }
+    os = __shfl_sync(0xffffffffu, os, 0);
+    oj = __shfl_sync(0xffffffffu, oj, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (setup) b.slist[os + __popc(bs & below)] = (int)slot;
+    if (jreq) b.jlist[oj + __popc(bj & below)] = (int)slot;
+    const unsigned bl = __ballot_sync(0xffffffffu, act == I::A_RET);
+    if (lane == 0 && bl) atomicAdd(&blive, (unsigned long long)__popc(bl));
+  }
+  __syncthreads();
+  {
+    double* dst = b.ts + s0 * TS_STRIDE;
+    for (long long i = threadIdx.x; i < nrec; i += BDFB_SPLIT_BLOCK) dst[i] = smem[i];
+  }
+  if (threadIdx.x == 0 && blive) atomicAdd(&b.live[it & 1], blive);
+  if (lane == 0 && wacc[warp].cells_done) {
+    const Agg& a = wacc[warp];
+    atomicAdd(&agg->n_failed, a.n_failed);
+    atomicAdd(&agg->nst, a.nst);
+    atomicAdd(&agg->nfe, a.nfe);
+    atomicAdd(&agg->nje, a.nje);
+    atomicAdd(&agg->nsetups, a.nsetups);
+    atomicAdd(&agg->nni, a.nni);
+    atomicAdd(&agg->netf, a.netf);
+    atomicAdd(&agg->ncfn, a.ncfn);
+    atomicMax(&agg->nst_max, a.nst_max);
+    atomicMax(&agg->nfe_max, a.nfe_max);
+    atomicAdd(&agg->cells_done, a.cells_done);
+  }
+}
+
+// ------------------------------------------------------------------ K_jac
+// one cell per group of G lanes (lane i = component i): the analytic Jacobian
+// of the group model (mech_model.cuh: lanes over species and reactions), row
+// i into the cell's column-major J record; status -> TS.coop (nonzero:
+// recoverable failure).  Shared scratch per group: RHS scratch SG + the
+// Jacobian's per-reaction partials JG.
+template <class Mech, class GM>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_kernel(SplitBufs b) {
+  using SP = Split<Mech, GM>;
+  constexpr int N = Mech::N, G = GM::G;
+  constexpr int MS = N | 1;                      // odd row stride of the shared J (conflict-free)
+  extern __shared__ double smem[];
+  Grp<G> g;
+  const int gi = threadIdx.x / G;
+  double* sc = smem + gi * (GM::SG + GM::JG + N * MS);
+  double* jm = sc + GM::SG + GM::JG;
+  const long long cnt = b.cnt[1], groups = (long long)gridDim.x * (BDFB_SPLIT_BLOCK / G);
+  for (long long e = ((long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x) / G; e < cnt; e += groups) {
+    const long long slot = b.jlist[e];
+    const typename SP::W w = SP::ws(b, slot);
+    TS* t = SP::ts(b, slot);
+    const double yv = g.lane < N ? w.yq(g.lane) : 0.0;
+    double* J = b.J + slot * SP::JREC;
+    const int r = GM::template jac<MS>(g, yv, t->aux, jm + (g.lane < N ? g.lane : 0), sc, sc + GM::SG);
+    g.sync();
+    if (!r && g.lane < N) {
+#pragma unroll 2
+      for (int j = 0; j < N; ++j) J[j * N + g.lane] = jm[j * MS + g.lane];
+    }
+    if (g.lane == 0) t->coop = r;
+    g.sync();
+  }
+}
+
+// ------------------------------------------------------------------ K_lu
+// one cell per group of G lanes (lane i = row i): M = I - gamma J and the
+// listing's LU_FACTOR in registers (coop_factor, bit-identical pivots and
+// factors), stored column-major in pivoted row order + 1/U_kk + perm.
+template <class Mech, class GM>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b) {
+  using SP = Split<Mech, GM>;
+  constexpr int N = Mech::N, G = GM::G;
+  Grp<G> g;
+  const long long cnt = b.cnt[0], groups = (long long)gridDim.x * (BDFB_SPLIT_BLOCK / G);
+  for (long long e = ((long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x) / G; e < cnt; e += groups) {
+    const long long slot = b.slist[e];
+    TS* t = SP::ts(b, slot);
+    if (t->coop) continue;                       // the Jacobian failed: the resumed trip handles it (uniform)
+    const double gm = t->gamma;
+    const double* J = b.J + slot * SP::JREC;
+    double* lu = b.LU + slot * SP::LUREC;
+    const int i = g.lane;
+    double row[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) row[j] = (i < N) ? (i == j ? 1.0 : 0.0) - gm * J[j * N + i] : 0.0;
+    int pos;
+    double dinv;
+    const int r = coop_factor<N, G>(g, row, pos, dinv);
+    if (!r && i < N) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) lu[j * N + pos] = row[j];
+      lu[SP::LU_INVD + pos] = dinv;
+      reinterpret_cast<int*>(lu + SP::LU_PERM)[pos] = i;
+    }
+    g.sync();
+    if (i == 0) t->coop = r;
+  }
+}
+
+// ------------------------------------------------------------------ K_rhs
+// thread per slot: fr = R(yq) + F for a pending RHS request.  Also resets the
+// list counters and the live count for the next iteration (it + 1) -- after
+// the setup kernels of this iteration consumed the lists.
+template <class Mech, class GM>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_rhs_kernel(SplitBufs b, int it) {
+  using SP = Split<Mech, GM>;
+  constexpr int N = Mech::N;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    b.cnt[0] = b.cnt[1] = 0;
+    b.live[(it + 1) & 1] = 0;
+  }
+  const long long stride = (long long)gridDim.x * BDFB_SPLIT_BLOCK;
+  for (long long slot = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; slot < b.slots; slot += stride) {
+    const TS* t = SP::ts(b, slot);
+    const int ph = t->phase;
+    if (!(ph == PH_INIT || ph == PH_HIN || ph == PH_NRES || ph == PH_ETF3)) continue;
+    const typename SP::W w = SP::ws(b, slot);
+    double yv[N], fv[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) yv[k] = w.yq(k);
+    const int rv = Mech::rhs(yv, t->aux, fv);
+#pragma unroll
+    for (int k = 0; k < N; ++k) w.fr(k) = fv[k] + w.fext(k);
+    b.rv[slot] = rv;
+  }
+}
+
+}  // namespace bdfb

@@ -48,6 +48,7 @@ struct TS {
   int nst, nfe, nje, nsetups, nni, netf, ncfn;
   int nstlp, nstlj, nef, ncf, nflag, convfail, setup, jcur, m;
   int count1, count2, phase, status, flag, coop;   // coop: result of a warp-cooperative stage
+  int pend;                                        // split kernel: setup stage requested (A_SETUP_J/LU)
 };
 constexpr int TS_STRIDE = (int)((sizeof(TS) + 7) / 8) | 1;   // odd number of doubles
 
@@ -68,12 +69,12 @@ constexpr int TS_STRIDE = (int)((sizeof(TS) + 7) / 8) | 1;   // odd number of do
 // coalesced 256-byte line pair, and every element offset is a compile-time
 // immediate (e * BLOCK * 8 bytes) from ONE base pointer per thread -- no
 // per-element address registers (which otherwise spill).
-template <int N>
+template <int N, long long SS = BDFB_TPC_BLOCK, bool MATS = true>
 struct TWs {
   static constexpr int O_ZN = 0, O_EWT = (QMAX + 1) * N, O_ACOR = O_EWT + N, O_YQ = O_ACOR + N, O_DEL = O_YQ + N,
-                       O_FEXT = O_DEL + N, O_INVD = O_FEXT + N, O_J = O_INVD + N, O_LU = O_J + N * N,
-                       DOUBLES = O_LU + N * N, INTS = N;
-  static constexpr long long S = BDFB_TPC_BLOCK;
+                       O_FEXT = O_DEL + N, O_INVD = O_FEXT + N, O_FR = O_INVD + N, O_J = O_FR + N,
+                       O_LU = O_J + N * N, DOUBLES = MATS ? O_LU + N * N : O_J, INTS = MATS ? N : 0;
+  static constexpr long long S = SS;
   double* w;
   int* iw;
   __device__ __forceinline__ double& at(int e) const { return w[(long long)e * S]; }
@@ -84,6 +85,7 @@ struct TWs {
   __device__ __forceinline__ double& del(int i) const { return at(O_DEL + i); }
   __device__ __forceinline__ double& fext(int i) const { return at(O_FEXT + i); }
   __device__ __forceinline__ double& invd(int i) const { return at(O_INVD + i); }
+  __device__ __forceinline__ double& fr(int i) const { return at(O_FR + i); }
   __device__ __forceinline__ double& J(int i, int j) const { return at(O_J + i * N + j); }
   __device__ __forceinline__ double& LU(int i, int j) const { return at(O_LU + i * N + j); }
   __device__ __forceinline__ int& perm(int i) const { return iw[(long long)i * S]; }
@@ -261,10 +263,10 @@ __device__ __forceinline__ int nth_bit(unsigned m, int n) {
 // The Nordsieck vector work of a step is fused into two element-wise passes
 // (registers per component): ERRTEST (complete step + the order-selection
 // norms) and ATTEMPT (weights O1 + RESCALE + PREDICT + Newton start).
-template <class Mech, class GM>
+template <class Mech, class GM, long long SS = BDFB_TPC_BLOCK, bool MATS = true>
 struct TpcIntegrator {
   static constexpr int N = Mech::N;
-  using W = TWs<N>;
+  using W = TWs<N, SS, MATS>;
   // warp-cooperative stages (Jacobian, LU): one cell per group of G lanes of
   // the group model GM (csrc/mech_model.cuh), GPW cells at a time per warp
   static constexpr int G = GM::G, GPW = 32 / G;
@@ -291,6 +293,7 @@ struct TpcIntegrator {
   __device__ static __noinline__ void restore(TS& s, const W& w) {
     s.tn = s.saved_t;
     const int q = s.q;
+#pragma unroll 2
     for (int i = 0; i < N; ++i) {
       double z[QMAX + 1];
 #pragma unroll
@@ -371,10 +374,13 @@ struct TpcIntegrator {
     }
     const double A1 = (-alpha0 - alpha1) / prod;
     const int q = s.q;
+#pragma unroll
     for (int i = 0; i < N; ++i) {
       const double zL = A1 * w.zn(o.qmax, i);
       w.zn(q + 1, i) = zL;
-      for (int j = 2; j <= q; ++j) w.zn(j, i) = l[j] * zL + w.zn(j, i);
+#pragma unroll
+      for (int j = 2; j <= QMAX; ++j)
+        if (j <= q) w.zn(j, i) = l[j] * zL + w.zn(j, i);
     }
   }
 
@@ -390,9 +396,12 @@ struct TpcIntegrator {
       for (int i = j + 2; i >= 2; --i) l[i] = l[i] * xi + l[i - 1];
     }
     const int q = s.q;
+#pragma unroll
     for (int i = 0; i < N; ++i) {
       const double zq = w.zn(q, i);
-      for (int j = 2; j < q; ++j) w.zn(j, i) = -l[j] * zq + w.zn(j, i);
+#pragma unroll
+      for (int j = 2; j < QMAX; ++j)
+        if (j < q) w.zn(j, i) = -l[j] * zq + w.zn(j, i);
     }
   }
 
@@ -455,6 +464,7 @@ struct TpcIntegrator {
     } else {
       s.eta = etaqp1;
       s.qprime = s.q + 1;
+#pragma unroll
       for (int i = 0; i < N; ++i) w.zn(o.qmax, i) = w.acor(i);
     }
     set_eta(o, s);
@@ -700,26 +710,42 @@ struct TpcIntegrator {
 #pragma unroll
       for (int j = 0; j <= QMAX; ++j) lj[j] = s.l[j];
       double sdn = 0.0, sup = 0.0;
-#pragma unroll 4
-      for (int i = 0; i < N; ++i) {
-        const double a = w.acor(i);
-        double zq = 0.0;
+      // chunks of CH components: all loads of a chunk are issued before its
+      // arithmetic and stores (memory-level parallelism on the workspace)
+      constexpr int CH = (N % 4 == 0) ? 4 : 2;
+      static_assert(N % CH == 0, "chunking");
+#pragma unroll 1
+      for (int i0 = 0; i0 < N; i0 += CH) {
+        double a[CH], e[CH], zm[CH], z[CH][QMAX + 1];
 #pragma unroll
-        for (int j = 0; j <= QMAX; ++j)
-          if (j <= q) {
-            const double z = lj[j] * a + w.zn(j, i);
-            w.zn(j, i) = z;
-            if (j == q) zq = z;
-          }
-        if (fq) w.zn(qmax, i) = a;
-        const double e = w.ewt(i);
-        if (nm1) {
-          const double p = zq * e;
-          sdn = sdn + p * p;
+        for (int c = 0; c < CH; ++c) {
+          a[c] = w.acor(i0 + c);
+          e[c] = w.ewt(i0 + c);
+          zm[c] = np1 ? w.zn(qmax, i0 + c) : 0.0;
+#pragma unroll
+          for (int j = 0; j <= QMAX; ++j) z[c][j] = (j <= q) ? w.zn(j, i0 + c) : 0.0;
         }
-        if (np1) {
-          const double p = (-cquot * w.zn(qmax, i) + a) * e;
-          sup = sup + p * p;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const int i = i0 + c;
+          double zq = 0.0;
+#pragma unroll
+          for (int j = 0; j <= QMAX; ++j)
+            if (j <= q) {
+              const double zz = lj[j] * a[c] + z[c][j];
+              w.zn(j, i) = zz;
+              if (j == q) zq = zz;
+            }
+          if (fq) w.zn(qmax, i) = a[c];
+          if (nm1) {
+            const double p = zq * e[c];
+            sdn = sdn + p * p;
+          }
+          if (np1) {
+            // zn[qmax] as read before this pass (fq and np1 are exclusive: qwait = 1 vs 0)
+            const double p = (-cquot * zm[c] + a[c]) * e[c];
+            sup = sup + p * p;
+          }
         }
       }
       prepare_next(o, s, w, dsm, sqrt(sdn / (double)N), sqrt(sup / (double)N));
@@ -808,27 +834,36 @@ struct TpcIntegrator {
       }
     }
     const double rtol = o.rtol;
-#pragma unroll 4
-    for (int i = 0; i < N; ++i) {
-      double z[QMAX + 1];
+    constexpr int CH = (N % 4 == 0) ? 4 : 2;
+    static_assert(N % CH == 0, "chunking");
+#pragma unroll 1
+    for (int i0 = 0; i0 < N; i0 += CH) {
+      double zc[CH][QMAX + 1];
 #pragma unroll
-      for (int j = 0; j <= QMAX; ++j) z[j] = (j <= q) ? w.zn(j, i) : 0.0;
-      if (fl & F_EWT) w.ewt(i) = 1.0 / (rtol * fabs(z[0]) + atol[i]);
-      if (fl & F_RESCALE) {
+      for (int c = 0; c < CH; ++c)
 #pragma unroll
-        for (int j = 1; j <= QMAX; ++j)
-          if (j <= q) z[j] = f[j] * z[j];
+        for (int j = 0; j <= QMAX; ++j) zc[c][j] = (j <= q) ? w.zn(j, i0 + c) : 0.0;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int i = i0 + c;
+        double* z = zc[c];
+        if (fl & F_EWT) w.ewt(i) = 1.0 / (rtol * fabs(z[0]) + atol[i]);
+        if (fl & F_RESCALE) {
+#pragma unroll
+          for (int j = 1; j <= QMAX; ++j)
+            if (j <= q) z[j] = f[j] * z[j];
+        }
+#pragma unroll
+        for (int k = 1; k <= QMAX; ++k)
+#pragma unroll
+          for (int j = QMAX; j >= 1; --j)
+            if (k <= q && j >= k && j <= q) z[j - 1] = z[j - 1] + z[j];
+#pragma unroll
+        for (int j = 0; j <= QMAX; ++j)
+          if (j <= q) w.zn(j, i) = z[j];
+        w.yq(i) = z[0];
+        w.acor(i) = 0.0;
       }
-#pragma unroll
-      for (int k = 1; k <= QMAX; ++k)
-#pragma unroll
-        for (int j = QMAX; j >= 1; --j)
-          if (k <= q && j >= k && j <= q) z[j - 1] = z[j - 1] + z[j];
-#pragma unroll
-      for (int j = 0; j <= QMAX; ++j)
-        if (j <= q) w.zn(j, i) = z[j];
-      w.yq(i) = z[0];
-      w.acor(i) = 0.0;
     }
     s.tn = s.tn + s.h;
     if ((s.tn - o.tf) * s.h > 0.0) s.tn = o.tf;
@@ -1078,8 +1113,8 @@ struct TpcIntegrator {
   }
 };
 
-template <class Mech, class GM>
-__device__ typename TpcIntegrator<Mech, GM>::W TpcIntegrator<Mech, GM>::ws_of(int l) {
+template <class Mech, class GM, long long SS, bool MATS>
+__device__ typename TpcIntegrator<Mech, GM, SS, MATS>::W TpcIntegrator<Mech, GM, SS, MATS>::ws_of(int l) {
   extern __shared__ double smem[];
   double* const* bases = reinterpret_cast<double* const*>(smem + BDFB_TPC_BLOCK * TS_STRIDE);
   int* const* ibases = reinterpret_cast<int* const*>(smem + BDFB_TPC_BLOCK * TS_STRIDE + 1);

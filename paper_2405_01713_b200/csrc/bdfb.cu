@@ -22,6 +22,8 @@
 #include "mech_model.cuh"
 #include "models_simple.cuh"
 #include "tpc_api.h"
+#include "bdf_split.cuh"
+#include "split_api.h"
 
 using namespace bdfb;
 
@@ -51,11 +53,18 @@ struct bdfb_batch {
   double* d_ws = nullptr;          // thread-per-cell workspace (bdf_tpc.cuh), sized for the resident grid
   int* d_iws = nullptr;
   long long ws_slots = 0;
+  SplitBufs sb{};                  // SPLIT kernel slot pool (bdf_split.cuh)
+  SplitGeom sgeom{};
+  unsigned long long* h_live = nullptr;   // pinned: live-slot count read back per launch batch
   std::string err;
 };
 
 static bool is_mech(int model) { return model == BDFB_MODEL_MECH_H2 || model == BDFB_MODEL_MECH_DRM19; }
-static bool use_tpc(const bdfb_batch* b) { return is_mech(b->model) && b->kernel != BDFB_KERNEL_GROUP; }
+// mechanism models: AUTO = SPLIT (the fastest organisation measured on B200, profiles/r1)
+static bool use_split(const bdfb_batch* b) {
+  return is_mech(b->model) && (b->kernel == BDFB_KERNEL_SPLIT || b->kernel == BDFB_KERNEL_AUTO);
+}
+static bool use_tpc(const bdfb_batch* b) { return is_mech(b->model) && b->kernel == BDFB_KERNEL_THREAD; }
 
 static std::string g_err;
 
@@ -81,7 +90,74 @@ static int model_n(int model) {
 
 // ---- thread-per-cell mechanism kernel (csrc/tpc.cu): the per-slot workspace is
 // sized once for the resident grid (host setup, never in bdfb_integrate).
+static void free_split(bdfb_batch* b) {
+  cudaFree(b->sb.vec);
+  cudaFree(b->sb.ts);
+  cudaFree(b->sb.J);
+  cudaFree(b->sb.LU);
+  cudaFree(b->sb.rv);
+  cudaFree(b->sb.slist);
+  cudaFree(b->sb.jlist);
+  cudaFree(b->sb.cnt);
+  cudaFree(b->sb.live);
+  b->sb = SplitBufs{};
+}
+
+// SPLIT kernel: slot pool of S = min(n_cells rounded up to 32, BDFB_SPLIT_SLOTS env or 262144) slots
+static int prepare_split(bdfb_batch* b) {
+  cudaError_t e = cudaSetDevice(b->device);
+  SplitGeom gm{};
+  if (e == cudaSuccess) e = split_geometry(b->model, b->device, &gm);
+  if (e != cudaSuccess) return cuda_fail(b, e, "split geometry");
+  long long cap = 262144;
+  if (const char* env = getenv("BDFB_SPLIT_SLOTS")) cap = atoll(env) > 0 ? atoll(env) : cap;
+  long long S = b->ncells < cap ? b->ncells : cap;
+  S = (S + 31) / 32 * 32;
+  if (S != b->sb.slots || gm.vec_doubles != b->sgeom.vec_doubles || gm.lurec != b->sgeom.lurec) {
+    free_split(b);
+    bool ok = true;
+    auto A = [&](void** p, size_t bytes) { if (ok && cudaMalloc(p, bytes) != cudaSuccess) ok = false; };
+    A((void**)&b->sb.vec, sizeof(double) * (size_t)gm.vec_doubles * S);
+    A((void**)&b->sb.ts, sizeof(double) * (size_t)gm.ts_doubles * S);
+    A((void**)&b->sb.J, sizeof(double) * (size_t)gm.jrec * S);
+    A((void**)&b->sb.LU, sizeof(double) * (size_t)gm.lurec * S);
+    A((void**)&b->sb.rv, sizeof(int) * (size_t)S);
+    A((void**)&b->sb.slist, sizeof(int) * (size_t)S);
+    A((void**)&b->sb.jlist, sizeof(int) * (size_t)S);
+    A((void**)&b->sb.cnt, 2 * sizeof(unsigned));
+    A((void**)&b->sb.live, 2 * sizeof(unsigned long long));
+    if (!ok) {
+      free_split(b);
+      return fail(b, BDFB_ENOMEM, "split slot pool");
+    }
+    b->sb.slots = S;
+  }
+  if (!b->h_live && cudaHostAlloc((void**)&b->h_live, sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess)
+    return fail(b, BDFB_ENOMEM, "pinned live counter");
+  b->sgeom = gm;
+  return BDFB_OK;
+}
+
+static int launch_split(bdfb_batch* b, const Opts& o, double* y, const double* fext, const double* aux,
+                        cudaStream_t st) {
+  if (b->sb.slots < 1) return fail(b, BDFB_ENOMODEL, "split slot pool not prepared");
+  cudaMemsetAsync(b->d_counter, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(b->d_agg, 0, sizeof(Agg), st);
+  cudaEventRecord(b->ev0, st);
+  int launches = 0;
+  int batch = 16;
+  if (const char* env = getenv("BDFB_SPLIT_BATCH")) batch = atoi(env) > 0 ? atoi(env) : batch;
+  cudaError_t e = split_integrate(b->model, o, y, fext, aux, b->d_atol, b->sb, b->sgeom, b->d_counter, b->d_agg,
+                                  b->cs, b->h_live, batch, st, &launches);
+  cudaEventRecord(b->ev1, st);
+  if (e != cudaSuccess) return cuda_fail(b, e, "split integrate");
+  b->launches = launches;
+  b->timed = true;
+  return BDFB_OK;
+}
+
 static int prepare_kernel(bdfb_batch* b) {
+  if (b->opt.mode == BDFB_MODE_PER_CELL && use_split(b)) return prepare_split(b);
   if (b->opt.mode != BDFB_MODE_PER_CELL || !use_tpc(b)) return BDFB_OK;
   long long slots = 0, dps = 0, ips = 0;
   cudaError_t e = cudaSetDevice(b->device);
@@ -205,6 +281,8 @@ void bdfb_destroy(bdfb_batch* b) {
   if (b->d_aux) cudaFree(b->d_aux);
   if (b->d_ws) cudaFree(b->d_ws);
   if (b->d_iws) cudaFree(b->d_iws);
+  free_split(b);
+  if (b->h_live) cudaFreeHost(b->h_live);
   {
     GlobalBuffers& g = b->gb;
     for (int j = 0; j <= QMAX; ++j) cudaFree(g.v.zn[j]);
@@ -259,7 +337,8 @@ int bdfb_set_model(bdfb_batch* b, int32_t model_id, const void* params, size_t b
 
 int bdfb_set_kernel(bdfb_batch* b, int32_t kernel) {
   if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
-  if (kernel != BDFB_KERNEL_AUTO && kernel != BDFB_KERNEL_THREAD && kernel != BDFB_KERNEL_GROUP)
+  if (kernel != BDFB_KERNEL_AUTO && kernel != BDFB_KERNEL_THREAD && kernel != BDFB_KERNEL_GROUP &&
+      kernel != BDFB_KERNEL_SPLIT)
     return fail(b, BDFB_EINVAL, "bad kernel id");
   b->kernel = kernel;
   return b->model >= 0 ? prepare_kernel(b) : BDFB_OK;
@@ -268,7 +347,7 @@ int bdfb_set_kernel(bdfb_batch* b, int32_t kernel) {
 int32_t bdfb_wrms_group(const bdfb_batch* b) {
   if (!b || b->model < 0) return 0;
   if (b->opt.mode == BDFB_MODE_GLOBAL_NORM) return b->model == BDFB_MODEL_MECH_H2 ? ModelH2::G : ModelDRM19::G;
-  if (use_tpc(b)) return 1;
+  if (use_tpc(b) || use_split(b)) return 1;
   switch (b->model) {
     case BDFB_MODEL_MECH_H2: return ModelH2::G;
     case BDFB_MODEL_MECH_DRM19: return ModelDRM19::G;
@@ -456,9 +535,11 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
     case BDFB_MODEL_ROBERTSON: return launch_integrate<ModelRobertson>(b, o, y, f_ext, aux, st);
     case BDFB_MODEL_NYX_KWH: return launch_integrate<ModelNyxKwh>(b, o, y, f_ext, aux, st);
     case BDFB_MODEL_MECH_H2:
+      if (use_split(b)) return launch_split(b, o, y, f_ext, aux, st);
       return use_tpc(b) ? launch_tpc(b, o, y, f_ext, aux, st)
                         : launch_integrate<ModelH2>(b, o, y, f_ext, aux, st);
     case BDFB_MODEL_MECH_DRM19:
+      if (use_split(b)) return launch_split(b, o, y, f_ext, aux, st);
       return use_tpc(b) ? launch_tpc(b, o, y, f_ext, aux, st)
                         : launch_integrate<ModelDRM19>(b, o, y, f_ext, aux, st);
   }
@@ -641,11 +722,11 @@ extern "C" int bdfb_eval_rhs(bdfb_batch* b, double t, const double* y, const dou
     case BDFB_MODEL_ROBERTSON: return launch_eval<ModelRobertson>(b, t, y, f_ext, aux, f, status, nullptr, st);
     case BDFB_MODEL_NYX_KWH: return launch_eval<ModelNyxKwh>(b, t, y, f_ext, aux, f, status, nullptr, st);
     case BDFB_MODEL_MECH_H2:
-      return use_tpc(b) ? launch_eval_tpc(b, y, f_ext, aux, f, status, nullptr, st)
-                        : launch_eval<ModelH2>(b, t, y, f_ext, aux, f, status, nullptr, st);
+      return (use_tpc(b) || use_split(b)) ? launch_eval_tpc(b, y, f_ext, aux, f, status, nullptr, st)
+                                          : launch_eval<ModelH2>(b, t, y, f_ext, aux, f, status, nullptr, st);
     case BDFB_MODEL_MECH_DRM19:
-      return use_tpc(b) ? launch_eval_tpc(b, y, f_ext, aux, f, status, nullptr, st)
-                        : launch_eval<ModelDRM19>(b, t, y, f_ext, aux, f, status, nullptr, st);
+      return (use_tpc(b) || use_split(b)) ? launch_eval_tpc(b, y, f_ext, aux, f, status, nullptr, st)
+                                          : launch_eval<ModelDRM19>(b, t, y, f_ext, aux, f, status, nullptr, st);
   }
   return fail(b, BDFB_ENOMODEL, "unknown model");
 }

@@ -1,0 +1,114 @@
+// split.cu -- the SPLIT per-cell integrator (bdf_split.cuh): slot pool
+// geometry, the five kernels of a trip and the host loop that enqueues them;
+// a translation unit of libbdfb.so, used by bdfb.cu through split_api.h.
+#include <cuda_runtime.h>
+
+#include "../../include/bdfb.h"
+#include "bdf_split.cuh"
+#include "gen/mech_drm19_class.cuh"
+#include "gen/mech_h2_lidryer.cuh"
+#include "gen/tpc_drm19_class.cuh"
+#include "gen/tpc_h2_lidryer.cuh"
+#include "mech_model.cuh"
+#include "split_api.h"
+
+namespace bdfb {
+namespace {
+
+template <class Mech, class GM>
+struct SplitK {
+  using SP = Split<Mech, GM>;
+  static constexpr size_t ctl_smem() { return sizeof(double) * (size_t)TS_STRIDE * BDFB_SPLIT_BLOCK; }
+  static constexpr size_t jac_smem() {
+    return sizeof(double) * (size_t)(GM::SG + GM::JG + GM::N * (GM::N | 1)) * (BDFB_SPLIT_BLOCK / GM::G);
+  }
+
+  static cudaError_t geometry(int device, SplitGeom* gm) {
+    cudaError_t e;
+    const int sm = (int)ctl_smem();
+    if ((e = cudaFuncSetAttribute(split_ctl_kernel<Mech, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) !=
+        cudaSuccess)
+      return e;
+    int nsm = 0, pr = 0;
+    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pr, split_rhs_kernel<Mech, GM>, BDFB_SPLIT_BLOCK, 0)) !=
+        cudaSuccess)
+      return e;
+    if (pr < 1) return cudaErrorInvalidConfiguration;
+    if (jac_smem() > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(split_jac_kernel<Mech, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)jac_smem())) != cudaSuccess)
+      return e;
+    gm->rhs_grid = nsm * pr;
+    gm->setup_grid = nsm * 8;
+    gm->vec_doubles = SP::D;
+    gm->ts_doubles = TS_STRIDE;
+    gm->jrec = SP::JREC;
+    gm->lurec = SP::LUREC;
+    return cudaSuccess;
+  }
+
+  static cudaError_t run(const Opts& o, double* y, const double* fext, const double* aux, const double* atol,
+                         const SplitBufs& b, const SplitGeom& gm, unsigned long long* counter, Agg* agg,
+                         const CellStatsPtrs& cs, unsigned long long* h_live, int batch, cudaStream_t st,
+                         int* launches) {
+    const long long S = b.slots;
+    const unsigned blk = BDFB_SPLIT_BLOCK;
+    const unsigned gs = (unsigned)((S + blk - 1) / blk);            // one thread per slot / list entry
+    // setup kernels: persistent grids, one group of G lanes per list entry (grid-stride)
+    unsigned glu = (unsigned)((S * GM::G + blk - 1) / blk);
+    if (glu > (unsigned)gm.setup_grid) glu = (unsigned)gm.setup_grid;
+    unsigned grhs = (unsigned)gm.rhs_grid;
+    if (grhs > gs) grhs = gs;
+    const size_t sm = ctl_smem();
+    split_init_kernel<Mech, GM><<<gs, blk, 0, st>>>(b);
+    int n = 1;
+    cudaError_t e;
+    for (int it = 0;;) {
+      for (int k = 0; k < batch; ++k, ++it) {
+        split_ctl_kernel<Mech, GM><<<gs, blk, sm, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
+        split_jac_kernel<Mech, GM><<<glu, blk, jac_smem(), st>>>(b);
+        split_lu_kernel<Mech, GM><<<glu, blk, 0, st>>>(b);
+        split_rhs_kernel<Mech, GM><<<grhs, blk, 0, st>>>(b, it);
+        n += 4;
+      }
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      // live slots after the last pass A of the batch (iteration it - 1)
+      if ((e = cudaMemcpyAsync(h_live, &b.live[(it - 1) & 1], sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               st)) != cudaSuccess)
+        return e;
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+      if (*h_live == 0) break;
+    }
+    *launches = n;
+    return cudaSuccess;
+  }
+};
+
+using KH2 = SplitK<Tpc_h2_lidryer, ModelMech<mech_h2_lidryer::Traits>>;
+using KDRM = SplitK<Tpc_drm19_class, ModelMech<mech_drm19_class::Traits>>;
+
+}  // namespace
+
+cudaError_t split_geometry(int mech, int device, SplitGeom* gm) {
+  switch (mech) {
+    case BDFB_MODEL_MECH_H2: return KH2::geometry(device, gm);
+    case BDFB_MODEL_MECH_DRM19: return KDRM::geometry(device, gm);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t split_integrate(int mech, const Opts& o, double* y, const double* fext, const double* aux,
+                            const double* atol, const SplitBufs& sb, const SplitGeom& gm, unsigned long long* counter,
+                            Agg* agg, const CellStatsPtrs& cs, unsigned long long* h_live, int batch,
+                            cudaStream_t st, int* launches) {
+  switch (mech) {
+    case BDFB_MODEL_MECH_H2:
+      return KH2::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches);
+    case BDFB_MODEL_MECH_DRM19:
+      return KDRM::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace bdfb

@@ -1,0 +1,30 @@
+// split_api.h -- internal (not ABI) host interface of the SPLIT per-cell
+// integrator (split.cu, bdf_split.cuh), used by bdfb.cu.  `mech` is a
+// BDFB_MODEL_MECH_* id; functions return a CUDA error code
+// (cudaErrorInvalidValue for an unknown id).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "bdf_cell.cuh"   // Opts, Agg, CellStatsPtrs
+
+namespace bdfb {
+
+struct SplitBufs;
+
+struct SplitGeom {
+  int rhs_grid;                            // resident blocks of K_rhs on the device
+  int setup_grid;                          // blocks of the (grid-stride) Jacobian / LU kernels
+  int vec_doubles, ts_doubles, jrec, lurec;   // doubles per slot of the VEC, TS, J and LU records
+};
+
+cudaError_t split_geometry(int mech, int device, SplitGeom* gm);
+
+// Integrate all o.ncells cells through the slot pool sb (host loop over
+// K_ctl/K_rhs launch batches of `batch` iterations on st, one live-count read
+// back per batch; synchronous).  launches: kernels enqueued.
+cudaError_t split_integrate(int mech, const Opts& o, double* y, const double* fext, const double* aux,
+                            const double* atol, const SplitBufs& sb, const SplitGeom& gm, unsigned long long* counter,
+                            Agg* agg, const CellStatsPtrs& cs, unsigned long long* h_live, int batch,
+                            cudaStream_t st, int* launches);
+
+}  // namespace bdfb

@@ -64,16 +64,16 @@ for s in steps:
             run("nyx_kwh", "kwh", 1, e, 3e15, 1e-6, 1e-10, rho=rho, F=fe)
         if s == "h2":
             y, rho, F, prog = flame_field("h2_lidryer", 16)
-            for k in ("thread", "group"):
+            for k in ("thread", "group", "split"):
                 run("h2", "h2_lidryer", 10, y, 1e-5, 1e-6, 1e-10, rho=rho, F=F, kernel=k)
         if s == "drm":
             y, rho, F, prog = flame_field("drm19_class", 16)
-            for k in ("thread", "group"):
+            for k in ("thread", "group", "split"):
                 run("drm19", "drm19_class", 22, y, 1e-5, 1e-6, 1e-10, rho=rho, F=F, kernel=k)
         if s == "time":
             L = int(os.environ.get("L", "64"))
             y, rho, F, prog = flame_field("drm19_class", L)
-            for k in ("thread", "group", "thread"):
+            for k in os.environ.get("KS", "thread,split").split(","):
                 b = P.Batch(y.shape[1], 22, 1e-6, 1e-10)
                 b.set_kernel(k)
                 b.set_model("drm19")

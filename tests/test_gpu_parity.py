@@ -22,7 +22,7 @@ from synth.fields import stratified_sample  # noqa: E402
 DEV = torch.device("cuda", 0)
 STAT_KEYS = ("nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn")
 MECH = {"h2": ("h2_lidryer", 10), "drm19": ("drm19_class", 22)}
-KERNELS = ("thread", "group")   # per-cell kernel organisations of the mechanism models (bdfb_set_kernel)
+KERNELS = ("split", "thread", "group")   # per-cell kernel organisations of the mechanism models (bdfb_set_kernel)
 
 
 def cu(a):
@@ -36,7 +36,7 @@ def end_state_check(yg, yo, rtol, atol, frac_min=0.0):
     assert ok.all(), f"{(~ok.all(axis=0)).sum()} cells outside 10 tol; worst {np.max(err / tol):.3g}"
 
 
-def run_gpu(model, n, y0, t1, rtol, atol, rho=None, F=None, layout="YC", kernel="thread", **kw):
+def run_gpu(model, n, y0, t1, rtol, atol, rho=None, F=None, layout="YC", kernel="auto", **kw):
     """Integrate on the GPU; st carries the aggregate stats plus "group", the WRMS lane-group
     size (reading R15) of the kernel used, which the oracle reproduces."""
     N = y0.shape[1]
@@ -99,7 +99,8 @@ def oracle_model(oracle, name):
 
 
 @pytest.mark.parametrize("name,kernel", [("robertson", "thread"), ("nyx_kwh", "thread"), ("h2", "thread"),
-                                         ("h2", "group"), ("drm19", "thread"), ("drm19", "group")])
+                                         ("h2", "group"), ("h2", "split"), ("drm19", "thread"), ("drm19", "group"),
+                                         ("drm19", "split")])
 def test_rhs_parity(oracle, name, kernel):
     y, rho, F = model_states(name, 32768)
     n, N = y.shape
@@ -125,7 +126,8 @@ def test_rhs_parity(oracle, name, kernel):
 
 
 @pytest.mark.parametrize("name,kernel", [("robertson", "thread"), ("h2", "thread"), ("h2", "group"),
-                                         ("drm19", "thread"), ("drm19", "group")])
+                                         ("h2", "split"), ("drm19", "thread"), ("drm19", "group"),
+                                         ("drm19", "split")])
 def test_jacobian_parity(oracle, name, kernel):
     y, rho, F = model_states(name, 4096)
     n, N = y.shape
@@ -282,3 +284,35 @@ def test_global_norm_mode_parity(oracle, name, L, dt):
     assert st["nst"] == so["nst"] and st["nfe"] == so["nfe"] and st["netf"] == so["netf"]
     end_state_check(y.cpu().numpy(), yo, 1e-6, 1e-10)
     assert np.all(cs["nst"].cpu().numpy() == so["nst"])
+
+
+def test_full_size_c4_sampled(oracle):
+    """C4 at its BASELINE size (256^3 = 16.7M DRM19-class cells) in exactly the launch
+    configuration bench.py times (default thread-per-cell kernel, one persistent launch);
+    end-state parity on a stratified sample the oracle integrates cell by cell, plus the
+    conservation check (sum_k Y_k, F_Y = 0) on every cell."""
+    mech, n = MECH["drm19"]
+    y0, rho, F, prog = flame_field(mech, 256, dt=1e-5)
+    yg, sg, st = run_gpu("drm19", n, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    assert st["n_failed"] == 0 and st["n_cells"] == 256 ** 3
+    s0 = y0[:-1].sum(axis=0)
+    assert np.abs(yg[:-1].sum(axis=0) - s0).max() <= 1e-13
+    idx = stratified_sample(prog, 240)
+    yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0[:, idx], 0.0, 1e-5, 1e-6, 1e-10, rho=rho[idx],
+                                    fext_yc=F[:, idx], group=st["group"], threads=8)
+    end_state_check(yg[:, idx], yo, 1e-6, 1e-10)
+    assert np.array_equal(sg["status"][idx], so["status"])
+
+
+def test_full_size_c2_sampled(oracle):
+    """C2 at its BASELINE size (128^3 Nyx cells, n = 1) as bench.py launches it; parity on sampled cells."""
+    e, rho, fe = nyx_field(128)
+    dt = 3e15
+    yg, sg, st = run_gpu("nyx_kwh", 1, e, dt, 1e-6, 1e-10, rho=rho, F=fe)
+    assert st["n_cells"] == 128 ** 3
+    idx = np.sort(np.random.default_rng(7).choice(128 ** 3, 2000, replace=False))
+    yo, so = oracle.integrate_batch(oracle.Model.nyx_kwh(), e[:, idx], 0.0, dt, 1e-6, 1e-10, rho=rho[idx],
+                                    fext_yc=fe[:, idx], threads=8)
+    assert np.array_equal(sg["status"][idx], so["status"])
+    ok = so["status"] == 0
+    end_state_check(yg[:, idx][:, ok], yo[:, ok], 1e-6, 1e-10)
