@@ -107,12 +107,49 @@ def hbm_bytes_global(cfg, st):
     return per_cell * st["n_cells"]
 
 
+TS_RECORD_BYTES = 456          # struct TS record of the SPLIT slot pool (TS_STRIDE = 57 doubles, csrc/bdf_tpc.cuh)
+QBAR = 3                       # mean BDF order assumed by the byte model (zn[0..q] rows moved per pass)
+
+
+def ctl_bytes(cfg, st):
+    """Bytes the SPLIT control kernel K_ctl must move per integrate: every visit of a slot
+    (one per consumed RHS value and one per resumed setup) reads and writes the cell's TS record; a
+    consumed Newton residual reads fr, zn[1], acor and writes del (32n + 4); a Newton solve streams the
+    LU record (8n^2 + 12n) and moves del, acor (r/w), ewt, zn[0], yq (48n); a completed step and an
+    attempt each read and write zn[0..q] (16 (q+1) n) plus acor/ewt (16n) or ewt/yq/acor (24n)."""
+    n = CONFIGS[cfg][2]
+    att = st["nst"] + st["netf"] + st["ncfn"]
+    trips = st["nfe"] + st["nsetups"]
+    zq = 16 * (QBAR + 1) * n
+    return (trips * 2 * TS_RECORD_BYTES + st["nfe"] * (32 * n + 4) + st["nni"] * (8 * n * n + 12 * n + 48 * n) +
+            st["nst"] * (zq + 16 * n) + att * (zq + 24 * n))
+
+
+def rhs_flops(cfg, st):
+    """Algorithmic FP64 flops of the RHS evaluations (the K_rhs kernel of SPLIT)."""
+    model, mech, n, *_ = CONFIGS[cfg]
+    hdr = open(os.path.join(REPO, "paper_2405_01713_b200", "csrc", "gen", f"mech_{mech}.cuh")).read()
+    g = lambda k: int(re.search(rf"{k} = (\d+)", hdr).group(1))  # noqa: E731
+    return st["nfe"] * (g("FLOPS_RHS_ARITH") + TRANSC_FLOPS * g("RHS_TRANSCENDENTALS"))
+
+
 def hbm_peak():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
     except Exception:
         return 7700.0, "fallback: B200 nominal HBM3e 7.7 TB/s"
+
+
+def traffic_split(cfg, st):
+    """K_ctl DRAM bytes (read + write) per integrate, scaled per slot visit from the committed ncu --set full
+    capture of one K_ctl launch (profiles/traffic.json "split_ctl": dram bytes / slots visited)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            t = json.load(f)["split_ctl_" + cfg]
+        return t["dram_bytes_per_visit"] * (st["nfe"] + st["nsetups"])
+    except Exception:
+        return None
 
 
 def traffic_per_launch(cfg, cells):
@@ -309,7 +346,7 @@ def main():
     st_w = b.stats()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kern_ms, stats = [], []
+    kern_ms, stats, phase_ms = [], [], []
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             y.copy_(y_pristine)
@@ -322,6 +359,7 @@ def main():
             torch.cuda.synchronize()
             kern_ms.append(b.last_kernel_ms())
             stats.append(b.stats())
+            phase_ms.append(b.phase_ms())
     step_ms = [a.elapsed_time(z) for a, z in ev]
     total_ms = PL.max_over_ranks(sum(step_ms), dist, dev)
     ms_per_step = total_ms / args.steps
@@ -346,6 +384,28 @@ def main():
             "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
             "fp64_probe_tflops": probe, "kernel_ms": statistics.mean(kern_ms),
             "flops_per_launch": statistics.mean(flops)}
+    phases = None
+    if phase_ms and phase_ms[0]:
+        # SPLIT: four kernels per trip; the roofline is that of the dominant one, K_ctl (HBM-bound: the slot
+        # pool's state round trip + the LU record of every Newton solve), with the whole-step FP64 fraction beside
+        hpk, src = hbm_peak()
+        pm = {k: statistics.mean(p[k] for p in phase_ms) for k in phase_ms[0]}
+        tot = sum(pm.values())
+        cb = statistics.mean(ctl_bytes(cfg, s) for s in stats)
+        rf = statistics.mean(rhs_flops(cfg, s) for s in stats)
+        ctl_gbs = cb / (pm["ctl"] * 1e-3) / 1e9
+        rhs_tf = rf / (pm["rhs"] * 1e-3) / 1e12
+        phases = {k: {"ms": v, "share": v / tot} for k, v in pm.items()}
+        phases["ctl"].update({"bound": "hbm", "gbs": ctl_gbs, "frac": ctl_gbs / hpk, "bytes": cb})
+        phases["rhs"].update({"bound": "alu", "tflops": rhs_tf, "frac": rhs_tf / peak, "flops": rf})
+        roof = {"bound": "hbm", "achieved": ctl_gbs, "peak": hpk, "unit": "GB/s", "frac": ctl_gbs / hpk,
+                "traffic": traffic_split(cfg, stats[-1]), "kernel": f"split_ctl_kernel<Tpc_{mech}> (K_ctl, "
+                f"{100 * pm['ctl'] / tot:.0f}% of the step)", "peak_source": src,
+                "kernel_ms": pm["ctl"], "bytes_per_integrate": cb,
+                "bytes_model": "DESIGN.md §6: per visit 2 TS records, per RHS value 32n+4, per Newton solve "
+                               "8n^2+60n, per step/attempt zn[0..q] r/w (q=3) + vectors",
+                "fp64_whole_step": {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                                    "flops_per_launch": statistics.mean(flops)}}
     if glob_mode:
         # lockstep batch: the state, J and LU stream through HBM every stage -> HBM roofline
         hb = [hbm_bytes_global(cfg, s) for s in stats]
@@ -405,7 +465,7 @@ def main():
                 "clocks": clk.summary(),
                 "stats": {k: s[k] for k in ("n_cells", "n_failed", "nst", "nfe", "nje", "nsetups", "nni", "netf",
                                             "ncfn", "nst_max")},
-                "kernel_ms_per_step": kern_ms}
+                "kernel_ms_per_step": kern_ms, "phases": phases}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

@@ -202,9 +202,17 @@ int bdfb_integrate_host(bdfb_batch *b, double t0, double tf, double *y_host, con
 int64_t bdfb_get_stats(bdfb_batch *b, bdfb_stats *agg);
 
 /* Kernel launches made by the last bdfb_integrate (for bench accounting):
- * 1 in PER_CELL mode (one persistent kernel); in GLOBAL_NORM mode every
- * device kernel the host control loop issued (NCCL's own kernels excluded). */
+ * 1 for the persistent PER_CELL kernels (THREAD, GROUP); for SPLIT and in
+ * GLOBAL_NORM mode every device kernel the host loop issued (NCCL's own
+ * kernels excluded). */
 int32_t bdfb_last_launch_count(const bdfb_batch *b);
+
+/* Device time per kernel phase of the last bdfb_integrate with the SPLIT
+ * kernel, summed over its launches and measured with CUDA events on the
+ * launch stream: ms[0] K_ctl (control + Newton solve), ms[1] K_jac,
+ * ms[2] K_lu, ms[3] K_rhs.  Writes min(count, max) values to ms (host, may
+ * be NULL) and returns the number of phases (0 for the other kernels).     */
+int32_t bdfb_phase_ms(const bdfb_batch *b, double *ms, int32_t max);
 
 /* Device time in milliseconds of the last integrate's main kernel, measured
  * with CUDA events on the launch stream (synchronises that stream).  In

@@ -164,6 +164,12 @@ class Batch:
     def last_kernel_ms(self):
         return float(self._L.bdfb_last_kernel_ms(self.h))
 
+    def phase_ms(self):
+        """SPLIT kernel: device ms per phase of the last integrate (bdfb_phase_ms), else {}."""
+        buf = (C.c_double * 8)()
+        n = int(self._L.bdfb_phase_ms(self.h, buf, 8))
+        return dict(zip(["ctl", "jac", "lu", "rhs"], list(buf)[:n]))
+
     def last_launch_count(self):
         return int(self._L.bdfb_last_launch_count(self.h))
 

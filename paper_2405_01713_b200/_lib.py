@@ -20,7 +20,8 @@ KERNEL_AUTO, KERNEL_THREAD, KERNEL_GROUP, KERNEL_SPLIT = 0, 1, 2, 3
 SYMBOLS = ["bdfb_default_options", "bdfb_create", "bdfb_set_model", "bdfb_set_cell_stats", "bdfb_integrate",
            "bdfb_integrate_host", "bdfb_get_stats", "bdfb_last_launch_count", "bdfb_last_kernel_ms",
            "bdfb_destroy", "bdfb_last_error", "bdfb_version", "bdfb_eval_rhs", "bdfb_eval_jac",
-           "bdfb_lu_factor_solve", "bdfb_probe_fp64", "bdfb_set_comm", "bdfb_set_kernel", "bdfb_wrms_group"]
+           "bdfb_lu_factor_solve", "bdfb_probe_fp64", "bdfb_set_comm", "bdfb_set_kernel", "bdfb_wrms_group",
+           "bdfb_phase_ms"]
 
 
 class Options(C.Structure):
@@ -77,6 +78,8 @@ def lib():
     L.bdfb_get_stats.argtypes = [vp, C.POINTER(Stats)]
     L.bdfb_last_launch_count.restype = i32
     L.bdfb_last_launch_count.argtypes = [vp]
+    L.bdfb_phase_ms.restype = i32
+    L.bdfb_phase_ms.argtypes = [vp, C.POINTER(C.c_double), i32]
     L.bdfb_last_kernel_ms.restype = dp
     L.bdfb_last_kernel_ms.argtypes = [vp]
     L.bdfb_destroy.restype = None

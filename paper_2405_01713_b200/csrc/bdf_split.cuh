@@ -45,6 +45,8 @@
 //        (ints): the Newton solve of a thread streams its own record with
 //        16-byte loads, column by column in the order of the substitutions.
 #pragma once
+#include <utility>
+
 #include "bdf_tpc.cuh"
 
 namespace bdfb {
@@ -224,15 +226,18 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_CTL_MINB)
   if (threadIdx.x < N) satol[threadIdx.x] = atol[threadIdx.x];
   if (lane == 0) wacc[warp] = Agg{};
   if (threadIdx.x == 0) blive = 0;
-  const long long s0 = (long long)blockIdx.x * BDFB_SPLIT_BLOCK;
-  const long long nrec = (b.slots - s0 < BDFB_SPLIT_BLOCK ? b.slots - s0 : BDFB_SPLIT_BLOCK) * TS_STRIDE;
+  // the warp's 32 TS records are contiguous in HBM: stage them through shared memory (coalesced), warp-local
+  const long long w0 = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + (threadIdx.x & ~31u);
+  const long long nrec = (b.slots - w0 < 32 ? (b.slots - w0 > 0 ? b.slots - w0 : 0) : 32) * TS_STRIDE;
+  double* wsm = smem + (threadIdx.x & ~31u) * TS_STRIDE;
   {
-    const double* src = b.ts + s0 * TS_STRIDE;
-    for (long long i = threadIdx.x; i < nrec; i += BDFB_SPLIT_BLOCK) smem[i] = src[i];
+    const double* src = b.ts + w0 * TS_STRIDE;
+#pragma unroll 4
+    for (long long i = lane; i < nrec; i += 32) wsm[i] = src[i];
   }
-  const long long slot = s0 + threadIdx.x;
+  const long long slot = w0 + lane;
   const bool have = slot < b.slots;
-  __syncthreads();
+  __syncthreads();   // satol, wacc, blive
   TS& s = *reinterpret_cast<TS*>(smem + threadIdx.x * TS_STRIDE);
   const typename SP::W w = SP::ws(b, have ? slot : 0);
   const double* lu = b.LU + (have ? slot : 0) * SP::LUREC;
@@ -300,11 +305,13 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_CTL_MINB)
     const unsigned bl = __ballot_sync(0xffffffffu, act == I::A_RET);
     if (lane == 0 && bl) atomicAdd(&blive, (unsigned long long)__popc(bl));
   }
-  __syncthreads();
+  __syncwarp();
   {
-    double* dst = b.ts + s0 * TS_STRIDE;
-    for (long long i = threadIdx.x; i < nrec; i += BDFB_SPLIT_BLOCK) dst[i] = smem[i];
+    double* dst = b.ts + w0 * TS_STRIDE;
+#pragma unroll 4
+    for (long long i = lane; i < nrec; i += 32) dst[i] = wsm[i];
   }
+  __syncthreads();
   if (threadIdx.x == 0 && blive) atomicAdd(&b.live[it & 1], blive);
   if (lane == 0 && wacc[warp].cells_done) {
     const Agg& a = wacc[warp];
@@ -357,37 +364,150 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_kernel(SplitBufs b
 }
 
 // ------------------------------------------------------------------ K_lu
-// one cell per group of G lanes (lane i = row i): M = I - gamma J and the
-// listing's LU_FACTOR in registers (coop_factor, bit-identical pivots and
-// factors), stored column-major in pivoted row order + 1/U_kk + perm.
+// One cell per group of 8 lanes, 4 cells per warp.  Lane l of the group holds
+// rows r = l + 8 s (s < R = ceil(n/8)) of M = I - gamma J in registers; rows
+// never move between lanes, each tracks its LAPACK position pos (as
+// coop_factor).  Per column k: the first index (in position order) of the
+// max |.| over positions >= k by a 3-step xor butterfly, the pivot row's
+// entries broadcast by shuffles, 1/pivot once, multipliers m = a_ik (1/pv)
+// and fma updates -- the listing's LU_FACTOR operation for operation
+// (reading R16), so pivots and factors are bit-identical to the oracle.
+// Versus one cell per warp (coop_factor) every shuffle of the pivot row
+// serves 4 cells and every lane has ~3 rows of FMAs: ~4x fewer instructions
+// per factorisation.  Returns 0, or k+1 for an exact zero pivot (uniform).
+constexpr int OCT = 8;
+// column k of oct_factor (k a compile-time constant so that a[][] stays in registers)
+template <int N, int K>
+__device__ __forceinline__ bool oct_column(unsigned gmask, int gl, double (&a)[(N + OCT - 1) / OCT][N],
+                                           int (&pos)[(N + OCT - 1) / OCT], double (&dinv)[(N + OCT - 1) / OCT]) {
+  constexpr int R = (N + OCT - 1) / OCT;
+  // local candidate: max |a[s][K]| over owned rows with pos >= K, ties -> smaller pos
+  double bv = -1.0;
+  int bp = 0x7fffffff, br = -1;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int r = gl + OCT * s;
+    if (r < N && pos[s] >= K) {
+      const double v = fabs(a[s][K]);
+      if (v > bv || (v == bv && pos[s] < bp)) {
+        bv = v;
+        bp = pos[s];
+        br = r;
+      }
+    }
+  }
+#pragma unroll
+  for (int off = OCT / 2; off >= 1; off >>= 1) {
+    const double ov = __shfl_xor_sync(gmask, bv, off, OCT);
+    const int op = __shfl_xor_sync(gmask, bp, off, OCT);
+    const int orr = __shfl_xor_sync(gmask, br, off, OCT);
+    if (ov > bv || (ov == bv && op < bp)) {
+      bv = ov;
+      bp = op;
+      br = orr;
+    }
+  }
+  if (!(bv > 0.0)) return false;               // exact zero pivot (uniform in the group)
+  const int pl = br % OCT, ps = br / OCT;      // owner lane and slot of the pivot row
+  double pk = 0.0;
+#pragma unroll
+  for (int s = 0; s < R; ++s)
+    if (s == ps) pk = a[s][K];
+  const double pv = __shfl_sync(gmask, pk, pl, OCT);
+  const double rinv = 1.0 / pv;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int r = gl + OCT * s;
+    if (r == br) {
+      pos[s] = K;
+      dinv[s] = rinv;
+    } else if (pos[s] == K) {
+      pos[s] = bp;
+    }
+  }
+  double m[R];
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    m[s] = a[s][K] * rinv;
+    if ((gl + OCT * s < N) && pos[s] > K) a[s][K] = m[s];
+  }
+#pragma unroll
+  for (int j = K + 1; j < N; ++j) {
+    double pj = 0.0;
+#pragma unroll
+    for (int s = 0; s < R; ++s)
+      if (s == ps) pj = a[s][j];
+    pj = __shfl_sync(gmask, pj, pl, OCT);
+#pragma unroll
+    for (int s = 0; s < R; ++s)
+      if ((gl + OCT * s < N) && pos[s] > K) a[s][j] = fma(-m[s], pj, a[s][j]);
+  }
+  return true;
+}
+
+template <int N, int... Ks>
+__device__ __forceinline__ int oct_columns(unsigned gmask, int gl, double (&a)[(N + OCT - 1) / OCT][N],
+                                           int (&pos)[(N + OCT - 1) / OCT], double (&dinv)[(N + OCT - 1) / OCT],
+                                           std::integer_sequence<int, Ks...>) {
+  int info = 0;
+  // left to right; stops at the first zero pivot (info = k + 1)
+  (void)((oct_column<N, Ks>(gmask, gl, a, pos, dinv) ? true : (info = Ks + 1, false)) && ...);
+  return info;
+}
+
+template <int N>
+__device__ __forceinline__ int oct_factor(unsigned gmask, int gl, double (&a)[(N + OCT - 1) / OCT][N],
+                                          int (&pos)[(N + OCT - 1) / OCT], double (&dinv)[(N + OCT - 1) / OCT]) {
+  constexpr int R = (N + OCT - 1) / OCT;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    pos[s] = gl + OCT * s;
+    dinv[s] = 0.0;
+  }
+  return oct_columns<N>(gmask, gl, a, pos, dinv, std::make_integer_sequence<int, N>{});
+}
+
+// K_lu: one setup-list entry per group of 8 lanes (grid-stride); M = I - gamma J
+// from the cell's column-major J, oct_factor, factors stored column-major in
+// pivoted row order + 1/U_kk + perm, as the Newton solve of K_ctl reads them.
 template <class Mech, class GM>
 __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b) {
   using SP = Split<Mech, GM>;
-  constexpr int N = Mech::N, G = GM::G;
-  Grp<G> g;
-  const long long cnt = b.cnt[0], groups = (long long)gridDim.x * (BDFB_SPLIT_BLOCK / G);
-  for (long long e = ((long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x) / G; e < cnt; e += groups) {
+  constexpr int N = Mech::N, R = (N + OCT - 1) / OCT;
+  const int lane = threadIdx.x & 31, gl = lane & (OCT - 1);
+  const unsigned gmask = 0xffu << (lane & ~(OCT - 1));
+  const long long cnt = b.cnt[0], groups = (long long)gridDim.x * (BDFB_SPLIT_BLOCK / OCT);
+  for (long long e = ((long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x) / OCT; e < cnt; e += groups) {
     const long long slot = b.slist[e];
     TS* t = SP::ts(b, slot);
     if (t->coop) continue;                       // the Jacobian failed: the resumed trip handles it (uniform)
     const double gm = t->gamma;
     const double* J = b.J + slot * SP::JREC;
     double* lu = b.LU + slot * SP::LUREC;
-    const int i = g.lane;
-    double row[N];
+    double a[R][N];
 #pragma unroll
-    for (int j = 0; j < N; ++j) row[j] = (i < N) ? (i == j ? 1.0 : 0.0) - gm * J[j * N + i] : 0.0;
-    int pos;
-    double dinv;
-    const int r = coop_factor<N, G>(g, row, pos, dinv);
-    if (!r && i < N) {
+    for (int s = 0; s < R; ++s) {
+      const int r = gl + OCT * s;
 #pragma unroll
-      for (int j = 0; j < N; ++j) lu[j * N + pos] = row[j];
-      lu[SP::LU_INVD + pos] = dinv;
-      reinterpret_cast<int*>(lu + SP::LU_PERM)[pos] = i;
+      for (int j = 0; j < N; ++j) a[s][j] = (r < N) ? (r == j ? 1.0 : 0.0) - gm * J[j * N + r] : 0.0;
     }
-    g.sync();
-    if (i == 0) t->coop = r;
+    int pos[R];
+    double dinv[R];
+    const int info = oct_factor<N>(gmask, gl, a, pos, dinv);
+    if (!info) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int r = gl + OCT * s;
+        if (r < N) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) lu[j * N + pos[s]] = a[s][j];
+          lu[SP::LU_INVD + pos[s]] = dinv[s];
+          reinterpret_cast<int*>(lu + SP::LU_PERM)[pos[s]] = r;
+        }
+      }
+    }
+    __syncwarp(gmask);
+    if (gl == 0) t->coop = info;
   }
 }
 

@@ -99,13 +99,14 @@ struct TWs {
 // piv (optional, diagnostics): LAPACK-style pivot indices.
 // FORM_M = false factors the given matrix itself (diagnostic entry point; Jp may
 // alias LUp: column j is read before any column >= j is written).
-// SS: compile-time element stride (0 = the runtime stride Srt).
-template <int N, bool FORM_M, long long SS>
+// SS: compile-time element stride (0 = the runtime stride Srt).  CM: J and LU
+// column-major ((i, j) at element j * N + i) instead of row-major.
+template <int N, bool FORM_M, long long SS, bool CM = false>
 __device__ __noinline__ int tpc_factor(const double* Jp, double* LUp, double* __restrict__ invdp,
                                        int* __restrict__ permp, long long Srt, double gamma, int* __restrict__ pivp) {
   const long long S = SS ? SS : Srt;
-  auto J = [&](int i, int j) -> const double& { return Jp[(long long)(i * N + j) * S]; };
-  auto LU = [&](int i, int j) -> double& { return LUp[(long long)(i * N + j) * S]; };
+  auto J = [&](int i, int j) -> const double& { return Jp[(long long)(CM ? j * N + i : i * N + j) * S]; };
+  auto LU = [&](int i, int j) -> double& { return LUp[(long long)(CM ? j * N + i : i * N + j) * S]; };
   int perm[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) perm[i] = i;

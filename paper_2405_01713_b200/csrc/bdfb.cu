@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/bdfb.h"
 #include "bdf_cell.cuh"
@@ -56,6 +57,9 @@ struct bdfb_batch {
   SplitBufs sb{};                  // SPLIT kernel slot pool (bdf_split.cuh)
   SplitGeom sgeom{};
   unsigned long long* h_live = nullptr;   // pinned: live-slot count read back per launch batch
+  std::vector<cudaEvent_t> sev;           // split: per-phase timing events of one launch batch
+  double phase_ms[8] = {};                // split: device ms per phase of the last integrate
+  int nphases = 0;
   std::string err;
 };
 
@@ -147,8 +151,15 @@ static int launch_split(bdfb_batch* b, const Opts& o, double* y, const double* f
   int launches = 0;
   int batch = 16;
   if (const char* env = getenv("BDFB_SPLIT_BATCH")) batch = atoi(env) > 0 ? atoi(env) : batch;
+  if ((int)b->sev.size() < (SPLIT_PHASES + 1) * batch) {
+    for (auto ev : b->sev) cudaEventDestroy(ev);
+    b->sev.assign((SPLIT_PHASES + 1) * batch, nullptr);
+    for (auto& ev : b->sev)
+      if (cudaEventCreate(&ev) != cudaSuccess) return fail(b, BDFB_ECUDA, "timing events");
+  }
   cudaError_t e = split_integrate(b->model, o, y, fext, aux, b->d_atol, b->sb, b->sgeom, b->d_counter, b->d_agg,
-                                  b->cs, b->h_live, batch, st, &launches);
+                                  b->cs, b->h_live, batch, st, &launches, b->sev.data(), b->phase_ms);
+  b->nphases = SPLIT_PHASES;
   cudaEventRecord(b->ev1, st);
   if (e != cudaSuccess) return cuda_fail(b, e, "split integrate");
   b->launches = launches;
@@ -283,6 +294,7 @@ void bdfb_destroy(bdfb_batch* b) {
   if (b->d_iws) cudaFree(b->d_iws);
   free_split(b);
   if (b->h_live) cudaFreeHost(b->h_live);
+  for (auto ev : b->sev) cudaEventDestroy(ev);
   {
     GlobalBuffers& g = b->gb;
     for (int j = 0; j <= QMAX; ++j) cudaFree(g.v.zn[j]);
@@ -607,6 +619,13 @@ extern "C" int64_t bdfb_get_stats(bdfb_batch* b, bdfb_stats* agg) {
 }
 
 extern "C" int32_t bdfb_last_launch_count(const bdfb_batch* b) { return b ? b->launches : 0; }
+
+extern "C" int32_t bdfb_phase_ms(const bdfb_batch* b, double* ms, int32_t max) {
+  if (!b) return 0;
+  const int n = b->nphases < max ? b->nphases : max;
+  for (int i = 0; ms && i < n; ++i) ms[i] = b->phase_ms[i];
+  return b->nphases;
+}
 
 extern "C" double bdfb_last_kernel_ms(bdfb_batch* b) {
   if (!b || !b->timed) return -1.0;

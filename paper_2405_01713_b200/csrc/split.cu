@@ -51,12 +51,15 @@ struct SplitK {
   static cudaError_t run(const Opts& o, double* y, const double* fext, const double* aux, const double* atol,
                          const SplitBufs& b, const SplitGeom& gm, unsigned long long* counter, Agg* agg,
                          const CellStatsPtrs& cs, unsigned long long* h_live, int batch, cudaStream_t st,
-                         int* launches) {
+                         int* launches, cudaEvent_t* events, double* phase_ms) {
     const long long S = b.slots;
     const unsigned blk = BDFB_SPLIT_BLOCK;
     const unsigned gs = (unsigned)((S + blk - 1) / blk);            // one thread per slot / list entry
-    // setup kernels: persistent grids, one group of G lanes per list entry (grid-stride)
-    unsigned glu = (unsigned)((S * GM::G + blk - 1) / blk);
+    // setup kernels: persistent grids (grid-stride over the lists): K_jac one group of G lanes per entry,
+    // K_lu one group of 8 lanes per entry
+    unsigned gjac = (unsigned)((S * GM::G + blk - 1) / blk);
+    if (gjac > (unsigned)gm.setup_grid) gjac = (unsigned)gm.setup_grid;
+    unsigned glu = (unsigned)((S * OCT + blk - 1) / blk);
     if (glu > (unsigned)gm.setup_grid) glu = (unsigned)gm.setup_grid;
     unsigned grhs = (unsigned)gm.rhs_grid;
     if (grhs > gs) grhs = gs;
@@ -64,20 +67,35 @@ struct SplitK {
     split_init_kernel<Mech, GM><<<gs, blk, 0, st>>>(b);
     int n = 1;
     cudaError_t e;
+    for (int i = 0; i < SPLIT_PHASES; ++i) phase_ms[i] = 0.0;
     for (int it = 0;;) {
-      for (int k = 0; k < batch; ++k, ++it) {
+      int k = 0;
+      for (; k < batch; ++k, ++it) {
+        cudaEvent_t* ev = events + k * (SPLIT_PHASES + 1);
+        if (events) cudaEventRecord(ev[0], st);
         split_ctl_kernel<Mech, GM><<<gs, blk, sm, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
-        split_jac_kernel<Mech, GM><<<glu, blk, jac_smem(), st>>>(b);
+        if (events) cudaEventRecord(ev[1], st);
+        split_jac_kernel<Mech, GM><<<gjac, blk, jac_smem(), st>>>(b);
+        if (events) cudaEventRecord(ev[2], st);
         split_lu_kernel<Mech, GM><<<glu, blk, 0, st>>>(b);
+        if (events) cudaEventRecord(ev[3], st);
         split_rhs_kernel<Mech, GM><<<grhs, blk, 0, st>>>(b, it);
+        if (events) cudaEventRecord(ev[4], st);
         n += 4;
       }
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
-      // live slots after the last pass A of the batch (iteration it - 1)
+      // live slots after the last K_ctl of the batch (iteration it - 1)
       if ((e = cudaMemcpyAsync(h_live, &b.live[(it - 1) & 1], sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                st)) != cudaSuccess)
         return e;
       if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+      for (int j = 0; events && j < k; ++j) {
+        cudaEvent_t* ev = events + j * (SPLIT_PHASES + 1);
+        for (int i = 0; i < SPLIT_PHASES; ++i) {
+          float ms = 0.f;
+          if (cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) == cudaSuccess) phase_ms[i] += ms;
+        }
+      }
       if (*h_live == 0) break;
     }
     *launches = n;
@@ -101,12 +119,14 @@ cudaError_t split_geometry(int mech, int device, SplitGeom* gm) {
 cudaError_t split_integrate(int mech, const Opts& o, double* y, const double* fext, const double* aux,
                             const double* atol, const SplitBufs& sb, const SplitGeom& gm, unsigned long long* counter,
                             Agg* agg, const CellStatsPtrs& cs, unsigned long long* h_live, int batch,
-                            cudaStream_t st, int* launches) {
+                            cudaStream_t st, int* launches, cudaEvent_t* events, double* phase_ms) {
   switch (mech) {
     case BDFB_MODEL_MECH_H2:
-      return KH2::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches);
+      return KH2::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches, events,
+                       phase_ms);
     case BDFB_MODEL_MECH_DRM19:
-      return KDRM::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches);
+      return KDRM::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches, events,
+                        phase_ms);
   }
   return cudaErrorInvalidValue;
 }

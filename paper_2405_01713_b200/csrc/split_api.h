@@ -22,9 +22,12 @@ cudaError_t split_geometry(int mech, int device, SplitGeom* gm);
 // Integrate all o.ncells cells through the slot pool sb (host loop over
 // K_ctl/K_rhs launch batches of `batch` iterations on st, one live-count read
 // back per batch; synchronous).  launches: kernels enqueued.
+// events: (SPLIT_PHASES + 1) * batch timing events (or NULL); phase_ms: device
+// time of each phase (K_ctl, K_jac, K_lu, K_rhs) summed over the integrate.
+constexpr int SPLIT_PHASES = 4;
 cudaError_t split_integrate(int mech, const Opts& o, double* y, const double* fext, const double* aux,
                             const double* atol, const SplitBufs& sb, const SplitGeom& gm, unsigned long long* counter,
                             Agg* agg, const CellStatsPtrs& cs, unsigned long long* h_live, int batch,
-                            cudaStream_t st, int* launches);
+                            cudaStream_t st, int* launches, cudaEvent_t* events, double* phase_ms);
 
 }  // namespace bdfb
