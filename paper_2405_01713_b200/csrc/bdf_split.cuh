@@ -57,6 +57,10 @@ namespace bdfb {
 #ifndef BDFB_SPLIT_CTL_MINB
 #define BDFB_SPLIT_CTL_MINB 3
 #endif
+// 1: K_ctl stages each warp's TS records through shared memory; 0: accesses them in HBM (L1-cached)
+#ifndef BDFB_SPLIT_TS_SMEM
+#define BDFB_SPLIT_TS_SMEM 1
+#endif
 
 struct SplitBufs {
   double* vec;                 // S/32 * D * 32
@@ -229,16 +233,22 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_CTL_MINB)
   // the warp's 32 TS records are contiguous in HBM: stage them through shared memory (coalesced), warp-local
   const long long w0 = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + (threadIdx.x & ~31u);
   const long long nrec = (b.slots - w0 < 32 ? (b.slots - w0 > 0 ? b.slots - w0 : 0) : 32) * TS_STRIDE;
+#if BDFB_SPLIT_TS_SMEM
   double* wsm = smem + (threadIdx.x & ~31u) * TS_STRIDE;
   {
     const double* src = b.ts + w0 * TS_STRIDE;
 #pragma unroll 4
     for (long long i = lane; i < nrec; i += 32) wsm[i] = src[i];
   }
+#endif
   const long long slot = w0 + lane;
   const bool have = slot < b.slots;
   __syncthreads();   // satol, wacc, blive
+#if BDFB_SPLIT_TS_SMEM
   TS& s = *reinterpret_cast<TS*>(smem + threadIdx.x * TS_STRIDE);
+#else
+  TS& s = *SP::ts(b, have ? slot : 0);
+#endif
   const typename SP::W w = SP::ws(b, have ? slot : 0);
   const double* lu = b.LU + (have ? slot : 0) * SP::LUREC;
   int act = I::A_DONE;
@@ -305,12 +315,14 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_CTL_MINB)
     const unsigned bl = __ballot_sync(0xffffffffu, act == I::A_RET);
     if (lane == 0 && bl) atomicAdd(&blive, (unsigned long long)__popc(bl));
   }
+#if BDFB_SPLIT_TS_SMEM
   __syncwarp();
   {
     double* dst = b.ts + w0 * TS_STRIDE;
 #pragma unroll 4
     for (long long i = lane; i < nrec; i += 32) dst[i] = wsm[i];
   }
+#endif
   __syncthreads();
   if (threadIdx.x == 0 && blive) atomicAdd(&b.live[it & 1], blive);
   if (lane == 0 && wacc[warp].cells_done) {

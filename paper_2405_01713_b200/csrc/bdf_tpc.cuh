@@ -278,7 +278,8 @@ struct TpcIntegrator {
   enum : int { A_NONE = 0, A_RET, A_DONE, A_HIN_FINISH, A_START, A_SETUP, A_SETUP_J, A_SETUP_LU, A_SOLVE, A_NFAIL,
                A_ERRTEST, A_STEP_TOP, A_STORE, A_LOAD, A_ATTEMPT };
   // ATTEMPT-pass flags (TS::flag): recompute ewt from zn[0] first (O1); rescale zn[1..q] by eta^j
-  enum : int { F_EWT = 1, F_RESCALE = 2 };
+  // F_RESTORE: RESTORE deferred into the ATTEMPT pass (failure retries that go straight to ATTEMPT)
+  enum : int { F_EWT = 1, F_RESCALE = 2, F_RESTORE = 4 };
 
   __device__ static double wrms_reg(const double (&v)[N], const W& w) {
     double acc = 0.0;
@@ -303,11 +304,17 @@ struct TpcIntegrator {
       for (int k = 1; k <= QMAX; ++k)
 #pragma unroll
         for (int j = QMAX; j >= 1; --j)
-          if (k <= q && j >= k && j <= q) z[j - 1] = z[j - 1] - z[j];
+          if (j >= k && j <= q) z[j - 1] = z[j - 1] - z[j];   // k <= j <= q (j >= k is compile-time)
 #pragma unroll
       for (int j = 0; j < QMAX; ++j)
         if (j < q) w.zn(j, i) = z[j];
     }
+  }
+
+  // RESTORE whose vector part runs in the next ATTEMPT pass (same operations, same order)
+  __device__ static void restore_deferred(TS& s) {
+    s.tn = s.saved_t;
+    s.flag |= F_RESTORE;
   }
 
   // cvSetBDF + cvSetTqBDF (scalar)
@@ -670,15 +677,16 @@ struct TpcIntegrator {
       return req_res(s, w);
     }
     s.ncfn++;
-    restore(s, w);
     s.ncf++;
     s.etamax = 1.0;
     if (fabs(s.h) <= o.hmin * (1.0 + UROUND) || s.ncf == MXNCF) {
+      restore(s, w);
       s.status = ST_CONV_FAILURE;
       return A_STORE;
     }
     s.eta = fmax(ETACF, o.hmin / fabs(s.h));
     s.nflag = NF_PREV_CONV;
+    restore_deferred(s);
     rescale(s);
     return A_ATTEMPT;
   }
@@ -715,7 +723,7 @@ struct TpcIntegrator {
       // arithmetic and stores (memory-level parallelism on the workspace)
       constexpr int CH = (N % 4 == 0) ? 4 : 2;
       static_assert(N % CH == 0, "chunking");
-#pragma unroll 1
+#pragma unroll 2
       for (int i0 = 0; i0 < N; i0 += CH) {
         double a[CH], e[CH], zm[CH], z[CH][QMAX + 1];
 #pragma unroll
@@ -760,8 +768,8 @@ struct TpcIntegrator {
     s.nef++;
     s.netf++;
     s.nflag = NF_PREV_ERR;
-    restore(s, w);
     if (fabs(s.h) <= o.hmin * (1.0 + UROUND) || s.nef == MXNEF) {
+      restore(s, w);
       s.status = ST_ERR_FAILURE;
       return A_STORE;
     }
@@ -770,9 +778,11 @@ struct TpcIntegrator {
       s.eta = 1.0 / (root_l(BIAS2 * dsm, s.L) + ADDON);
       s.eta = fmax(ETAMIN, fmax(s.eta, o.hmin / fabs(s.h)));
       if (s.nef >= SMALL_NEF) s.eta = fmin(s.eta, ETAMXF);
+      restore_deferred(s);
       rescale(s);
       return A_ATTEMPT;
     }
+    restore(s, w);   // the order-decrease and q = 1 paths read the restored history
     if (s.q > 1) {
       s.eta = fmax(ETAMIN, o.hmin / fabs(s.h));
       adjust_order(o, s, w, -1);
@@ -837,7 +847,7 @@ struct TpcIntegrator {
     const double rtol = o.rtol;
     constexpr int CH = (N % 4 == 0) ? 4 : 2;
     static_assert(N % CH == 0, "chunking");
-#pragma unroll 1
+#pragma unroll 2
     for (int i0 = 0; i0 < N; i0 += CH) {
       double zc[CH][QMAX + 1];
 #pragma unroll
@@ -848,6 +858,13 @@ struct TpcIntegrator {
       for (int c = 0; c < CH; ++c) {
         const int i = i0 + c;
         double* z = zc[c];
+        if (fl & F_RESTORE) {   // deferred RESTORE (q unchanged since the failed attempt)
+#pragma unroll
+          for (int k = 1; k <= QMAX; ++k)
+#pragma unroll
+            for (int j = QMAX; j >= 1; --j)
+              if (j >= k && j <= q) z[j - 1] = z[j - 1] - z[j];
+        }
         if (fl & F_EWT) w.ewt(i) = 1.0 / (rtol * fabs(z[0]) + atol[i]);
         if (fl & F_RESCALE) {
 #pragma unroll
@@ -858,7 +875,7 @@ struct TpcIntegrator {
         for (int k = 1; k <= QMAX; ++k)
 #pragma unroll
           for (int j = QMAX; j >= 1; --j)
-            if (k <= q && j >= k && j <= q) z[j - 1] = z[j - 1] + z[j];
+            if (j >= k && j <= q) z[j - 1] = z[j - 1] + z[j];
 #pragma unroll
         for (int j = 0; j <= QMAX; ++j)
           if (j <= q) w.zn(j, i) = z[j];

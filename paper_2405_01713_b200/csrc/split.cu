@@ -18,7 +18,9 @@ namespace {
 template <class Mech, class GM>
 struct SplitK {
   using SP = Split<Mech, GM>;
-  static constexpr size_t ctl_smem() { return sizeof(double) * (size_t)TS_STRIDE * BDFB_SPLIT_BLOCK; }
+  static constexpr size_t ctl_smem() {
+    return BDFB_SPLIT_TS_SMEM ? sizeof(double) * (size_t)TS_STRIDE * BDFB_SPLIT_BLOCK : 0;
+  }
   static constexpr size_t jac_smem() {
     return sizeof(double) * (size_t)(GM::SG + GM::JG + GM::N * (GM::N | 1)) * (BDFB_SPLIT_BLOCK / GM::G);
   }
