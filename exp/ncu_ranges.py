@@ -2,12 +2,7 @@
 import csv, sys, collections, bisect
 csv.field_size_limit(1 << 30)
 path = sys.argv[1]
-ranges = [(97, "tpc_factor"), (171, "tpc_solve"), (206, "coop_factor"), (275, "wrms"), (286, "restore"),
-          (305, "set_bdf"), (351, "increase_bdf"), (377, "decrease_bdf"), (394, "adjust/set_eta/rescale"),
-          (420, "prepare_next"), (458, "idx/req_res"), (477, "consume"), (560, "hin/start/setup_done/decide"),
-          (610, "solve"), (650, "nfail"), (671, "errtest"), (765, "step_top"), (789, "attempt"), (845, "store"),
-          (876, "load"), (927, "ts_of/ws_of"), (933, "trip"), (941, "SETUP_J stage"), (974, "SETUP_LU stage"),
-          (1010, "trip tail"), (1040, "kernel")]
+ranges = [(105, 'tpc_factor'), (179, 'tpc_solve'), (214, 'coop_factor'), (250, 'nth_bit'), (284, 'wrms_reg'), (295, 'restore'), (315, 'restore_deferred'), (321, 'set_bdf'), (367, 'increase_bdf'), (396, 'decrease_bdf'), (416, 'adjust_order'), (422, 'set_eta'), (434, 'rescale'), (442, 'prepare_next'), (486, 'req_res'), (500, 'consume'), (583, 'hin_finish'), (592, 'start'), (609, 'setup_done'), (618, 'setup_decide'), (633, 'solve'), (673, 'nfail'), (695, 'errtest'), (808, 'step_top'), (832, 'attempt'), (905, 'store'), (936, 'load'), (987, 'ts_of'), (991, 'ws_of'), (993, 'lu_list'), (999, 'trip')]
 starts = [r[0] for r in ranges]
 agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0])
 fname = None; hdr = None

@@ -150,6 +150,14 @@ def generate(name, out_dir):
         for k in range(K):
             A(f"  double eg{k};\n")
 
+    recip = sorted({idx[s] for x in rx if x["reversible"] for s in x["products"]})
+
+    def post_thermo(A):
+        for k in recip:
+            A(f"  const double ieg{k} = 1.0 / eg{k};\n")
+        if tb:
+            A(f"  const double ctot = {' + '.join(f'C{k}' for k in range(K))};\n")
+
     def eg_body(k, a):
         # -g/RT = -(h/RT - s/R) = a0 (lnT - 1) + a1 T/2 + a2 T^2/6 + a3 T^3/12 + a4 T^4/20 - a5/T + a6
         A(f"    eg{k} = fexp({d(a[0])} * (lnT - 1.0) + {d(a[1] / 2)} * T + {d(a[2] / 6)} * T2 + {d(a[3] / 12)} * T3 + "
@@ -167,7 +175,8 @@ def generate(name, out_dir):
         A(f"    const double Cf = {_prod([f'C{i}' for i in reac])}, Cr = {_prod([f'C{i}' for i in prod])};\n")
         fac = {0: "", 1: " * cRT", -1: " * icRT", 2: " * (cRT * cRT)", -2: " * (icRT * icRT)"}[dn]
         if x["reversible"]:
-            A(f"    const double invKc = ({_prod([f'eg{i}' for i in reac])}) / ({_prod([f'eg{i}' for i in prod])}){fac};\n")
+            # 1/K_c = prod_reac e^{-g/RT} * prod_prod e^{+g/RT} (reciprocals once per species, no division here)
+            A(f"    const double invKc = ({_prod([f'eg{i}' for i in reac])}) * ({_prod([f'ieg{i}' for i in prod])}){fac};\n")
         else:
             A("    const double invKc = 0.0;\n")
         A("    const double net = Cf - Cr * invKc;\n")
@@ -179,15 +188,14 @@ def generate(name, out_dir):
             else:
                 A("    const double dlnKc = 0.0;\n")
         if typ != "elementary":
+            # [M] = sum_k alpha_k C_k = ctot + sum_{alpha_k != 1} (alpha_k - 1) C_k
             eff = x["efficiencies"]
-            terms = []
+            m = "ctot"
             for s in sp:
                 e = eff.get(s, 1.0)
-                if e == 1.0:
-                    terms.append(f"C{idx[s]}")
-                elif e != 0.0:
-                    terms.append(f"{d(e)} * C{idx[s]}")
-            A(f"    const double M = {' + '.join(terms)};\n")
+                if e != 1.0:
+                    m = f"fma({d(e - 1.0)}, C{idx[s]}, {m})"
+            A(f"    const double M = {m};\n")
         if typ in ("elementary", "three_body"):
             Mf = "M * " if typ == "three_body" else ""
             A(f"    const double kf = {Mf}kinf;\n")
@@ -255,6 +263,7 @@ def generate(name, out_dir):
         A(f"  const double y{k} = yv[{k}];\n")
     thermo_common(A)
     _nasa(A, tab, tm, eg_body)
+    post_thermo(A)
     for k in range(K):
         A(f"  double w{k} = 0.0;\n")
     for r, x in enumerate(rx):
@@ -287,6 +296,7 @@ def generate(name, out_dir):
         A(f"    sc[{O_H + k}*S] = {d(a[0])} + T * ({d(a[1] / 2)} + T * ({d(a[2] / 3)} + T * ({d(a[3] / 4)} + T * {d(a[4] / 5)}))) + {d(a[5])} * invT;\n")
         A(f"    sc[{O_CV + k}*S] = ({d(a[0] - 1)} + T * ({d(a[1])} + T * ({d(a[2])} + T * ({d(a[3])} + T * {d(a[4])})))) * {d(RU / W[k])};\n")
     _nasa(A, tab, tm, jac_thermo)
+    post_thermo(A)
     for k in range(K):
         A(f"  double w{k} = 0.0;\n")
     for r, x in enumerate(rx):

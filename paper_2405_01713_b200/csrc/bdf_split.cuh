@@ -61,6 +61,9 @@ namespace bdfb {
 #ifndef BDFB_SPLIT_TS_SMEM
 #define BDFB_SPLIT_TS_SMEM 1
 #endif
+#ifndef BDFB_SPLIT_PREFETCH
+#define BDFB_SPLIT_PREFETCH 0
+#endif
 
 struct SplitBufs {
   double* vec;                 // S/32 * D * 32
@@ -243,6 +246,17 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_CTL_MINB)
 #endif
   const long long slot = w0 + lane;
   const bool have = slot < b.slots;
+#if BDFB_SPLIT_PREFETCH
+  // L2 prefetch of the warp's Nordsieck history, weights, corrections and RHS rows (contiguous in the
+  // warp-blocked SoA): the error test and the predictor then hit L2 instead of waiting on HBM
+  if (w0 < b.slots) {
+    using Wt = typename SP::W;
+    const char* base = reinterpret_cast<const char*>(b.vec + ((w0 >> 5) * SP::D) * 32);
+    constexpr int L0 = Wt::O_ZN * 2, L1 = (Wt::O_ACOR + N) * 2, F0 = Wt::O_FR * 2, F1 = (Wt::O_FR + N) * 2;
+    for (int l = L0 + lane; l < L1; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128 * l));
+    for (int l = F0 + lane; l < F1; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128 * l));
+  }
+#endif
   __syncthreads();   // satol, wacc, blive
 #if BDFB_SPLIT_TS_SMEM
   TS& s = *reinterpret_cast<TS*>(smem + threadIdx.x * TS_STRIDE);
