@@ -240,21 +240,34 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_CTL_MINB)
   double* wsm = smem + (threadIdx.x & ~31u) * TS_STRIDE;
   {
     const double* src = b.ts + w0 * TS_STRIDE;
-#pragma unroll 4
-    for (long long i = lane; i < nrec; i += 32) wsm[i] = src[i];
+    if (nrec == 32 * TS_STRIDE) {   // full warp: all 16-byte loads in flight at once (one HBM round trip)
+      constexpr int NV2 = 32 * TS_STRIDE / 2;   // TS_STRIDE odd: 32 records = an even number of doubles
+      const double2* s2 = reinterpret_cast<const double2*>(src);
+      double2* d2 = reinterpret_cast<double2*>(wsm);
+      double2 v[(NV2 + 31) / 32];
+#pragma unroll
+      for (int k = 0; k < (NV2 + 31) / 32; ++k)
+        if (lane + 32 * k < NV2) v[k] = s2[lane + 32 * k];
+#pragma unroll
+      for (int k = 0; k < (NV2 + 31) / 32; ++k)
+        if (lane + 32 * k < NV2) d2[lane + 32 * k] = v[k];
+    } else {
+      for (long long i = lane; i < nrec; i += 32) wsm[i] = src[i];
+    }
   }
 #endif
   const long long slot = w0 + lane;
   const bool have = slot < b.slots;
 #if BDFB_SPLIT_PREFETCH
-  // L2 prefetch of the warp's Nordsieck history, weights, corrections and RHS rows (contiguous in the
-  // warp-blocked SoA): the error test and the predictor then hit L2 instead of waiting on HBM
-  if (w0 < b.slots) {
-    using Wt = typename SP::W;
-    const char* base = reinterpret_cast<const char*>(b.vec + ((w0 >> 5) * SP::D) * 32);
-    constexpr int L0 = Wt::O_ZN * 2, L1 = (Wt::O_ACOR + N) * 2, F0 = Wt::O_FR * 2, F1 = (Wt::O_FR + N) * 2;
-    for (int l = L0 + lane; l < L1; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128 * l));
-    for (int l = F0 + lane; l < F1; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128 * l));
+  // bulk L2 prefetch (one TMA instruction each) of the warp's 32 LU records and of its state rows: the
+  // Newton solve's column loads and the Nordsieck passes then hit L2 instead of waiting on HBM
+  if (lane == 0 && w0 + 32 <= b.slots) {
+    const double* lu0 = b.LU + w0 * SP::LUREC;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lu0), "r"((unsigned)(32 * SP::LUREC * 8)) : "memory");
+#if BDFB_SPLIT_PREFETCH > 1
+    const double* v0 = b.vec + ((w0 >> 5) * SP::D) * 32;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v0), "r"((unsigned)(SP::D * 32 * 8)) : "memory");
+#endif
   }
 #endif
   __syncthreads();   // satol, wacc, blive
