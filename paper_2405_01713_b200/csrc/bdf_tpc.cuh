@@ -49,6 +49,7 @@ struct TS {
   int nstlp, nstlj, nef, ncf, nflag, convfail, setup, jcur, m;
   int count1, count2, phase, status, flag, coop;   // coop: result of a warp-cooperative stage
   int pend;                                        // split kernel: setup stage requested (A_SETUP_J/LU)
+  double oc_a1;                                    // deferred order increase: cvIncreaseBDF's A1
 };
 constexpr int TS_STRIDE = (int)((sizeof(TS) + 7) / 8) | 1;   // odd number of doubles
 
@@ -279,7 +280,9 @@ struct TpcIntegrator {
                A_ERRTEST, A_STEP_TOP, A_STORE, A_LOAD, A_ATTEMPT };
   // ATTEMPT-pass flags (TS::flag): recompute ewt from zn[0] first (O1); rescale zn[1..q] by eta^j
   // F_RESTORE: RESTORE deferred into the ATTEMPT pass (failure retries that go straight to ATTEMPT)
-  enum : int { F_EWT = 1, F_RESCALE = 2, F_RESTORE = 4 };
+  // F_INCR / F_DECR: the vector part of an order change (step_top) deferred into the ATTEMPT pass; its
+  // coefficients are parked in s.l[] (rewritten by set_bdf right after that pass) and s.oc_a1
+  enum : int { F_EWT = 1, F_RESCALE = 2, F_RESTORE = 4, F_INCR = 8, F_DECR = 16 };
 
   __device__ static double wrms_reg(const double (&v)[N], const W& w) {
     double acc = 0.0;
@@ -411,6 +414,40 @@ struct TpcIntegrator {
       for (int j = 2; j < QMAX; ++j)
         if (j < q) w.zn(j, i) = -l[j] * zq + w.zn(j, i);
     }
+  }
+
+  // step_top's order change with the vector work deferred into the ATTEMPT pass (same operations, same order
+  // per component; q is updated by the caller)
+  __device__ static __noinline__ void order_deferred(const Opts& o, TS& s, int dq) {
+    if (s.q == 2 && dq != 1) return;
+    double l[QMAX + 1];
+    for (int i = 0; i <= QMAX; ++i) l[i] = 0.0;
+    l[2] = 1.0;
+    if (dq == 1) {   // cvIncreaseBDF coefficients
+      double alpha1 = 1.0, prod = 1.0, xiold = 1.0, alpha0 = -1.0, hsum = s.hscale;
+      if (s.q > 1) {
+        for (int j = 1; j < s.q; ++j) {
+          hsum = hsum + s.tau[j + 1];
+          const double xi = hsum / s.hscale;
+          prod = prod * xi;
+          alpha0 = alpha0 - 1.0 / (j + 1);
+          alpha1 = alpha1 + 1.0 / xi;
+          for (int i = j + 2; i >= 2; --i) l[i] = l[i] * xiold + l[i - 1];
+          xiold = xi;
+        }
+      }
+      s.oc_a1 = (-alpha0 - alpha1) / prod;
+      s.flag |= F_INCR;
+    } else {         // cvDecreaseBDF coefficients
+      double hsum = 0.0;
+      for (int j = 1; j <= s.q - 2; ++j) {
+        hsum = hsum + s.tau[j];
+        const double xi = hsum / s.hscale;
+        for (int i = j + 2; i >= 2; --i) l[i] = l[i] * xi + l[i - 1];
+      }
+      s.flag |= F_DECR;
+    }
+    for (int i = 0; i <= QMAX; ++i) s.l[i] = l[i];
   }
 
   __device__ static void adjust_order(const Opts& o, TS& s, const W& w, int dq) {
@@ -818,7 +855,7 @@ struct TpcIntegrator {
     s.nflag = NF_FIRST;
     if (s.nst > 0 && s.hprime != s.h) {
       if (s.qprime != s.q) {
-        adjust_order(o, s, w, s.qprime - s.q);
+        order_deferred(o, s, s.qprime - s.q);
         s.q = s.qprime;
         s.L = s.q + 1;
         s.qwait = s.L;
@@ -847,13 +884,21 @@ struct TpcIntegrator {
     const double rtol = o.rtol;
     constexpr int CH = (N % 4 == 0) ? 4 : 2;
     static_assert(N % CH == 0, "chunking");
+    const int qld = q + ((fl & F_DECR) ? 1 : 0);   // a deferred decrease reads the old zn[q + 1]
+    double lc[QMAX + 1];
+#pragma unroll
+    for (int j = 0; j <= QMAX; ++j) lc[j] = s.l[j];
+    const double a1 = s.oc_a1;
+    const int qmx = o.qmax;
 #pragma unroll 2
     for (int i0 = 0; i0 < N; i0 += CH) {
-      double zc[CH][QMAX + 1];
+      double zc[CH][QMAX + 1], zm[CH];
 #pragma unroll
-      for (int c = 0; c < CH; ++c)
+      for (int c = 0; c < CH; ++c) {
 #pragma unroll
-        for (int j = 0; j <= QMAX; ++j) zc[c][j] = (j <= q) ? w.zn(j, i0 + c) : 0.0;
+        for (int j = 0; j <= QMAX; ++j) zc[c][j] = (j <= qld) ? w.zn(j, i0 + c) : 0.0;
+        zm[c] = (fl & F_INCR) ? w.zn(qmx, i0 + c) : 0.0;
+      }
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const int i = i0 + c;
@@ -864,6 +909,24 @@ struct TpcIntegrator {
 #pragma unroll
             for (int j = QMAX; j >= 1; --j)
               if (j >= k && j <= q) z[j - 1] = z[j - 1] - z[j];
+        }
+        if (fl & F_INCR) {   // cvIncreaseBDF, vector part (q = old q + 1): zn[q] = A1 zn[qmax], zn[j] += l_j zn[q]
+          const double zL = a1 * zm[c];
+#pragma unroll
+          for (int j = 2; j < QMAX; ++j)
+            if (j < q) z[j] = lc[j] * zL + z[j];
+#pragma unroll
+          for (int j = 2; j <= QMAX; ++j)
+            if (j == q) z[j] = zL;
+        }
+        if (fl & F_DECR) {   // cvDecreaseBDF, vector part (q = old q - 1): zn[j] -= l_j zn[old q]
+          double zq = 0.0;
+#pragma unroll
+          for (int j = 2; j <= QMAX; ++j)
+            if (j == q + 1) zq = z[j];
+#pragma unroll
+          for (int j = 2; j < QMAX; ++j)
+            if (j <= q) z[j] = -lc[j] * zq + z[j];
         }
         if (fl & F_EWT) w.ewt(i) = 1.0 / (rtol * fabs(z[0]) + atol[i]);
         if (fl & F_RESCALE) {
