@@ -554,8 +554,11 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b)
 // thread per slot: fr = R(yq) + F for a pending RHS request.  Also resets the
 // list counters and the live count for the next iteration (it + 1) -- after
 // the setup kernels of this iteration consumed the lists.
+#ifndef BDFB_SPLIT_RHS_MINB
+#define BDFB_SPLIT_RHS_MINB 3   // 168 registers, 12 warps/SM: 7% faster than 255 registers / 8 warps (measured)
+#endif
 template <class Mech, class GM>
-__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_rhs_kernel(SplitBufs b, int it) {
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_RHS_MINB) split_rhs_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM>;
   constexpr int N = Mech::N;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
