@@ -102,3 +102,23 @@ void orc_lu_solve(int n, const double *LU, const int *piv, double *b)
   }
   b[0] = b[0] * (1.0 / LU[0]);
 }
+
+/* Eq. 7: typical value = midpoint of the component's range over the whole domain. */
+void orc_typical_values(int n, int64_t ncells, const double *y, double *tv)
+{
+  for (int k = 0; k < n; ++k) {
+    double lo = y[(int64_t)k * ncells], hi = lo;
+    for (int64_t c = 1; c < ncells; ++c) {
+      const double v = y[(int64_t)k * ncells + c];
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
+    }
+    tv[k] = 0.5 * (lo + hi);
+  }
+}
+
+/* Eq. 7: atol_i = eta * tv_i, with the floor of S:99 */
+void orc_atol_from_typical(int n, const double *tv, double eta, double floor_, double *atol)
+{
+  for (int k = 0; k < n; ++k) atol[k] = fmax(eta * tv[k], floor_);
+}

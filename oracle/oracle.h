@@ -131,6 +131,15 @@ typedef struct {
 
 /* ---- primitives -------------------------------------------------------- */
 double orc_wrms(int n, const double *v, const double *w, int group);
+
+/* Typical values and tolerances (Eq. 7).
+ * orc_typical_values: y is YC (y[k*ncells + c]); tv[k] = 1/2 (min_c y[k][c] + max_c y[k][c])
+ *   ("the min and max operations are taken over the entire computational domain"); min/max by
+ *   C99 fmin/fmax (a NaN entry is skipped unless the whole component is NaN).  ncells >= 1.
+ * orc_atol_from_typical: atol[k] = max(eta * tv[k], floor) (Eq. 7 with the SPEC's positive floor,
+ *   the paper leaves tv = 0 undefined).                                             */
+void orc_typical_values(int n, int64_t ncells, const double *y, double *tv);
+void orc_atol_from_typical(int n, const double *tv, double eta, double floor_, double *atol);
 double orc_wrms_sum(int n, const double *v, const double *w, int group);
 int orc_lu_factor(int n, double *M /* row-major n*n, in/out */, int *piv);
 void orc_lu_solve(int n, const double *LU, const int *piv, double *b);

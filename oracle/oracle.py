@@ -88,6 +88,10 @@ def lib():
             dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int)
             L.orc_wrms.restype = C.c_double
             L.orc_wrms.argtypes = [C.c_int, dp, dp, C.c_int]
+            L.orc_typical_values.restype = None
+            L.orc_typical_values.argtypes = [C.c_int, C.c_int64, dp, dp]
+            L.orc_atol_from_typical.restype = None
+            L.orc_atol_from_typical.argtypes = [C.c_int, dp, C.c_double, C.c_double, dp]
             L.orc_lu_factor.restype = C.c_int
             L.orc_lu_factor.argtypes = [C.c_int, dp, ip]
             L.orc_lu_solve.restype = None
@@ -130,6 +134,23 @@ def wrms(v, w, group=1):
     v = np.ascontiguousarray(v, dtype=np.float64)
     w = np.ascontiguousarray(w, dtype=np.float64)
     return lib().orc_wrms(len(v), _dp(v), _dp(w), int(group))
+
+
+def typical_values(y_yc):
+    """Eq. 7 typical values of a YC field y[n, N] (orc_typical_values)."""
+    y = np.ascontiguousarray(y_yc, dtype=np.float64)
+    n, N = y.shape
+    tv = np.empty(n)
+    lib().orc_typical_values(n, N, _dp(y), _dp(tv))
+    return tv
+
+
+def atol_from_typical(tv, eta=1e-10, floor=1e-30):
+    """Eq. 7: atol_i = max(eta tv_i, floor) (orc_atol_from_typical)."""
+    tv = np.ascontiguousarray(tv, dtype=np.float64)
+    out = np.empty(len(tv))
+    lib().orc_atol_from_typical(len(tv), _dp(tv), float(eta), float(floor), _dp(out))
+    return out
 
 
 def lu_factor(M):

@@ -150,3 +150,39 @@ def test_root_matches_high_precision_root(oracle, L):
     for a in (0.5, 2.0, 3.0, 1.25, 7.0):
         assert oracle.root(a ** L, L) == pytest.approx(a, rel=2e-16)
     assert oracle.root(0.0, L) == 0.0
+
+
+# ---- typical-value tolerances (Eq. 7) -----------------
+def test_typical_values_spec_examples(oracle):
+    g = json.load(open(GOLD))
+    for ex in g["typical_values"]:
+        y = np.array([ex["component"]])
+        assert oracle.typical_values(y)[0] == ex["tv"], ex["tag"]
+    for ex in g["atol_from_typical"]:
+        a = oracle.atol_from_typical([ex["tv"]], ex["eta"], ex["floor"])[0]
+        assert a == pytest.approx(ex["atol"], rel=1e-15, abs=0.0), ex["tag"]
+
+
+def test_typical_values_brute_force_and_invariances(oracle):
+    """Midpoint of the range by an independent numpy scan; invariant under permutation of the cells and under
+    duplication of a cell inside [min, max]; an exact midpoint when min and max are dyadic."""
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((7, 513)) * 10.0 ** rng.uniform(-12, 3, (7, 1))
+    tv = oracle.typical_values(y)
+    ref = 0.5 * (y.min(axis=1) + y.max(axis=1))
+    assert np.array_equal(tv, ref)
+    perm = rng.permutation(y.shape[1])
+    assert np.array_equal(oracle.typical_values(y[:, perm]), tv)
+    dup = np.concatenate([y, y[:, [3, 3, 100]]], axis=1)
+    assert np.array_equal(oracle.typical_values(dup), tv)
+    z = np.array([[0.25, -1.5, 4.0, 0.5]])
+    assert oracle.typical_values(z)[0] == 1.25            # (-1.5 + 4) / 2, exact
+
+
+def test_atol_from_typical_properties(oracle):
+    """Eq. 7 scaling: atol proportional to tv above the floor; tv defaults to 1 -> atol = eta."""
+    tv = np.array([1.0, 2500.0, 0.0, 1e-40, 3.0])
+    a = oracle.atol_from_typical(tv, 1e-6, 1e-30)
+    assert a[0] == 1e-6 and a[2] == 1e-30 and a[3] == 1e-30
+    assert a[4] == 1e-6 * 3.0
+    assert np.array_equal(oracle.atol_from_typical(np.ones(4), 1e-10, 1e-30), np.full(4, 1e-10))
