@@ -219,6 +219,27 @@ int32_t bdfb_phase_ms(const bdfb_batch *b, double *ms, int32_t max);
  * GLOBAL_NORM mode: the whole host-driven kernel sequence.                 */
 double bdfb_last_kernel_ms(bdfb_batch *b);
 
+/* ---- typical-value tolerances (Eq. 7; §8(f) row f2) ----------
+ * "typical values" y~_i = (min(y_i) + max(y_i)) / 2 "taken over the entire
+ * computational domain", atol_i = eta y~_i (eta = 1e-10 is Pele's default,
+ * P:334), floored at a positive `floor` (the paper leaves y~_i = 0
+ * undefined).
+ *
+ * bdfb_minmax: ymin[k], ymax[k] (device, n doubles each) = min and max of
+ * component k over the handle's n_cells cells of y (device, `layout`),
+ * with C99 fmin/fmax semantics (NaN entries are skipped).  Exact: the
+ * result is independent of the reduction order except for the sign of a
+ * zero.  On several ranks, reduce ymin/ymax with MIN/MAX across ranks
+ * (e.g. torch.distributed.all_reduce) before the next call.
+ * bdfb_set_atol_typical: tv_k = (ymin_k + ymax_k) / 2 (written to tv,
+ * device, if not NULL) and the handle's atol_k = max(eta tv_k, floor); takes
+ * effect for the next integrate on the same stream.  Both enqueue on
+ * `stream` and return BDFB_EINVAL / BDFB_ECUDA on bad arguments / launch
+ * failure.                                                                  */
+int bdfb_minmax(bdfb_batch *b, const double *y, int32_t layout, double *ymin, double *ymax, void *stream);
+int bdfb_set_atol_typical(bdfb_batch *b, const double *ymin, const double *ymax, double eta, double floor_,
+                          double *tv, void *stream);
+
 /* Free everything owned by the handle (NULL is a no-op). */
 void bdfb_destroy(bdfb_batch *b);
 

@@ -29,6 +29,11 @@ STATUS = {0: "OK", 1: "TOO_MUCH_WORK", 2: "ERR_FAILURE", 3: "CONV_FAILURE", 4: "
 CELL_STAT_FIELDS = ["status", "nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn", "q_last", "h_last", "t_reached"]
 
 
+def torch_empty_like(t):
+    import torch
+    return torch.empty_like(t)
+
+
 def library_path():
     return L.LIB_PATH
 
@@ -163,6 +168,28 @@ class Batch:
 
     def last_kernel_ms(self):
         return float(self._L.bdfb_last_kernel_ms(self.h))
+
+    def minmax(self, y, layout="YC", stream=None):
+        """Per-component min and max of y over the handle's cells (bdfb_minmax); device tensors [n]."""
+        import torch
+        lo = torch.empty(self.n, dtype=torch.float64, device=y.device)
+        hi = torch.empty_like(lo)
+        lay = L.LAYOUT_YC if layout == "YC" else L.LAYOUT_CY
+        _check(self._L.bdfb_minmax(self.h, _ptr(y), lay, _ptr(lo), _ptr(hi), _stream(stream)), self.h)
+        return lo, hi
+
+    def set_typical_atol(self, y, eta=1e-10, floor=1e-30, layout="YC", group=None, stream=None):
+        """Eq. 7 typical-value absolute tolerances from the current field y: the min/max of
+        every component over all cells -- of all ranks of `group` when given (torch.distributed MIN/MAX
+        reductions of n doubles) -- then atol_i = max(eta (min_i + max_i)/2, floor) on the device.
+        Returns the typical values (device tensor [n])."""
+        from . import parallel
+        lo, hi = self.minmax(y, layout, stream)
+        lo, hi = parallel.allreduce_minmax(lo, hi, group)
+        tv = torch_empty_like(lo)
+        _check(self._L.bdfb_set_atol_typical(self.h, _ptr(lo), _ptr(hi), float(eta), float(floor), _ptr(tv),
+                                             _stream(stream)), self.h)
+        return tv
 
     def phase_ms(self):
         """SPLIT kernel: device ms per phase of the last integrate (bdfb_phase_ms), else {}."""

@@ -40,6 +40,7 @@ struct bdfb_batch {
   int model = -1;
   unsigned char params[256] = {};
   double* d_atol = nullptr;
+  double* d_tvpart = nullptr;      // typical values: per-block partial min/max (2 * TV_BLOCKS * n)
   unsigned long long* d_counter = nullptr;
   Agg* d_agg = nullptr;
   double *d_y = nullptr, *d_f = nullptr, *d_aux = nullptr;   // host-API staging
@@ -245,6 +246,7 @@ int bdfb_create(bdfb_batch** out, int64_t n_cells, int32_t n, double rtol, const
   b->rtol = rtol;
   b->opt = o;
   if ((e = cudaMalloc(&b->d_atol, sizeof(double) * n)) != cudaSuccess ||
+      (e = cudaMalloc(&b->d_tvpart, sizeof(double) * 2 * 592 * n)) != cudaSuccess ||
       (e = cudaMalloc(&b->d_counter, sizeof(unsigned long long))) != cudaSuccess ||
       (e = cudaMalloc(&b->d_agg, sizeof(Agg))) != cudaSuccess) {
     bdfb_destroy(b);
@@ -285,6 +287,7 @@ void bdfb_destroy(bdfb_batch* b) {
   if (!b) return;
   cudaSetDevice(b->device);
   if (b->d_atol) cudaFree(b->d_atol);
+  if (b->d_tvpart) cudaFree(b->d_tvpart);
   if (b->d_counter) cudaFree(b->d_counter);
   if (b->d_agg) cudaFree(b->d_agg);
   if (b->d_y) cudaFree(b->d_y);
@@ -920,4 +923,105 @@ extern "C" int bdfb_probe_fp64(int32_t device, double ms, double* tflops, int32_
   *tflops = best;
   if (sms) *sms = nsm;
   return BDFB_OK;
+}
+
+// ------------------------------------------------ typical-value tolerances (Eq. 7)
+// Per-component min and max over all cells: pass 1, block (b, k) folds a
+// grid-stride share of component k with fmin/fmax (starting from NaN, which
+// fmin/fmax skip: the oracle's semantics); pass 2, one block per component
+// folds the TV_BLOCKS partials.  min/max are exact, so the result does not
+// depend on the folding order (except the sign of a zero).
+namespace {
+constexpr int TV_BLOCKS = 592, TV_THREADS = 256;
+
+__device__ __forceinline__ void tv_fold_block(double& lo, double& hi) {
+  __shared__ double slo[TV_THREADS / 32], shi[TV_THREADS / 32];
+  for (int off = 16; off >= 1; off >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    slo[w] = lo;
+    shi[w] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    lo = threadIdx.x < TV_THREADS / 32 ? slo[threadIdx.x] : __longlong_as_double(0x7ff8000000000000ll);
+    hi = threadIdx.x < TV_THREADS / 32 ? shi[threadIdx.x] : __longlong_as_double(0x7ff8000000000000ll);
+    for (int off = 16; off >= 1; off >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(TV_THREADS) tv_partial_kernel(const double* y, long long N, int n, int layout,
+                                                                double* part) {
+  const int k = blockIdx.y;
+  double lo = __longlong_as_double(0x7ff8000000000000ll), hi = lo;
+  for (long long c = blockIdx.x * (long long)TV_THREADS + threadIdx.x; c < N; c += (long long)gridDim.x * TV_THREADS) {
+    const double v = layout == BDFB_LAYOUT_YC ? y[(long long)k * N + c] : y[c * n + k];
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  tv_fold_block(lo, hi);
+  if (threadIdx.x == 0) {
+    part[(long long)k * gridDim.x + blockIdx.x] = lo;
+    part[(long long)(n + k) * gridDim.x + blockIdx.x] = hi;
+  }
+}
+
+__global__ void __launch_bounds__(TV_THREADS) tv_final_kernel(const double* part, int nb, int n, double* ymin,
+                                                              double* ymax) {
+  const int k = blockIdx.x;
+  double lo = __longlong_as_double(0x7ff8000000000000ll), hi = lo;
+  for (int i = threadIdx.x; i < nb; i += TV_THREADS) {
+    lo = fmin(lo, part[(long long)k * nb + i]);
+    hi = fmax(hi, part[(long long)(n + k) * nb + i]);
+  }
+  tv_fold_block(lo, hi);
+  if (threadIdx.x == 0) {
+    ymin[k] = lo;
+    ymax[k] = hi;
+  }
+}
+
+// Eq. 7: tv_i = (min_i + max_i) / 2, atol_i = max(eta tv_i, floor)
+__global__ void tv_atol_kernel(const double* ymin, const double* ymax, int n, double eta, double floor_, double* atol,
+                               double* tv) {
+  const int k = threadIdx.x;
+  if (k >= n) return;
+  const double t = 0.5 * (ymin[k] + ymax[k]);
+  if (tv) tv[k] = t;
+  atol[k] = fmax(eta * t, floor_);
+}
+}  // namespace
+
+extern "C" int bdfb_minmax(bdfb_batch* b, const double* y, int32_t layout, double* ymin, double* ymax,
+                           void* stream) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (!y || !ymin || !ymax) return fail(b, BDFB_EINVAL, "y, ymin and ymax are required");
+  if (layout != BDFB_LAYOUT_YC && layout != BDFB_LAYOUT_CY) return fail(b, BDFB_EINVAL, "bad layout");
+  cudaSetDevice(b->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  long long nb = (b->ncells + TV_THREADS - 1) / TV_THREADS;
+  if (nb > TV_BLOCKS) nb = TV_BLOCKS;
+  tv_partial_kernel<<<dim3((unsigned)nb, (unsigned)b->n), TV_THREADS, 0, st>>>(y, b->ncells, b->n, layout,
+                                                                               b->d_tvpart);
+  tv_final_kernel<<<(unsigned)b->n, TV_THREADS, 0, st>>>(b->d_tvpart, (int)nb, b->n, ymin, ymax);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BDFB_OK : cuda_fail(b, e, "minmax launch");
+}
+
+extern "C" int bdfb_set_atol_typical(bdfb_batch* b, const double* ymin, const double* ymax, double eta,
+                                     double floor_, double* tv, void* stream) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (!ymin || !ymax) return fail(b, BDFB_EINVAL, "ymin and ymax are required");
+  if (!(eta > 0.0) || !(floor_ > 0.0) || !isfinite(eta) || !isfinite(floor_))
+    return fail(b, BDFB_EINVAL, "eta and floor must be finite and > 0");
+  cudaSetDevice(b->device);
+  tv_atol_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(ymin, ymax, b->n, eta, floor_, b->d_atol, tv);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BDFB_OK : cuda_fail(b, e, "atol launch");
 }

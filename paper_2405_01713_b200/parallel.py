@@ -56,3 +56,17 @@ def reduce_stats(stats: dict, dist=None, device=None) -> dict:
 def job_throughput(cells_per_rank: int, world: int, max_seconds_per_step: float) -> float:
     """Whole-job cells/s: all ranks' cells over the slowest rank's time."""
     return cells_per_rank * world / max_seconds_per_step
+
+
+def allreduce_minmax(lo, hi, group=None):
+    """Typical values over the whole domain (Eq. 7, "taken over the entire computational domain"):
+    element-wise MIN of the per-rank minima and MAX of the maxima over the ranks of `group`
+    (torch.distributed; NCCL for device tensors, gloo on CPU).  n doubles each: statistics-sized plumbing,
+    not a data-path collective.  No-op without an initialised process group."""
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return lo, hi
+    lo, hi = lo.clone(), hi.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    return lo, hi

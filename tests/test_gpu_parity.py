@@ -316,3 +316,50 @@ def test_full_size_c2_sampled(oracle):
     assert np.array_equal(sg["status"][idx], so["status"])
     ok = so["status"] == 0
     end_state_check(yg[:, idx][:, ok], yo[:, ok], 1e-6, 1e-10)
+
+
+# ------------------------------------------------------------------ typical-value tolerances (Eq. 7, row f2)
+@pytest.mark.parametrize("layout", ["YC", "CY"])
+def test_typical_values_bitwise(oracle, layout):
+    """bdfb_minmax + bdfb_set_atol_typical vs orc_typical_values / orc_atol_from_typical on identical inputs:
+    bit-identical (min/max are exact; the midpoint and eta*tv are single roundings on both sides), including
+    a ragged cell count and NaN entries (skipped by fmin/fmax on both sides)."""
+    y, rho, F, prog = flame_field("drm19_class", 16, dt=1e-5)
+    y = y[:, :4093].copy()                                  # ragged
+    y[3, 17] = np.nan
+    y[0, 4000] = -2.5                                       # a negative entry (S:146: signed min/max)
+    n, N = y.shape
+    b = P.Batch(N, n, 1e-6, 1e-10)
+    b.set_model("drm19")
+    yd = cu(y if layout == "YC" else y.T)
+    tv = b.set_typical_atol(yd, eta=1e-10, floor=1e-30, layout=layout).cpu().numpy()
+    tvo = oracle.typical_values(y)
+    assert np.array_equal(tv, tvo)
+    lo, hi = b.minmax(yd, layout=layout)
+    assert np.array_equal(lo.cpu().numpy(), np.fmin.reduce(y, axis=1))
+    assert np.array_equal(hi.cpu().numpy(), np.fmax.reduce(y, axis=1))
+
+
+@pytest.mark.parametrize("name", ["h2", "drm19"])
+def test_integrate_with_typical_atol(oracle, name):
+    """Integration with the Eq. 7 tolerances (Pele's eta = 1e-10) set on the device (SPLIT kernel) vs the
+    oracle with the oracle's own Eq. 7 atol vector: the end states agree within 10 (rtol |y| + atol_i).
+    (At looser eta, e.g. 1e-8, single ignition cells can drift past that bar: the two valid trajectories differ
+    by the global error -- measured 1 cell of 4096 at ratio 1.12 for H2, exp/tv_check.py.)"""
+    mech, n = MECH[name]
+    y0, rho, F, prog = flame_field(mech, 16, dt=1e-5)
+    N = y0.shape[1]
+    eta = 1e-10
+    b = P.Batch(N, n, 1e-6, 1e-10)
+    b.set_model(name)
+    yd = cu(y0)
+    b.set_typical_atol(yd, eta=eta)
+    b.integrate(0.0, 1e-5, yd, f_ext=cu(F), aux=cu(rho))
+    st = b.stats()
+    atol = oracle.atol_from_typical(oracle.typical_values(y0), eta, 1e-30)
+    yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, 1e-5, 1e-6, atol, rho=rho, fext_yc=F,
+                                    group=b.wrms_group, threads=8)
+    assert st["n_failed"] == 0 and np.all(so["status"] == 0)
+    yg = yd.cpu().numpy()
+    tol = 10.0 * (1e-6 * np.abs(yo) + atol[:, None])
+    assert np.all(np.abs(yg - yo) <= tol)

@@ -79,3 +79,37 @@ def test_shard_arithmetic():
     with pytest.raises(ValueError):
         PL.shard(4, 4, 10)
     assert PL.job_throughput(100, 8, 2.0) == 400.0
+
+
+def _tv_worker(rank, world, port, cells_per_rank, out):
+    sys.path.insert(0, REPO)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2405_01713_b200 import parallel as PL
+    from synth import flame_field
+    a, b = PL.shard(rank, world, cells_per_rank)
+    y, _, _, _ = flame_field("h2_lidryer", 8, cells=np.arange(a, b))
+    # each rank's own min/max (what bdfb_minmax returns on its GPU), then the MIN/MAX over ranks
+    lo, hi = torch.tensor(y.min(axis=1)), torch.tensor(y.max(axis=1))
+    glo, ghi = PL.allreduce_minmax(lo, hi)
+    out[rank] = (glo.numpy(), ghi.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_typical_values_gloo():
+    """Eq. 7 typical values over the whole domain: the per-rank min/max combined with MIN/MAX over 2 ranks
+    give the oracle's typical values of the unsharded field, bit for bit, on every rank."""
+    world, cpr = 2, 256
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_tv_worker, args=(world, _free_port(), cpr, out), nprocs=world, join=True)
+    sys.path.insert(0, REPO)
+    from oracle import oracle as O
+    from synth import flame_field
+    y, _, _, _ = flame_field("h2_lidryer", 8, cells=np.arange(world * cpr))
+    tv = O.typical_values(y)
+    for r in range(world):
+        lo, hi = out[r]
+        assert np.array_equal(0.5 * (lo + hi), tv)
