@@ -2,6 +2,7 @@
 // geometry, the five kernels of a trip and the host loop that enqueues them;
 // a translation unit of libbdfb.so, used by bdfb.cu through split_api.h.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "../../include/bdfb.h"
 #include "bdf_split.cuh"
@@ -28,8 +29,8 @@ struct SplitK {
   static cudaError_t geometry(int device, SplitGeom* gm) {
     cudaError_t e;
     const int sm = (int)ctl_smem();
-    if ((e = cudaFuncSetAttribute(split_ctl_kernel<Mech, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) !=
-        cudaSuccess)
+    if ((e = cudaFuncSetAttribute(split_ctl_kernel<Mech, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  sm > 110 * 1024 ? sm : 110 * 1024)) != cudaSuccess)
       return e;
     int nsm = 0, pr = 0;
     if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) return e;
@@ -65,7 +66,11 @@ struct SplitK {
     if (glu > (unsigned)gm.setup_grid) glu = (unsigned)gm.setup_grid;
     unsigned grhs = (unsigned)gm.rhs_grid;
     if (grhs > gs) grhs = gs;
-    const size_t sm = ctl_smem();
+    size_t sm = ctl_smem();
+    if (const char* pad = getenv("BDFB_SPLIT_CTL_SMEM")) {  // experiments: cap the resident K_ctl blocks
+      const size_t want = (size_t)strtoul(pad, nullptr, 10);
+      if (want > sm) sm = want;
+    }
     split_init_kernel<Mech, GM><<<gs, blk, 0, st>>>(b);
     int n = 1;
     cudaError_t e;
