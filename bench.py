@@ -107,7 +107,7 @@ def hbm_bytes_global(cfg, st):
     return per_cell * st["n_cells"]
 
 
-TS_RECORD_BYTES = 472          # struct TS record of the SPLIT slot pool (TS_STRIDE = 59 doubles, csrc/bdf_tpc.cuh)
+TS_RECORD_BYTES = 408          # struct TS record of the SPLIT slot pool (TS_STRIDE = 51 doubles, csrc/bdf_tpc.cuh)
 QBAR = 3                       # mean BDF order assumed by the byte model (zn[0..q] rows moved per pass)
 
 

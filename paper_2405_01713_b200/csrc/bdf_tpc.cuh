@@ -43,13 +43,15 @@ struct TS {
   double tau[QMAX + 2], l[QMAX + 1], tq[6];
   double rl1, gamma, gammap, gamrat, crate, acnrm, saved_tq5, dprev, tol;
   double hg, hs, hub, hnew, aux, rs_eta;
-  long long cell;
-  int q, qprime, L, qwait;
-  int nst, nfe, nje, nsetups, nni, netf, ncfn;
-  int nstlp, nstlj, nef, ncf, nflag, convfail, setup, jcur, m;
-  int count1, count2, phase, status, flag, coop;   // coop: result of a warp-cooperative stage
-  int pend;                                        // split kernel: setup stage requested (A_SETUP_J/LU)
   double oc_a1;                                    // deferred order increase: cvIncreaseBDF's A1
+  long long cell;
+  int nst, nfe, nje, nsetups, nni, netf, ncfn, nstlp, nstlj;
+  // small counters and codes as bytes: the record is staged through shared memory by the SPLIT control
+  // kernel, whose occupancy its size bounds (51 doubles: 4 blocks of 128 threads per SM)
+  signed char q, qprime, L, qwait, nef, ncf, nflag, convfail, setup, jcur, m, count1, count2, phase, status;
+  signed char flag;                                // ATTEMPT-pass flags (F_*)
+  signed char coop;                                // result of a cooperative/separate stage (J, LU status)
+  signed char pend;                                // split kernel: setup stage requested (A_SETUP_J/LU)
 };
 constexpr int TS_STRIDE = (int)((sizeof(TS) + 7) / 8) | 1;   // odd number of doubles
 
