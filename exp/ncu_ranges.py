@@ -2,7 +2,7 @@
 import csv, sys, collections, bisect
 csv.field_size_limit(1 << 30)
 path = sys.argv[1]
-ranges = [(105, 'tpc_factor'), (179, 'tpc_solve'), (214, 'coop_factor'), (250, 'nth_bit'), (284, 'wrms_reg'), (295, 'restore'), (315, 'restore_deferred'), (321, 'set_bdf'), (367, 'increase_bdf'), (396, 'decrease_bdf'), (416, 'adjust_order'), (422, 'set_eta'), (434, 'rescale'), (442, 'prepare_next'), (486, 'req_res'), (500, 'consume'), (583, 'hin_finish'), (592, 'start'), (609, 'setup_done'), (618, 'setup_decide'), (633, 'solve'), (673, 'nfail'), (695, 'errtest'), (808, 'step_top'), (832, 'attempt'), (905, 'store'), (936, 'load'), (987, 'ts_of'), (991, 'ws_of'), (993, 'lu_list'), (999, 'trip')]
+ranges = [(108, 'tpc_factor'), (182, 'tpc_solve'), (217, 'coop_factor'), (253, 'nth_bit'), (289, 'wrms_reg'), (300, 'restore'), (320, 'restore_deferred'), (326, 'set_bdf'), (372, 'increase_bdf'), (401, 'decrease_bdf'), (423, 'order_deferred'), (455, 'adjust_order'), (461, 'set_eta'), (473, 'rescale'), (481, 'prepare_next'), (525, 'req_res'), (539, 'consume'), (622, 'hin_finish'), (631, 'start'), (648, 'setup_done'), (657, 'setup_decide'), (672, 'solve'), (712, 'nfail'), (734, 'errtest'), (847, 'step_top'), (871, 'attempt'), (970, 'store'), (1001, 'load'), (1052, 'ts_of'), (1056, 'ws_of'), (1058, 'lu_list'), (1064, 'trip')]
 starts = [r[0] for r in ranges]
 agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0])
 fname = None; hdr = None

@@ -52,6 +52,7 @@ struct TS {
   signed char flag;                                // ATTEMPT-pass flags (F_*)
   signed char coop;                                // result of a cooperative/separate stage (J, LU status)
   signed char pend;                                // split kernel: setup stage requested (A_SETUP_J/LU)
+  signed char qc;                                  // order of the step whose completion is deferred (F_COMPLETE)
 };
 constexpr int TS_STRIDE = (int)((sizeof(TS) + 7) / 8) | 1;   // odd number of doubles
 
@@ -283,8 +284,10 @@ struct TpcIntegrator {
   // ATTEMPT-pass flags (TS::flag): recompute ewt from zn[0] first (O1); rescale zn[1..q] by eta^j
   // F_RESTORE: RESTORE deferred into the ATTEMPT pass (failure retries that go straight to ATTEMPT)
   // F_INCR / F_DECR: the vector part of an order change (step_top) deferred into the ATTEMPT pass; its
-  // coefficients are parked in s.l[] (rewritten by set_bdf right after that pass) and s.oc_a1
-  enum : int { F_EWT = 1, F_RESCALE = 2, F_RESTORE = 4, F_INCR = 8, F_DECR = 16 };
+  // coefficients are parked in s.tq[] (rewritten by set_bdf right after that pass) and s.oc_a1
+  // F_COMPLETE: cvCompleteStep (zn[j] += l_j acor, j <= qc) deferred into the ATTEMPT pass; F_FQ: zn[qmax] = acor
+  // (saved for a possible order increase) deferred likewise.  Until then zn in memory is the predicted history.
+  enum : int { F_EWT = 1, F_RESCALE = 2, F_RESTORE = 4, F_INCR = 8, F_DECR = 16, F_COMPLETE = 32, F_FQ = 64 };
 
   __device__ static double wrms_reg(const double (&v)[N], const W& w) {
     double acc = 0.0;
@@ -449,7 +452,7 @@ struct TpcIntegrator {
       }
       s.flag |= F_DECR;
     }
-    for (int i = 0; i <= QMAX; ++i) s.l[i] = l[i];
+    for (int i = 0; i <= QMAX; ++i) s.tq[i] = l[i];   // tq is free until set_bdf (prepare_next has read it)
   }
 
   __device__ static void adjust_order(const Opts& o, TS& s, const W& w, int dq) {
@@ -511,8 +514,7 @@ struct TpcIntegrator {
     } else {
       s.eta = etaqp1;
       s.qprime = s.q + 1;
-#pragma unroll
-      for (int i = 0; i < N; ++i) w.zn(o.qmax, i) = w.acor(i);
+      s.flag |= F_FQ;   // zn[qmax] = acor, in the ATTEMPT pass
     }
     set_eta(o, s);
   }
@@ -754,44 +756,23 @@ struct TpcIntegrator {
         cquot = (s.tq[5] / s.saved_tq5) * pw;
       }
       const int q = s.q, qmax = o.qmax;
-      double lj[QMAX + 1];
-#pragma unroll
-      for (int j = 0; j <= QMAX; ++j) lj[j] = s.l[j];
+      // cvCompleteStep is deferred into the next ATTEMPT pass (or STORE); here only the norms PREPARE_NEXT
+      // needs, every q+1 steps: ||l_q acor + zn[q]|| and ||acor - cquot zn[qmax]|| (zn[qmax] before the
+      // pass; fq and np1 are exclusive: qwait = 1 vs 0)
+      s.flag |= F_COMPLETE | (fq ? F_FQ : 0);
+      s.qc = q;
       double sdn = 0.0, sup = 0.0;
-      // chunks of CH components: all loads of a chunk are issued before its
-      // arithmetic and stores (memory-level parallelism on the workspace)
-      constexpr int CH = (N % 4 == 0) ? 4 : 2;
-      static_assert(N % CH == 0, "chunking");
+      if (nm1 || np1) {
+        const double lq = s.l[q];
 #pragma unroll 2
-      for (int i0 = 0; i0 < N; i0 += CH) {
-        double a[CH], e[CH], zm[CH], z[CH][QMAX + 1];
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          a[c] = w.acor(i0 + c);
-          e[c] = w.ewt(i0 + c);
-          zm[c] = np1 ? w.zn(qmax, i0 + c) : 0.0;
-#pragma unroll
-          for (int j = 0; j <= QMAX; ++j) z[c][j] = (j <= q) ? w.zn(j, i0 + c) : 0.0;
-        }
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          const int i = i0 + c;
-          double zq = 0.0;
-#pragma unroll
-          for (int j = 0; j <= QMAX; ++j)
-            if (j <= q) {
-              const double zz = lj[j] * a[c] + z[c][j];
-              w.zn(j, i) = zz;
-              if (j == q) zq = zz;
-            }
-          if (fq) w.zn(qmax, i) = a[c];
+        for (int i = 0; i < N; ++i) {
+          const double a = w.acor(i), e = w.ewt(i);
           if (nm1) {
-            const double p = zq * e[c];
+            const double p = (lq * a + w.zn(q, i)) * e;
             sdn = sdn + p * p;
           }
           if (np1) {
-            // zn[qmax] as read before this pass (fq and np1 are exclusive: qwait = 1 vs 0)
-            const double p = (-cquot * zm[c] + a[c]) * e[c];
+            const double p = (-cquot * w.zn(qmax, i) + a) * e;
             sup = sup + p * p;
           }
         }
@@ -886,25 +867,40 @@ struct TpcIntegrator {
     const double rtol = o.rtol;
     constexpr int CH = (N % 4 == 0) ? 4 : 2;
     static_assert(N % CH == 0, "chunking");
-    const int qld = q + ((fl & F_DECR) ? 1 : 0);   // a deferred decrease reads the old zn[q + 1]
-    double lc[QMAX + 1];
+    // rows to read: the new order, the old zn[q + 1] of a deferred decrease, the rows of a deferred completion
+    const int qc = (fl & F_COMPLETE) ? s.qc : 0;
+    const int qdec = q + ((fl & F_DECR) ? 1 : 0);
+    const int qld = qdec > qc ? qdec : qc;
+    const int qwb = q > qc ? q : qc;                  // rows written back (a completed row above a decrease)
+    double lk[QMAX + 1], lc[QMAX + 1];
 #pragma unroll
-    for (int j = 0; j <= QMAX; ++j) lc[j] = s.l[j];
+    for (int j = 0; j <= QMAX; ++j) {
+      lk[j] = s.l[j];    // step coefficients of the deferred completion
+      lc[j] = s.tq[j];   // order-change coefficients (order_deferred)
+    }
     const double a1 = s.oc_a1;
     const int qmx = o.qmax;
+    const bool wqmax = (fl & F_FQ) && qmx > qwb;      // zn[qmax] = acor lands in its own row
 #pragma unroll 2
     for (int i0 = 0; i0 < N; i0 += CH) {
-      double zc[CH][QMAX + 1], zm[CH];
+      double zc[CH][QMAX + 1], zm[CH], ac[CH];
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
 #pragma unroll
         for (int j = 0; j <= QMAX; ++j) zc[c][j] = (j <= qld) ? w.zn(j, i0 + c) : 0.0;
-        zm[c] = (fl & F_INCR) ? w.zn(qmx, i0 + c) : 0.0;
+        ac[c] = (fl & F_COMPLETE) ? w.acor(i0 + c) : 0.0;
+        zm[c] = ((fl & F_INCR) && !(fl & F_FQ)) ? w.zn(qmx, i0 + c) : 0.0;
       }
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const int i = i0 + c;
         double* z = zc[c];
+        if (fl & F_COMPLETE) {   // deferred cvCompleteStep: zn[j] = l_j acor + zn[j], j <= qc
+#pragma unroll
+          for (int j = 0; j <= QMAX; ++j)
+            if (j <= qc) z[j] = lk[j] * ac[c] + z[j];
+          if (fl & F_FQ) zm[c] = ac[c];               // zn[qmax] = acor (read by an order increase)
+        }
         if (fl & F_RESTORE) {   // deferred RESTORE (q unchanged since the failed attempt)
 #pragma unroll
           for (int k = 1; k <= QMAX; ++k)
@@ -943,7 +939,8 @@ struct TpcIntegrator {
             if (j >= k && j <= q) z[j - 1] = z[j - 1] + z[j];
 #pragma unroll
         for (int j = 0; j <= QMAX; ++j)
-          if (j <= q) w.zn(j, i) = z[j];
+          if (j <= qwb) w.zn(j, i) = z[j];
+        if (wqmax) w.zn(qmx, i) = ac[c];
         w.yq(i) = z[0];
         w.acor(i) = 0.0;
       }
@@ -970,8 +967,10 @@ struct TpcIntegrator {
   __device__ static void store(const Opts& o, TS& s, const W& w, double* y, Agg& acc, const CellStatsPtrs& cs) {
     const long long c = s.cell;
     if (s.status != ST_NONFINITE) {
+      const bool pend = (s.flag & F_COMPLETE) != 0;   // the last step's completion is still deferred
+      const double l0 = s.l[0];
 #pragma unroll
-      for (int i = 0; i < N; ++i) y[idx(o, c, i)] = w.zn(0, i);
+      for (int i = 0; i < N; ++i) y[idx(o, c, i)] = pend ? l0 * w.acor(i) + w.zn(0, i) : w.zn(0, i);
     }
     if (cs.status) cs.status[c] = s.status;
     if (cs.nst) cs.nst[c] = s.nst;
