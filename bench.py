@@ -115,14 +115,15 @@ def ctl_bytes(cfg, st):
     """Bytes the SPLIT control kernel K_ctl must move per integrate: every visit of a slot
     (one per consumed RHS value and one per resumed setup) reads and writes the cell's TS record; a
     consumed Newton residual reads fr, zn[1], acor and writes del (32n + 4); a Newton solve streams the
-    LU record (8n^2 + 12n) and moves del, acor (r/w), ewt, zn[0], yq (48n); a completed step and an
-    attempt each read and write zn[0..q] (16 (q+1) n) plus acor/ewt (16n) or ewt/yq/acor (24n)."""
+    LU record (8n^2 + 12n) and moves del, acor (r/w), ewt, zn[0], yq (48n); an attempt reads and writes
+    zn[0..q] once (the deferred step completion, order change, rescale and predictor fused: 16 (q+1) n)
+    plus acor (r), ewt, yq, acor (w) (32n); every q+1 steps the PREPARE_NEXT norms read acor, ewt,
+    zn[q], zn[qmax] (32n)."""
     n = CONFIGS[cfg][2]
     att = st["nst"] + st["netf"] + st["ncfn"]
-    trips = st["nfe"] + st["nsetups"]
-    zq = 16 * (QBAR + 1) * n
-    return (trips * 2 * TS_RECORD_BYTES + st["nfe"] * (32 * n + 4) + st["nni"] * (8 * n * n + 12 * n + 48 * n) +
-            st["nst"] * (zq + 16 * n) + att * (zq + 24 * n))
+    visits = st["nfe"] + st["nsetups"]
+    return (visits * 2 * TS_RECORD_BYTES + st["nfe"] * (32 * n + 4) + st["nni"] * (8 * n * n + 12 * n + 48 * n) +
+            att * (16 * (QBAR + 1) * n + 32 * n) + st["nst"] * 32 * n // (QBAR + 1))
 
 
 def rhs_flops(cfg, st):
@@ -403,7 +404,7 @@ def main():
                 f"{100 * pm['ctl'] / tot:.0f}% of the step)", "peak_source": src,
                 "kernel_ms": pm["ctl"], "bytes_per_integrate": cb,
                 "bytes_model": "DESIGN.md §6: per visit 2 TS records, per RHS value 32n+4, per Newton solve "
-                               "8n^2+60n, per step/attempt zn[0..q] r/w (q=3) + vectors",
+                               "8n^2+60n, per attempt zn[0..q] r/w (q=3) + 32n, per step 32n/(q+1)",
                 "fp64_whole_step": {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                                     "flops_per_launch": statistics.mean(flops)}}
     if glob_mode:

@@ -54,6 +54,10 @@ namespace bdfb {
 #ifndef BDFB_SPLIT_BLOCK
 #define BDFB_SPLIT_BLOCK 128
 #endif
+// K_ctl block size (a block retires when its slowest warp finishes: small blocks waste less)
+#ifndef BDFB_SPLIT_CTL_BLOCK
+#define BDFB_SPLIT_CTL_BLOCK 128
+#endif
 #ifndef BDFB_SPLIT_CTL_MINB
 #define BDFB_SPLIT_CTL_MINB 3
 #endif
@@ -219,7 +223,7 @@ __global__ void split_init_kernel(SplitBufs b) {
 // (its RHS slot idles once) instead of a latency-bound second pass.
 constexpr int PH_SETUP = 6;
 template <class Mech, class GM>
-__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_CTL_MINB)
+__global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     split_ctl_kernel(Opts o, SplitBufs b, int it, double* y, const double* fext, const double* aux,
                      const double* atol, unsigned long long* counter, Agg* agg, CellStatsPtrs cs) {
   using SP = Split<Mech, GM>;
@@ -227,14 +231,14 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_CTL_MINB)
   constexpr int N = Mech::N;
   extern __shared__ double smem[];           // TS records of the block's threads (TS_STRIDE each)
   __shared__ double satol[N];
-  __shared__ Agg wacc[BDFB_SPLIT_BLOCK / 32];
+  __shared__ Agg wacc[BDFB_SPLIT_CTL_BLOCK / 32];
   __shared__ unsigned long long blive;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < N) satol[threadIdx.x] = atol[threadIdx.x];
   if (lane == 0) wacc[warp] = Agg{};
   if (threadIdx.x == 0) blive = 0;
   // the warp's 32 TS records are contiguous in HBM: stage them through shared memory (coalesced), warp-local
-  const long long w0 = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + (threadIdx.x & ~31u);
+  const long long w0 = (long long)blockIdx.x * BDFB_SPLIT_CTL_BLOCK + (threadIdx.x & ~31u);
   const long long nrec = (b.slots - w0 < 32 ? (b.slots - w0 > 0 ? b.slots - w0 : 0) : 32) * TS_STRIDE;
 #if BDFB_SPLIT_TS_SMEM
   double* wsm = smem + (threadIdx.x & ~31u) * TS_STRIDE;

@@ -20,7 +20,7 @@ template <class Mech, class GM>
 struct SplitK {
   using SP = Split<Mech, GM>;
   static constexpr size_t ctl_smem() {
-    return BDFB_SPLIT_TS_SMEM ? sizeof(double) * (size_t)TS_STRIDE * BDFB_SPLIT_BLOCK : 0;
+    return BDFB_SPLIT_TS_SMEM ? sizeof(double) * (size_t)TS_STRIDE * BDFB_SPLIT_CTL_BLOCK : 0;
   }
   static constexpr size_t jac_smem() {
     return sizeof(double) * (size_t)(GM::SG + GM::JG + GM::N * (GM::N | 1)) * (BDFB_SPLIT_BLOCK / GM::G);
@@ -58,6 +58,7 @@ struct SplitK {
     const long long S = b.slots;
     const unsigned blk = BDFB_SPLIT_BLOCK;
     const unsigned gs = (unsigned)((S + blk - 1) / blk);            // one thread per slot / list entry
+    const unsigned gctl = (unsigned)((S + BDFB_SPLIT_CTL_BLOCK - 1) / BDFB_SPLIT_CTL_BLOCK);
     // setup kernels: persistent grids (grid-stride over the lists): K_jac one group of G lanes per entry,
     // K_lu one group of 8 lanes per entry
     unsigned gjac = (unsigned)((S * GM::G + blk - 1) / blk);
@@ -80,7 +81,7 @@ struct SplitK {
       for (; k < batch; ++k, ++it) {
         cudaEvent_t* ev = events + k * (SPLIT_PHASES + 1);
         if (events) cudaEventRecord(ev[0], st);
-        split_ctl_kernel<Mech, GM><<<gs, blk, sm, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
+        split_ctl_kernel<Mech, GM><<<gctl, BDFB_SPLIT_CTL_BLOCK, sm, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
         if (events) cudaEventRecord(ev[1], st);
         split_jac_kernel<Mech, GM><<<gjac, blk, jac_smem(), st>>>(b);
         if (events) cudaEventRecord(ev[2], st);
