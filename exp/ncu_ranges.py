@@ -2,7 +2,7 @@
 import csv, sys, collections, bisect
 csv.field_size_limit(1 << 30)
 path = sys.argv[1]
-ranges = [(108, 'tpc_factor'), (182, 'tpc_solve'), (217, 'coop_factor'), (253, 'nth_bit'), (289, 'wrms_reg'), (300, 'restore'), (320, 'restore_deferred'), (326, 'set_bdf'), (372, 'increase_bdf'), (401, 'decrease_bdf'), (423, 'order_deferred'), (455, 'adjust_order'), (461, 'set_eta'), (473, 'rescale'), (481, 'prepare_next'), (525, 'req_res'), (539, 'consume'), (622, 'hin_finish'), (631, 'start'), (648, 'setup_done'), (657, 'setup_decide'), (672, 'solve'), (712, 'nfail'), (734, 'errtest'), (847, 'step_top'), (871, 'attempt'), (970, 'store'), (1001, 'load'), (1052, 'ts_of'), (1056, 'ws_of'), (1058, 'lu_list'), (1064, 'trip')]
+ranges = [(109, 'tpc_factor'), (183, 'tpc_solve'), (218, 'coop_factor'), (254, 'nth_bit'), (292, 'wrms_reg'), (303, 'restore'), (323, 'restore_deferred'), (329, 'set_bdf'), (375, 'increase_bdf'), (404, 'decrease_bdf'), (426, 'order_deferred'), (458, 'adjust_order'), (464, 'set_eta'), (476, 'rescale'), (484, 'prepare_next'), (527, 'req_res'), (541, 'consume'), (624, 'hin_finish'), (633, 'start'), (650, 'setup_done'), (659, 'setup_decide'), (674, 'solve'), (714, 'nfail'), (736, 'errtest'), (828, 'step_top'), (852, 'attempt'), (967, 'store'), (1000, 'load'), (1051, 'ts_of'), (1055, 'ws_of'), (1057, 'lu_list'), (1063, 'trip')]
 starts = [r[0] for r in ranges]
 agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0])
 fname = None; hdr = None

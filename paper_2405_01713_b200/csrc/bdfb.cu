@@ -108,13 +108,13 @@ static void free_split(bdfb_batch* b) {
   b->sb = SplitBufs{};
 }
 
-// SPLIT kernel: slot pool of S = min(n_cells rounded up to 32, BDFB_SPLIT_SLOTS env or 262144) slots
+// SPLIT kernel: slot pool of S = min(n_cells rounded up to 32, BDFB_SPLIT_SLOTS env or 393216) slots
 static int prepare_split(bdfb_batch* b) {
   cudaError_t e = cudaSetDevice(b->device);
   SplitGeom gm{};
   if (e == cudaSuccess) e = split_geometry(b->model, b->device, &gm);
   if (e != cudaSuccess) return cuda_fail(b, e, "split geometry");
-  long long cap = 262144;
+  long long cap = 393216;   // measured on C4: 196608 2.51M, 262144 2.65M, 393216 2.78M, 524288 2.76M, 786432 2.79M cells/s
   if (const char* env = getenv("BDFB_SPLIT_SLOTS")) cap = atoll(env) > 0 ? atoll(env) : cap;
   long long S = b->ncells < cap ? b->ncells : cap;
   S = (S + 31) / 32 * 32;
