@@ -68,6 +68,13 @@ namespace bdfb {
 #ifndef BDFB_SPLIT_PREFETCH
 #define BDFB_SPLIT_PREFETCH 0
 #endif
+// 1: cell start/end (store, load, cvHin) in a separate compacted kernel K_init (full warps of starting cells)
+#ifndef BDFB_SPLIT_INIT_KERNEL
+#define BDFB_SPLIT_INIT_KERNEL 0   // measured slower on C4 (K_ctl+K_init 3.80 s vs K_ctl 3.34 s): kept as an option
+#endif
+
+// split-local phases: waiting for the setup kernels; finished, to be stored by K_init
+constexpr int PH_SETUP = 6, PH_STORE = 7;
 
 struct SplitBufs {
   double* vec;                 // S/32 * D * 32
@@ -77,7 +84,8 @@ struct SplitBufs {
   int* rv;                     // S: RHS status of the last request
   int* slist;                  // setup list (slots)
   int* jlist;                  // Jacobian list (slots)
-  unsigned* cnt;               // [0] setup count, [1] Jacobian count
+  int* ilist;                  // cell start/end list (slots for K_init)
+  unsigned* cnt;               // [0] setup count, [1] Jacobian count, [2] K_init count
   unsigned long long* live;    // [2]: live slots after the K_ctl of iteration it (it & 1)
   long long slots;             // S (multiple of 32)
 };
@@ -182,6 +190,9 @@ struct Split {
 
   // the trip after the setup decision (both passes): SOLVE .. ATTEMPT, in the
   // stage order of TpcIntegrator::trip.  Returns A_RET (RHS requested) or A_DONE.
+  // DEFER_STORE: a finished cell is not stored here; it is marked PH_STORE and returns A_STORE (K_init
+  // stores it and loads the next cell with full warps)
+  template <bool DEFER_STORE = false>
   __device__ static int finish(const Opts& o, TS& s, const W& w, int act, const double* lu, double* y,
                                const double* fext, const double* aux, const double* atol,
                                unsigned long long* counter, Agg& acc, const CellStatsPtrs& cs) {
@@ -189,6 +200,10 @@ struct Split {
     if (act == I::A_NFAIL) act = I::nfail(o, s, w);
     if (act == I::A_ERRTEST) act = I::errtest(o, s, w);
     if (act == I::A_STEP_TOP) act = I::step_top(o, s, w);
+    if (DEFER_STORE && act == I::A_STORE) {
+      s.phase = PH_STORE;
+      return act;
+    }
     if (act == I::A_STORE) {
       I::store(o, s, w, y, acc, cs);
       act = I::A_LOAD;
@@ -205,7 +220,7 @@ __global__ void split_init_kernel(SplitBufs b) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s == 0) {
     b.live[0] = b.live[1] = 0;
-    b.cnt[0] = b.cnt[1] = 0;
+    b.cnt[0] = b.cnt[1] = b.cnt[2] = 0;
   }
   if (s >= b.slots) return;
   TS* t = Split<Mech, GM>::ts(b, s);
@@ -221,7 +236,6 @@ __global__ void split_init_kernel(SplitBufs b) {
 // trip stopped at a matrix setup (phase PH_SETUP) resumes after it: the setup
 // kernels ran in between, so the trip costs the cell one extra iteration
 // (its RHS slot idles once) instead of a latency-bound second pass.
-constexpr int PH_SETUP = 6;
 template <class Mech, class GM>
 __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     split_ctl_kernel(Opts o, SplitBufs b, int it, double* y, const double* fext, const double* aux,
@@ -283,13 +297,19 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
   const typename SP::W w = SP::ws(b, have ? slot : 0);
   const double* lu = b.LU + (have ? slot : 0) * SP::LUREC;
   int act = I::A_DONE;
-  bool setup = false, jreq = false;
+  bool setup = false, jreq = false, init = false;
   if (have) {
     bool run = true;
     if (s.phase == PH_DONE) {   // empty slot: live only while the work counter has cells left
       const unsigned long long next = *reinterpret_cast<volatile unsigned long long*>(counter);
       run = next < (unsigned long long)o.ncells;
     }
+#if BDFB_SPLIT_INIT_KERNEL
+    if (run && (s.phase == PH_DONE || s.phase == PH_INIT || s.phase == PH_HIN)) {   // K_init's work
+      init = true;
+      run = false;
+    }
+#endif
     if (run && s.phase == PH_SETUP) {   // resume after the setup kernels (TpcIntegrator::trip order)
       act = s.pend;
       if (act == I::A_SETUP_J) {
@@ -328,7 +348,9 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
       }
     }
     // one call site: lanes that resumed and lanes that consumed an RHS value run the rest together
-    if (run) act = SP::finish(o, s, w, act, lu, y, fext, aux, satol, counter, wacc[warp], cs);
+    if (run) act = SP::template finish<BDFB_SPLIT_INIT_KERNEL != 0>(o, s, w, act, lu, y, fext, aux, satol, counter,
+                                                                      wacc[warp], cs);
+    if (act == I::A_STORE) init = true;   // deferred store (K_init)
   }
   // setup / Jacobian lists: one atomic per warp and list
   {
@@ -343,6 +365,11 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     const unsigned below = (1u << lane) - 1u;
     if (setup) b.slist[os + __popc(bs & below)] = (int)slot;
     if (jreq) b.jlist[oj + __popc(bj & below)] = (int)slot;
+    const unsigned bi = __ballot_sync(0xffffffffu, init);
+    unsigned oi = 0;
+    if (lane == 0 && bi) oi = atomicAdd(&b.cnt[2], __popc(bi));
+    oi = __shfl_sync(0xffffffffu, oi, 0);
+    if (init) b.ilist[oi + __popc(bi & below)] = (int)slot;
     const unsigned bl = __ballot_sync(0xffffffffu, act == I::A_RET);
     if (lane == 0 && bl) atomicAdd(&blive, (unsigned long long)__popc(bl));
   }
@@ -356,6 +383,79 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
 #endif
   __syncthreads();
   if (threadIdx.x == 0 && blive) atomicAdd(&b.live[it & 1], blive);
+  if (lane == 0 && wacc[warp].cells_done) {
+    const Agg& a = wacc[warp];
+    atomicAdd(&agg->n_failed, a.n_failed);
+    atomicAdd(&agg->nst, a.nst);
+    atomicAdd(&agg->nfe, a.nfe);
+    atomicAdd(&agg->nje, a.nje);
+    atomicAdd(&agg->nsetups, a.nsetups);
+    atomicAdd(&agg->nni, a.nni);
+    atomicAdd(&agg->netf, a.netf);
+    atomicAdd(&agg->ncfn, a.ncfn);
+    atomicMax(&agg->nst_max, a.nst_max);
+    atomicMax(&agg->nfe_max, a.nfe_max);
+    atomicAdd(&agg->cells_done, a.cells_done);
+  }
+}
+
+// ------------------------------------------------------------------ K_init
+// thread per init-list entry (compacted: full warps of cells that start or end): store a finished cell and
+// load the next one from the work counter (f(t0, y0) requested), or consume a cvHin RHS value (h0 by cvHin;
+// once h0 is set, start, step_top and the first ATTEMPT: the first Newton residual requested).  The state
+// is accessed in place (TS record L1-cached; the SoA rows of scattered slots: rare work).
+template <class Mech, class GM>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_init_cells_kernel(Opts o, SplitBufs b, int it, double* y,
+                                                                           const double* fext, const double* aux,
+                                                                           const double* atol,
+                                                                           unsigned long long* counter, Agg* agg,
+                                                                           CellStatsPtrs cs) {
+  using SP = Split<Mech, GM>;
+  using I = typename SP::I;
+  constexpr int N = Mech::N;
+  __shared__ double satol[N];
+  __shared__ Agg wacc[BDFB_SPLIT_BLOCK / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < N) satol[threadIdx.x] = atol[threadIdx.x];
+  if (lane == 0) wacc[warp] = Agg{};
+  __syncthreads();
+  const long long cnt = b.cnt[2];
+  unsigned long long nlive = 0;
+  for (long long e = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; e - lane < cnt;
+       e += (long long)gridDim.x * BDFB_SPLIT_BLOCK) {
+    int act = I::A_DONE;
+    if (e < cnt) {
+      const long long slot = b.ilist[e];
+      TS& s = *SP::ts(b, slot);
+      const typename SP::W w = SP::ws(b, slot);
+      const int ph = s.phase;
+      if (ph == PH_STORE) {
+        I::store(o, s, w, y, wacc[warp], cs);
+        act = I::A_LOAD;
+      } else if (ph == PH_DONE) {
+        act = I::A_LOAD;
+      } else {                                   // PH_INIT / PH_HIN: a cvHin RHS value is ready
+        double fr[N];
+        const int rv = b.rv[slot];
+        s.nfe++;
+#pragma unroll
+        for (int i = 0; i < N; ++i) fr[i] = w.fr(i);
+        act = I::consume(o, s, w, rv, fr);
+        if (act == I::A_HIN_FINISH) act = I::hin_finish(o, s);
+        if (act == I::A_START) act = I::start(o, s, w);
+        if (act == I::A_STEP_TOP) act = I::step_top(o, s, w);
+        if (act == I::A_STORE) {
+          I::store(o, s, w, y, wacc[warp], cs);
+          act = I::A_LOAD;
+        }
+      }
+      if (act == I::A_LOAD) act = I::load(o, s, w, y, fext, aux, satol, counter, wacc[warp], cs);
+      if (act == I::A_ATTEMPT) act = I::attempt(o, s, w, satol);
+    }
+    const unsigned bl = __ballot_sync(0xffffffffu, act == I::A_RET);
+    if (lane == 0) nlive += __popc(bl);
+  }
+  if (lane == 0 && nlive) atomicAdd(&b.live[it & 1], nlive);
   if (lane == 0 && wacc[warp].cells_done) {
     const Agg& a = wacc[warp];
     atomicAdd(&agg->n_failed, a.n_failed);
@@ -566,7 +666,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_RHS_MINB) split_r
   using SP = Split<Mech, GM>;
   constexpr int N = Mech::N;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    b.cnt[0] = b.cnt[1] = 0;
+    b.cnt[0] = b.cnt[1] = b.cnt[2] = 0;
     b.live[(it + 1) & 1] = 0;
   }
   const long long stride = (long long)gridDim.x * BDFB_SPLIT_BLOCK;

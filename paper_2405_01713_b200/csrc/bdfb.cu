@@ -103,6 +103,7 @@ static void free_split(bdfb_batch* b) {
   cudaFree(b->sb.rv);
   cudaFree(b->sb.slist);
   cudaFree(b->sb.jlist);
+  cudaFree(b->sb.ilist);
   cudaFree(b->sb.cnt);
   cudaFree(b->sb.live);
   b->sb = SplitBufs{};
@@ -129,7 +130,8 @@ static int prepare_split(bdfb_batch* b) {
     A((void**)&b->sb.rv, sizeof(int) * (size_t)S);
     A((void**)&b->sb.slist, sizeof(int) * (size_t)S);
     A((void**)&b->sb.jlist, sizeof(int) * (size_t)S);
-    A((void**)&b->sb.cnt, 2 * sizeof(unsigned));
+    A((void**)&b->sb.ilist, sizeof(int) * (size_t)S);
+    A((void**)&b->sb.cnt, 3 * sizeof(unsigned));
     A((void**)&b->sb.live, 2 * sizeof(unsigned long long));
     if (!ok) {
       free_split(b);

@@ -63,6 +63,7 @@ struct SplitK {
     // K_lu one group of 8 lanes per entry
     unsigned gjac = (unsigned)((S * GM::G + blk - 1) / blk);
     if (gjac > (unsigned)gm.setup_grid) gjac = (unsigned)gm.setup_grid;
+    const unsigned ginit = gs < (unsigned)gm.setup_grid ? gs : (unsigned)gm.setup_grid;   // grid-stride over the list
     unsigned glu = (unsigned)((S * OCT + blk - 1) / blk);
     if (glu > (unsigned)gm.setup_grid) glu = (unsigned)gm.setup_grid;
     unsigned grhs = (unsigned)gm.rhs_grid;
@@ -82,6 +83,10 @@ struct SplitK {
         cudaEvent_t* ev = events + k * (SPLIT_PHASES + 1);
         if (events) cudaEventRecord(ev[0], st);
         split_ctl_kernel<Mech, GM><<<gctl, BDFB_SPLIT_CTL_BLOCK, sm, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
+#if BDFB_SPLIT_INIT_KERNEL
+        split_init_cells_kernel<Mech, GM><<<ginit, blk, 0, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
+        ++n;
+#endif
         if (events) cudaEventRecord(ev[1], st);
         split_jac_kernel<Mech, GM><<<gjac, blk, jac_smem(), st>>>(b);
         if (events) cudaEventRecord(ev[2], st);
