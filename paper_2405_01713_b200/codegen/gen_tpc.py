@@ -79,6 +79,21 @@ class Pool:
 d = lit   # rebound per mechanism in generate()
 
 
+NASA_SELECT = os.environ.get("BDFB_NASA_SELECT", "0") == "1"   # branch (default; selects measured 5% slower in K_rhs)
+
+
+def _nasa_sel(A, tab, tm, body):
+    """Branch-free NASA-7 range choice: `body(k, coeff)` with coeff(i, f) -> the expression
+    `(lo ? f(a_low[i]) : f(a_high[i]))` (lanes of one warp may straddle Tmid: no divergent double path)."""
+    for k, s in enumerate(tab["species"]):
+        al, ah = s["nasa"]["low"], s["nasa"]["high"]
+
+        def coeff(i, f=lambda x: x, al=al, ah=ah):
+            vl, vh = f(al[i]), f(ah[i])
+            return d(vl) if vl == vh else f"(lo ? {d(vl)} : {d(vh)})"
+        body(k, coeff)
+
+
 def _nasa(A, tab, tm, body):
     """Emit `body(k, coeffs, indent)` for both NASA-7 ranges (all Tmid equal)."""
     A(f"  if (T < {d(tm)}) {{\n")
@@ -144,6 +159,7 @@ def generate(name, out_dir):
     def thermo_common(A):
         A(f"  const double T = y{K};\n  if (!(T > 0.0)) return 1;\n")
         A("  const double lnT = log(T), invT = 1.0 / T, T2 = T * T, T3 = T2 * T, T4 = T3 * T;\n")
+        A(f"  const bool lo = T < {d(tm)};   // NASA-7 range (selects, _nasa_sel)\n")
         A(f"  const double cRT = T * {d(RU / PATM)}, icRT = {d(PATM / RU)} * invT;\n")
         for k in range(K):
             A(f"  const double C{k} = rho * y{k} * {d(1.0 / W[k])};\n")
@@ -162,6 +178,10 @@ def generate(name, out_dir):
         # -g/RT = -(h/RT - s/R) = a0 (lnT - 1) + a1 T/2 + a2 T^2/6 + a3 T^3/12 + a4 T^4/20 - a5/T + a6
         A(f"    eg{k} = fexp({d(a[0])} * (lnT - 1.0) + {d(a[1] / 2)} * T + {d(a[2] / 6)} * T2 + {d(a[3] / 12)} * T3 + "
           f"{d(a[4] / 20)} * T4 - {d(a[5])} * invT + {d(a[6])});\n")
+
+    def eg_body_sel(k, c):
+        A(f"    eg{k} = fexp({c(0)} * (lnT - 1.0) + {c(1, lambda x: x / 2)} * T + {c(2, lambda x: x / 6)} * T2 + "
+          f"{c(3, lambda x: x / 12)} * T3 + {c(4, lambda x: x / 20)} * T4 - {c(5)} * invT + {c(6)});\n")
 
     def reaction(A, r, x, deriv):
         """Emit the rate of progress q of reaction r (and its derivative data if deriv)."""
@@ -262,7 +282,10 @@ def generate(name, out_dir):
     for k in range(N):
         A(f"  const double y{k} = yv[{k}];\n")
     thermo_common(A)
-    _nasa(A, tab, tm, eg_body)
+    if NASA_SELECT:
+        _nasa_sel(A, tab, tm, eg_body_sel)
+    else:
+        _nasa(A, tab, tm, eg_body)
     post_thermo(A)
     for k in range(K):
         A(f"  double w{k} = 0.0;\n")
@@ -274,7 +297,14 @@ def generate(name, out_dir):
         A(f"    cv = fma(y{k} * {d(RU / W[k])}, {d(a[0] - 1)} + T * ({d(a[1])} + T * ({d(a[2])} + T * ({d(a[3])} + T * {d(a[4])}))), cv);\n")
         A(f"    su = fma({d(a[0] - 1)} + T * ({d(a[1] / 2)} + T * ({d(a[2] / 3)} + T * ({d(a[3] / 4)} + T * {d(a[4] / 5)}))) + "
           f"{d(a[5])} * invT, w{k}, su);\n")
-    _nasa(A, tab, tm, tail_body)
+    def tail_body_sel(k, c):
+        A(f"    cv = fma(y{k} * {d(RU / W[k])}, {c(0, lambda x: x - 1)} + T * ({c(1)} + T * ({c(2)} + T * ({c(3)} + T * {c(4)}))), cv);\n")
+        A(f"    su = fma({c(0, lambda x: x - 1)} + T * ({c(1, lambda x: x / 2)} + T * ({c(2, lambda x: x / 3)} + T * ({c(3, lambda x: x / 4)} + T * {c(4, lambda x: x / 5)}))) + "
+          f"{c(5)} * invT, w{k}, su);\n")
+    if NASA_SELECT:
+        _nasa_sel(A, tab, tm, tail_body_sel)
+    else:
+        _nasa(A, tab, tm, tail_body)
     A("  const double irho = 1.0 / rho;\n")
     for k in range(K):
         A(f"  f[{k}] = {d(W[k])} * w{k} * irho;\n")
