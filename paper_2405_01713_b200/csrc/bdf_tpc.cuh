@@ -55,6 +55,10 @@ struct TS {
   signed char qc;                                  // order of the step whose completion is deferred (F_COMPLETE)
 };
 constexpr int TS_STRIDE = (int)((sizeof(TS) + 7) / 8) | 1;   // odd number of doubles
+#ifndef BDFB_ATTEMPT_UNROLL
+#define BDFB_ATTEMPT_UNROLL 2
+#endif
+constexpr int kAttemptUnroll = BDFB_ATTEMPT_UNROLL;   // chunks of the ATTEMPT pass in flight
 
 #ifndef BDFB_TPC_BLOCK
 #define BDFB_TPC_BLOCK 128
@@ -764,7 +768,7 @@ struct TpcIntegrator {
       double sdn = 0.0, sup = 0.0;
       if (nm1 || np1) {
         const double lq = s.l[q];
-#pragma unroll 2
+#pragma unroll 11   // 2 rounds of loads in flight (latency-bound)
         for (int i = 0; i < N; ++i) {
           const double a = w.acor(i), e = w.ewt(i);
           if (nm1) {
@@ -881,7 +885,7 @@ struct TpcIntegrator {
     const double a1 = s.oc_a1;
     const int qmx = o.qmax;
     const bool wqmax = (fl & F_FQ) && qmx > qwb;      // zn[qmax] = acor lands in its own row
-#pragma unroll 2
+#pragma unroll kAttemptUnroll
     for (int i0 = 0; i0 < N; i0 += CH) {
       double zc[CH][QMAX + 1], zm[CH], ac[CH];
 #pragma unroll
