@@ -20,6 +20,8 @@
 #include "global_host.cuh"
 #include "gen/mech_drm19_class.cuh"
 #include "gen/mech_h2_lidryer.cuh"
+#include "gen/tpc_drm19_class.cuh"
+#include "gen/tpc_h2_lidryer.cuh"
 #include "mech_model.cuh"
 #include "models_simple.cuh"
 #include "tpc_api.h"
@@ -456,7 +458,7 @@ __global__ void gk_fill_stats(CellStatsPtrs cs, long long N, int status, int nst
 }
 
 // global-norm mode: host control loop over device kernels (global_host.cuh)
-template <class Model>
+template <class Model, class Tpc = void>
 static int run_global(bdfb_batch* b, const Opts& o, double* y, const double* fext, const double* aux,
                       cudaStream_t st) {
   if constexpr (Model::G > 1) {
@@ -472,7 +474,7 @@ static int run_global(bdfb_batch* b, const Opts& o, double* y, const double* fex
       cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     }
     cudaEventRecord(b->ev0, st);
-    GlobalRunner<Model> R(b->gb, o, prm, st, b->n, b->ncells, b->d_atol, fext, aux);
+    GlobalRunner<Model, Tpc> R(b->gb, o, prm, st, b->n, b->ncells, b->d_atol, fext, aux);
     const GlobalResult r = R.run(y);
     cudaEventRecord(b->ev1, st);
     const long long N = b->ncells;
@@ -542,8 +544,8 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
   if (b->opt.mode == BDFB_MODE_GLOBAL_NORM) {
     if (layout != BDFB_LAYOUT_YC) return fail(b, BDFB_EUNSUPPORTED, "global-norm mode takes the YC layout");
     switch (b->model) {
-      case BDFB_MODEL_MECH_H2: return run_global<ModelH2>(b, o, y, f_ext, aux, st);
-      case BDFB_MODEL_MECH_DRM19: return run_global<ModelDRM19>(b, o, y, f_ext, aux, st);
+      case BDFB_MODEL_MECH_H2: return run_global<ModelH2, Tpc_h2_lidryer>(b, o, y, f_ext, aux, st);
+      case BDFB_MODEL_MECH_DRM19: return run_global<ModelDRM19, Tpc_drm19_class>(b, o, y, f_ext, aux, st);
       default: return fail(b, BDFB_EUNSUPPORTED, "global-norm mode: group models only (MECH_H2, MECH_DRM19)");
     }
   }

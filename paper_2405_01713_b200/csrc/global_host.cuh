@@ -7,9 +7,11 @@
 #pragma once
 #include <nccl.h>
 
+#include <type_traits>
 #include <vector>
 
 #include "global_mode.cuh"
+#include "global_tpc.cuh"
 
 namespace bdfb {
 
@@ -31,8 +33,12 @@ struct GlobalResult {
   long long launches;
 };
 
-template <class Model>
+// Tpc: the thread-per-cell mechanism type (gen/tpc_<mech>.cuh) whose kernels (global_tpc.cuh) do the RHS,
+// setup and solve; void: the group kernels of global_mode.cuh
+template <class Model, class Tpc = void>
 struct GlobalRunner {
+  static constexpr bool TPC = !std::is_void<Tpc>::value;
+  using TM = typename std::conditional<TPC, Tpc, Model>::type;
   using P = typename Model::Params;
   static constexpr int QM = QMAX;
   GlobalBuffers& B;
@@ -113,7 +119,11 @@ struct GlobalRunner {
 
   int rhs(double t, const double* yin, double* fout) {
     cudaMemsetAsync(B.flag, 0, sizeof(int), st);
-    ++launches; gk_rhs<Model><<<gridg(), 128, smemg(), st>>>(prm, N, t, yin, fext, aux, fout, B.flag);
+    if constexpr (TPC) {
+      ++launches; gt_rhs<TM><<<gridc(), 128, 0, st>>>(N, yin, fext, aux, fout, B.flag);
+    } else {
+      ++launches; gk_rhs<Model><<<gridg(), 128, smemg(), st>>>(prm, N, t, yin, fext, aux, fout, B.flag);
+    }
     nfe++;
     int fl = 0;
     cudaMemcpyAsync(&fl, B.flag, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -242,8 +252,13 @@ struct GlobalRunner {
       jcur = 0;
     }
     cudaMemsetAsync(B.flag, 0, sizeof(int), st);
-    ++launches; gk_setup<Model><<<gridg(), 128, smemg(), st>>>(prm, N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.pos,
-                                                   B.perm, B.invd, B.flag);
+    if constexpr (TPC) {
+      ++launches; gt_setup<TM><<<gridc(), 128, 0, st>>>(N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.perm,
+                                                         B.invd, B.flag);
+    } else {
+      ++launches; gk_setup<Model><<<gridg(), 128, smemg(), st>>>(prm, N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU,
+                                                                  B.pos, B.perm, B.invd, B.flag);
+    }
     int fl = 0;
     cudaMemcpyAsync(&fl, B.flag, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
@@ -275,8 +290,13 @@ struct GlobalRunner {
         for (;;) {
           nni++;
           const double sc2 = (gamrat != 1.0) ? 2.0 / (1.0 + gamrat) : 1.0;
-          ++launches; gk_solve<Model><<<gridg(), 128, smemg(), st>>>(N, sc2, B.LU, B.pos, B.perm, B.invd, B.v.del, B.v.acor,
-                                                         B.v.tmp);
+          if constexpr (TPC) {
+            ++launches; gt_solve<TM><<<gridc(), 128, 0, st>>>(N, sc2, B.LU, B.perm, B.invd, B.v.del, B.v.acor,
+                                                               B.v.tmp);
+          } else {
+            ++launches; gk_solve<Model><<<gridg(), 128, smemg(), st>>>(N, sc2, B.LU, B.pos, B.perm, B.invd, B.v.del,
+                                                                        B.v.acor, B.v.tmp);
+          }
           const double del = wrms(B.v.tmp);
           if (m > 0) crate = fmax(CRDOWN * crate, del / dprev);
           const double dcon = del * fmin(1.0, crate) / tol;
