@@ -11,6 +11,10 @@
 // (|df| <= 1e-12 S, reading R19); the oracle uses its own libm exp.
 #pragma once
 
+#ifndef BDFB_FEXP_ESTRIN
+#define BDFB_FEXP_ESTRIN 0
+#endif
+
 namespace bdfb {
 
 __constant__ double kFexp[15] = {
@@ -35,11 +39,22 @@ __device__ __forceinline__ double fexp(double x) {
   const double k = t - 6755399441055744.0;
   double r = fma(k, -kFexp[1], x);
   r = fma(k, -kFexp[2], r);
+#if BDFB_FEXP_ESTRIN
+  // Estrin's scheme: the same degree-12 Taylor polynomial, 5 dependent FMA levels instead of 13 (the RHS is
+  // latency-bound on these chains); coefficients c_k = 1/k! (kFexp[15 - k] for k >= 2)
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  const double a0 = fma(r, 1.0, 1.0), a1 = fma(kFexp[12], r, kFexp[13]), a2 = fma(kFexp[10], r, kFexp[11]),
+               a3 = fma(kFexp[8], r, kFexp[9]), a4 = fma(kFexp[6], r, kFexp[7]), a5 = fma(kFexp[4], r, kFexp[5]);
+  const double b0 = fma(a1, r2, a0), b1 = fma(a3, r2, a2), b2 = fma(a5, r2, a4);
+  const double d0 = fma(b1, r4, b0), d1 = fma(kFexp[3], r4, b2);
+  const double p = fma(d1, r8, d0);
+#else
   double p = fma(kFexp[3], r, kFexp[4]);
 #pragma unroll
   for (int i = 5; i < 14; ++i) p = fma(p, r, kFexp[i]);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
+#endif
   const int ki = __double2loint(t);
   double res = __hiloint2double(__double2hiint(p) + (ki << 20), __double2loint(p));
   // branch-free range handling (a taken branch per exp breaks the instruction

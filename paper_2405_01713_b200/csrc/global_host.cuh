@@ -109,7 +109,7 @@ struct GlobalRunner {
     ++launches; gk_cellsum<<<gridc(), 128, 0, st>>>(x, B.v.ewt, B.s, n, N);
     const long long nb = (N + GM_BLK - 1) / GM_BLK;
     ++launches; gk_blocksum<<<(unsigned)((nb + 127) / 128), 128, 0, st>>>(B.s, B.P, N);
-    ++launches; gk_finalsum<<<1, 1, 0, st>>>(B.P, nb, B.sum);
+    ++launches; gk_finalsum<<<1, GK_FINAL_THREADS, 0, st>>>(B.P, nb, B.sum);
     double S = 0.0;
     cudaMemcpyAsync(&S, B.sum, sizeof(double), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);

@@ -132,12 +132,21 @@ __global__ void gk_blocksum(const double* s, double* P, long long N) {
   for (long long c = c0; c < c1; ++c) acc = acc + s[c];
   P[b] = acc;
 }
-__global__ void gk_finalsum(const double* P, long long nb, double* out) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double acc = 0.0;
-    for (long long b = 0; b < nb; ++b) acc = acc + P[b];
-    out[0] = acc;
+// the block partials summed in order (reading R15: bit-reproducible); the block stages chunks of P in
+// shared memory with coalesced loads so that the one sequential summing thread reads on-chip operands
+constexpr int GK_FINAL_THREADS = 256, GK_FINAL_CHUNK = 4096;
+__global__ void __launch_bounds__(GK_FINAL_THREADS) gk_finalsum(const double* P, long long nb, double* out) {
+  __shared__ double sp[GK_FINAL_CHUNK];
+  double acc = 0.0;
+  for (long long b0 = 0; b0 < nb; b0 += GK_FINAL_CHUNK) {
+    const int m = (int)(nb - b0 < GK_FINAL_CHUNK ? nb - b0 : GK_FINAL_CHUNK);
+    for (int i = threadIdx.x; i < m; i += GK_FINAL_THREADS) sp[i] = P[b0 + i];
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int i = 0; i < m; ++i) acc = acc + sp[i];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) out[0] = acc;
 }
 // max_i |zn1| / (0.1 |zn0| + 1/ewt)  (cvUpperBoundH0) -> atomicMax on the bits of a positive double
 __global__ void gk_hubinv(GVec v, long long M, unsigned long long* out) {
