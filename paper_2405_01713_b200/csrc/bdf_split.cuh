@@ -85,7 +85,7 @@ struct SplitBufs {
   int* slist;                  // setup list (slots)
   int* jlist;                  // Jacobian list (slots)
   int* ilist;                  // cell start/end list (slots for K_init)
-  unsigned* cnt;               // [0] setup count, [1] Jacobian count, [2] K_init count
+  unsigned* cnt;               // [3 (it & 1) + {0, 1, 2}]: setup, Jacobian, K_init list counts of iteration it
   unsigned long long* live;    // [2]: live slots after the K_ctl of iteration it (it & 1)
   long long slots;             // S (multiple of 32)
 };
@@ -220,7 +220,7 @@ __global__ void split_init_kernel(SplitBufs b) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s == 0) {
     b.live[0] = b.live[1] = 0;
-    b.cnt[0] = b.cnt[1] = b.cnt[2] = 0;
+    for (int i = 0; i < 6; ++i) b.cnt[i] = 0;
   }
   if (s >= b.slots) return;
   TS* t = Split<Mech, GM>::ts(b, s);
@@ -251,6 +251,12 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
   if (threadIdx.x < N) satol[threadIdx.x] = atol[threadIdx.x];
   if (lane == 0) wacc[warp] = Agg{};
   if (threadIdx.x == 0) blive = 0;
+  unsigned* cnt = b.cnt + 3 * (it & 1);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // the next iteration's lists and live count (their last
+    unsigned* nx = b.cnt + 3 * ((it + 1) & 1);   // readers, iteration it - 1, have finished)
+    nx[0] = nx[1] = nx[2] = 0;
+    b.live[(it + 1) & 1] = 0;
+  }
   // the warp's 32 TS records are contiguous in HBM: stage them through shared memory (coalesced), warp-local
   const long long w0 = (long long)blockIdx.x * BDFB_SPLIT_CTL_BLOCK + (threadIdx.x & ~31u);
   const long long nrec = (b.slots - w0 < 32 ? (b.slots - w0 > 0 ? b.slots - w0 : 0) : 32) * TS_STRIDE;
@@ -357,8 +363,8 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     const unsigned bs = __ballot_sync(0xffffffffu, setup), bj = __ballot_sync(0xffffffffu, jreq);
     unsigned os = 0, oj = 0;
     if (lane == 0) {
-      if (bs) os = atomicAdd(&b.cnt[0], __popc(bs));
-      if (bj) oj = atomicAdd(&b.cnt[1], __popc(bj));
+      if (bs) os = atomicAdd(&cnt[0], __popc(bs));
+      if (bj) oj = atomicAdd(&cnt[1], __popc(bj));
     }
     os = __shfl_sync(0xffffffffu, os, 0);
     oj = __shfl_sync(0xffffffffu, oj, 0);
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     if (jreq) b.jlist[oj + __popc(bj & below)] = (int)slot;
     const unsigned bi = __ballot_sync(0xffffffffu, init);
     unsigned oi = 0;
-    if (lane == 0 && bi) oi = atomicAdd(&b.cnt[2], __popc(bi));
+    if (lane == 0 && bi) oi = atomicAdd(&cnt[2], __popc(bi));
     oi = __shfl_sync(0xffffffffu, oi, 0);
     if (init) b.ilist[oi + __popc(bi & below)] = (int)slot;
     const unsigned bl = __ballot_sync(0xffffffffu, act == I::A_RET);
@@ -419,7 +425,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_init_cells_kernel(Opts
   if (threadIdx.x < N) satol[threadIdx.x] = atol[threadIdx.x];
   if (lane == 0) wacc[warp] = Agg{};
   __syncthreads();
-  const long long cnt = b.cnt[2];
+  const long long cnt = b.cnt[3 * (it & 1) + 2];
   unsigned long long nlive = 0;
   for (long long e = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; e - lane < cnt;
        e += (long long)gridDim.x * BDFB_SPLIT_BLOCK) {
@@ -479,7 +485,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_init_cells_kernel(Opts
 // recoverable failure).  Shared scratch per group: RHS scratch SG + the
 // Jacobian's per-reaction partials JG.
 template <class Mech, class GM>
-__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_kernel(SplitBufs b) {
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM>;
   constexpr int N = Mech::N, G = GM::G;
   constexpr int MS = N | 1;                      // odd row stride of the shared J (conflict-free)
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_kernel(SplitBufs b
   const int gi = threadIdx.x / G;
   double* sc = smem + gi * (GM::SG + GM::JG + N * MS);
   double* jm = sc + GM::SG + GM::JG;
-  const long long cnt = b.cnt[1], groups = (long long)gridDim.x * (BDFB_SPLIT_BLOCK / G);
+  const long long cnt = b.cnt[3 * (it & 1) + 1], groups = (long long)gridDim.x * (BDFB_SPLIT_BLOCK / G);
   for (long long e = ((long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x) / G; e < cnt; e += groups) {
     const long long slot = b.jlist[e];
     const typename SP::W w = SP::ws(b, slot);
@@ -614,12 +620,12 @@ __device__ __forceinline__ int oct_factor(unsigned gmask, int gl, double (&a)[(N
 // from the cell's column-major J, oct_factor, factors stored column-major in
 // pivoted row order + 1/U_kk + perm, as the Newton solve of K_ctl reads them.
 template <class Mech, class GM>
-__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b) {
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM>;
   constexpr int N = Mech::N, R = (N + OCT - 1) / OCT;
   const int lane = threadIdx.x & 31, gl = lane & (OCT - 1);
   const unsigned gmask = 0xffu << (lane & ~(OCT - 1));
-  const long long cnt = b.cnt[0], groups = (long long)gridDim.x * (BDFB_SPLIT_BLOCK / OCT);
+  const long long cnt = b.cnt[3 * (it & 1)], groups = (long long)gridDim.x * (BDFB_SPLIT_BLOCK / OCT);
   for (long long e = ((long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x) / OCT; e < cnt; e += groups) {
     const long long slot = b.slist[e];
     TS* t = SP::ts(b, slot);
@@ -655,9 +661,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b)
 }
 
 // ------------------------------------------------------------------ K_rhs
-// thread per slot: fr = R(yq) + F for a pending RHS request.  Also resets the
-// list counters and the live count for the next iteration (it + 1) -- after
-// the setup kernels of this iteration consumed the lists.
+// thread per slot: fr = R(yq) + F for a pending RHS request.
 #ifndef BDFB_SPLIT_RHS_MINB
 #define BDFB_SPLIT_RHS_MINB 3   // 168 registers, 12 warps/SM: 7% faster than 255 registers / 8 warps (measured)
 #endif
@@ -665,10 +669,6 @@ template <class Mech, class GM>
 __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_RHS_MINB) split_rhs_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM>;
   constexpr int N = Mech::N;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    b.cnt[0] = b.cnt[1] = b.cnt[2] = 0;
-    b.live[(it + 1) & 1] = 0;
-  }
   const long long stride = (long long)gridDim.x * BDFB_SPLIT_BLOCK;
   for (long long slot = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; slot < b.slots; slot += stride) {
     const TS* t = SP::ts(b, slot);

@@ -61,6 +61,8 @@ struct bdfb_batch {
   SplitGeom sgeom{};
   unsigned long long* h_live = nullptr;   // pinned: live-slot count read back per launch batch
   std::vector<cudaEvent_t> sev;           // split: per-phase timing events of one launch batch
+  std::vector<cudaEvent_t> xev;           // split overlap: ordering events between the two streams
+  cudaStream_t st2 = nullptr;             // split overlap: stream of K_jac + K_lu (BDFB_SPLIT_OVERLAP=1)
   double phase_ms[8] = {};                // split: device ms per phase of the last integrate
   int nphases = 0;
   std::string err;
@@ -133,7 +135,7 @@ static int prepare_split(bdfb_batch* b) {
     A((void**)&b->sb.slist, sizeof(int) * (size_t)S);
     A((void**)&b->sb.jlist, sizeof(int) * (size_t)S);
     A((void**)&b->sb.ilist, sizeof(int) * (size_t)S);
-    A((void**)&b->sb.cnt, 3 * sizeof(unsigned));
+    A((void**)&b->sb.cnt, 6 * sizeof(unsigned));
     A((void**)&b->sb.live, 2 * sizeof(unsigned long long));
     if (!ok) {
       free_split(b);
@@ -156,14 +158,28 @@ static int launch_split(bdfb_batch* b, const Opts& o, double* y, const double* f
   int launches = 0;
   int batch = 16;
   if (const char* env = getenv("BDFB_SPLIT_BATCH")) batch = atoi(env) > 0 ? atoi(env) : batch;
-  if ((int)b->sev.size() < (SPLIT_PHASES + 1) * batch) {
+  if ((int)b->sev.size() < (SPLIT_PHASES + 2) * batch) {
     for (auto ev : b->sev) cudaEventDestroy(ev);
-    b->sev.assign((SPLIT_PHASES + 1) * batch, nullptr);
+    b->sev.assign((SPLIT_PHASES + 2) * batch, nullptr);
     for (auto& ev : b->sev)
       if (cudaEventCreate(&ev) != cudaSuccess) return fail(b, BDFB_ECUDA, "timing events");
   }
+  const char* ov = getenv("BDFB_SPLIT_OVERLAP");
+  const bool overlap = ov && atoi(ov) == 1;
+  if (overlap) {
+    if (!b->st2 && cudaStreamCreateWithFlags(&b->st2, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(b, BDFB_ECUDA, "second stream");
+    if ((int)b->xev.size() < 2 * batch) {
+      for (auto ev : b->xev) cudaEventDestroy(ev);
+      b->xev.assign(2 * batch, nullptr);
+      for (auto& ev : b->xev)
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+          return fail(b, BDFB_ECUDA, "ordering events");
+    }
+  }
   cudaError_t e = split_integrate(b->model, o, y, fext, aux, b->d_atol, b->sb, b->sgeom, b->d_counter, b->d_agg,
-                                  b->cs, b->h_live, batch, st, &launches, b->sev.data(), b->phase_ms);
+                                  b->cs, b->h_live, batch, st, &launches, b->sev.data(), b->phase_ms,
+                                  overlap ? b->st2 : nullptr, overlap ? b->xev.data() : nullptr);
   b->nphases = SPLIT_PHASES;
   cudaEventRecord(b->ev1, st);
   if (e != cudaSuccess) return cuda_fail(b, e, "split integrate");
@@ -302,6 +318,8 @@ void bdfb_destroy(bdfb_batch* b) {
   free_split(b);
   if (b->h_live) cudaFreeHost(b->h_live);
   for (auto ev : b->sev) cudaEventDestroy(ev);
+  for (auto ev : b->xev) cudaEventDestroy(ev);
+  if (b->st2) cudaStreamDestroy(b->st2);
   {
     GlobalBuffers& g = b->gb;
     for (int j = 0; j <= QMAX; ++j) cudaFree(g.v.zn[j]);

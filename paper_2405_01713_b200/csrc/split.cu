@@ -54,7 +54,8 @@ struct SplitK {
   static cudaError_t run(const Opts& o, double* y, const double* fext, const double* aux, const double* atol,
                          const SplitBufs& b, const SplitGeom& gm, unsigned long long* counter, Agg* agg,
                          const CellStatsPtrs& cs, unsigned long long* h_live, int batch, cudaStream_t st,
-                         int* launches, cudaEvent_t* events, double* phase_ms) {
+                         int* launches, cudaEvent_t* events, double* phase_ms, cudaStream_t st2,
+                         cudaEvent_t* xev) {
     const long long S = b.slots;
     const unsigned blk = BDFB_SPLIT_BLOCK;
     const unsigned gs = (unsigned)((S + blk - 1) / blk);            // one thread per slot / list entry
@@ -77,10 +78,14 @@ struct SplitK {
     int n = 1;
     cudaError_t e;
     for (int i = 0; i < SPLIT_PHASES; ++i) phase_ms[i] = 0.0;
+    const bool ovl = st2 != nullptr;   // K_jac + K_lu on st2, overlapping K_rhs (disjoint slots)
+    if (ovl) grhs = grhs * 2 / 3 > 0 ? grhs * 2 / 3 : 1;   // leave registers for the setup kernels
+    cudaEvent_t last_l = nullptr;
     for (int it = 0;;) {
       int k = 0;
       for (; k < batch; ++k, ++it) {
-        cudaEvent_t* ev = events + k * (SPLIT_PHASES + 1);
+        cudaEvent_t* ev = events + k * (SPLIT_PHASES + 2);
+        if (ovl && last_l) cudaStreamWaitEvent(st, last_l, 0);
         if (events) cudaEventRecord(ev[0], st);
         split_ctl_kernel<Mech, GM><<<gctl, BDFB_SPLIT_CTL_BLOCK, sm, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
 #if BDFB_SPLIT_INIT_KERNEL
@@ -88,10 +93,21 @@ struct SplitK {
         ++n;
 #endif
         if (events) cudaEventRecord(ev[1], st);
-        split_jac_kernel<Mech, GM><<<gjac, blk, jac_smem(), st>>>(b);
-        if (events) cudaEventRecord(ev[2], st);
-        split_lu_kernel<Mech, GM><<<glu, blk, 0, st>>>(b);
-        if (events) cudaEventRecord(ev[3], st);
+        cudaStream_t ss = st;
+        if (ovl) {
+          cudaEventRecord(xev[2 * k], st);
+          cudaStreamWaitEvent(st2, xev[2 * k], 0);
+          ss = st2;
+          if (events) cudaEventRecord(ev[5], st2);
+        }
+        split_jac_kernel<Mech, GM><<<gjac, blk, jac_smem(), ss>>>(b, it);
+        if (events) cudaEventRecord(ev[2], ss);
+        split_lu_kernel<Mech, GM><<<glu, blk, 0, ss>>>(b, it);
+        if (events) cudaEventRecord(ev[3], ss);
+        if (ovl) {
+          cudaEventRecord(xev[2 * k + 1], st2);
+          last_l = xev[2 * k + 1];
+        }
         split_rhs_kernel<Mech, GM><<<grhs, blk, 0, st>>>(b, it);
         if (events) cudaEventRecord(ev[4], st);
         n += 4;
@@ -102,11 +118,15 @@ struct SplitK {
                                st)) != cudaSuccess)
         return e;
       if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+      if (ovl && (e = cudaStreamSynchronize(st2)) != cudaSuccess) return e;
       for (int j = 0; events && j < k; ++j) {
-        cudaEvent_t* ev = events + j * (SPLIT_PHASES + 1);
+        cudaEvent_t* ev = events + j * (SPLIT_PHASES + 2);
+        // phases: ctl ev0->ev1, jac (ev1 or ev5 on st2)->ev2, lu ev2->ev3, rhs (ev3 or ev1)->ev4
+        const cudaEvent_t from[SPLIT_PHASES] = {ev[0], ovl ? ev[5] : ev[1], ev[2], ovl ? ev[1] : ev[3]};
+        const cudaEvent_t to[SPLIT_PHASES] = {ev[1], ev[2], ev[3], ev[4]};
         for (int i = 0; i < SPLIT_PHASES; ++i) {
           float ms = 0.f;
-          if (cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) == cudaSuccess) phase_ms[i] += ms;
+          if (cudaEventElapsedTime(&ms, from[i], to[i]) == cudaSuccess) phase_ms[i] += ms;
         }
       }
       if (*h_live == 0) break;
@@ -132,14 +152,15 @@ cudaError_t split_geometry(int mech, int device, SplitGeom* gm) {
 cudaError_t split_integrate(int mech, const Opts& o, double* y, const double* fext, const double* aux,
                             const double* atol, const SplitBufs& sb, const SplitGeom& gm, unsigned long long* counter,
                             Agg* agg, const CellStatsPtrs& cs, unsigned long long* h_live, int batch,
-                            cudaStream_t st, int* launches, cudaEvent_t* events, double* phase_ms) {
+                            cudaStream_t st, int* launches, cudaEvent_t* events, double* phase_ms, cudaStream_t st2,
+                            cudaEvent_t* xev) {
   switch (mech) {
     case BDFB_MODEL_MECH_H2:
       return KH2::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches, events,
-                       phase_ms);
+                       phase_ms, st2, xev);
     case BDFB_MODEL_MECH_DRM19:
       return KDRM::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches, events,
-                        phase_ms);
+                        phase_ms, st2, xev);
   }
   return cudaErrorInvalidValue;
 }

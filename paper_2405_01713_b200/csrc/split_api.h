@@ -22,12 +22,15 @@ cudaError_t split_geometry(int mech, int device, SplitGeom* gm);
 // Integrate all o.ncells cells through the slot pool sb (host loop over
 // K_ctl/K_rhs launch batches of `batch` iterations on st, one live-count read
 // back per batch; synchronous).  launches: kernels enqueued.
-// events: (SPLIT_PHASES + 1) * batch timing events (or NULL); phase_ms: device
+// events: (SPLIT_PHASES + 2) * batch timing events (or NULL); phase_ms: device
 // time of each phase (K_ctl, K_jac, K_lu, K_rhs) summed over the integrate.
+// st2 (or NULL): a second stream on which K_jac and K_lu run, overlapping K_rhs
+// (they touch disjoint slots); xev: 2 * batch ordering events for it.
 constexpr int SPLIT_PHASES = 4;
 cudaError_t split_integrate(int mech, const Opts& o, double* y, const double* fext, const double* aux,
                             const double* atol, const SplitBufs& sb, const SplitGeom& gm, unsigned long long* counter,
                             Agg* agg, const CellStatsPtrs& cs, unsigned long long* h_live, int batch,
-                            cudaStream_t st, int* launches, cudaEvent_t* events, double* phase_ms);
+                            cudaStream_t st, int* launches, cudaEvent_t* events, double* phase_ms,
+                            cudaStream_t st2, cudaEvent_t* xev);
 
 }  // namespace bdfb
