@@ -313,11 +313,34 @@ static int residual(cell *c, const double *ycor, double *G)
 
 /* matrix setup (cvLsSetup dense / CVDiagSetup).  Returns 0, >0 recoverable,
  * <0 unrecoverable.  *jcur set when J was (re)evaluated.                  */
+/* cvLsDenseDQJac (CVODE; the paper's finite-difference Jacobian, approaches 3A/3B) */
+int orc_jac_dq(const orc_problem *p, double t, const double *y, const double *fy, const double *ewt, double h,
+               double *J)
+{
+  const int n = p->n;
+  const double srur = sqrt(UROUND);
+  const double fnorm = orc_wrms(n, fy, ewt, 1);
+  const double minInc = (fnorm != 0.0) ? (1000.0 * fabs(h) * UROUND * n * fnorm) : 1.0;
+  double yp[ORC_NMAX], ft[ORC_NMAX];
+  for (int i = 0; i < n; ++i) yp[i] = y[i];
+  for (int j = 0; j < n; ++j) {
+    const double yj = yp[j];
+    const double inc = fmax(srur * fabs(yj), minInc / ewt[j]);
+    yp[j] = yj + inc;
+    const int r = orc_rhs(p, t, yp, ft);
+    yp[j] = yj;
+    if (r) return r;
+    const double inc_inv = 1.0 / inc;
+    for (int i = 0; i < n; ++i) J[i * n + j] = inc_inv * ft[i] + (-inc_inv) * fy[i];
+  }
+  return 0;
+}
+
 static int lsetup(cell *c, int convfail, int *jcur)
 {
   int n = c->n;
   int rv = 0;
-  if (c->o->ls == ORC_LS_DENSE) {
+  if (c->o->ls == ORC_LS_DENSE || c->o->ls == ORC_LS_DENSE_DQ) {
     double dgamma = fabs(c->gamma / c->gammap - 1.0);
     int jbad = (c->st.nst == 0) || (c->st.nst >= c->nstlj + MSBJ) ||
                (convfail == CF_BAD_J && dgamma < DGMAX_JBAD) || (convfail == CF_OTHER);
@@ -331,7 +354,13 @@ static int lsetup(cell *c, int convfail, int *jcur)
           q.rho = c->rho_all ? c->rho_all[k] : q.rho;
           q.fext = c->fext_all ? c->fext_all + k * n : NULL;
         }
-        if (orc_jac(&q, c->tn, c->y + k * n, c->J + k * n * n)) rv = -1;
+        if (c->o->ls == ORC_LS_DENSE_DQ) {   /* per-cell mode only (the global variant uses the analytic J) */
+          const int r = orc_jac_dq(&q, c->tn, c->y + k * n, c->ftemp + k * n, c->ewt + k * n, c->h,
+                                   c->J + k * n * n);
+          if (r) rv = r > 0 ? 1 : -1;
+        } else if (orc_jac(&q, c->tn, c->y + k * n, c->J + k * n * n)) {
+          rv = -1;
+        }
       }
     } else {
       *jcur = 0;
@@ -383,7 +412,7 @@ static int lsetup(cell *c, int convfail, int *jcur)
 static int lsolve(cell *c, double *b)
 {
   int n = c->n;
-  if (c->o->ls == ORC_LS_DENSE) {
+  if (c->o->ls != ORC_LS_DIAG) {
     for (long k = 0; k < c->ncell; ++k) orc_lu_solve(n, c->M + k * n * n, c->piv + k * n, b + k * n);
     if (c->gamrat != 1.0) {
       double s = 2.0 / (1.0 + c->gamrat);

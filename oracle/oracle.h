@@ -44,7 +44,9 @@ enum {
 };
 
 /* linear-solver choice inside Newton (P:399 dense direct, P:480 CVDiag) */
-enum { ORC_LS_DENSE = 0, ORC_LS_DIAG = 1 };
+/* ORC_LS_DENSE_DQ: dense direct solver with the difference-quotient Jacobian (the paper's approaches 3A/3B,
+ * P:177-178) instead of the analytic one (2A/2B) */
+enum { ORC_LS_DENSE = 0, ORC_LS_DIAG = 1, ORC_LS_DENSE_DQ = 2 };
 
 /* Jacobian source for the dense solver */
 enum { ORC_JAC_ANALYTIC = 0 /* model's exact J: closed form or complex step */ };
@@ -105,7 +107,7 @@ typedef struct {
   int64_t mxstep;        /* R12: per outer step */
   double h0;             /* 0 = cvHin */
   double hmin, hmax;     /* hmax <= 0 means infinity */
-  int ls;                /* ORC_LS_DENSE | ORC_LS_DIAG */
+  int ls;                /* ORC_LS_DENSE | ORC_LS_DIAG | ORC_LS_DENSE_DQ */
   int group;             /* G: WRMS summation order emulation (R15); 1 = sequential */
 } orc_opts;
 
@@ -151,6 +153,12 @@ int orc_rhs_scale(const orc_problem *p, double t, const double *y, double *S);
 /* J = d f / d y (row-major).  Analytic (LINEAR, ROBERTSON) or complex-step
  * (MECH).  Returns 0 or >0 on failure.  KWH has no J (CVDiag only).       */
 int orc_jac(const orc_problem *p, double t, const double *y, double *J);
+/* Difference-quotient dense Jacobian (CVODE's cvLsDenseDQJac, the reading of the paper's "finite
+ * difference" Jacobian): srur = sqrt(u), fnorm = ||fy||_WRMS(ewt) (sequential order),
+ * minInc = 1000 |h| u n fnorm (1 if fnorm = 0); column j: inc = max(srur |y_j|, minInc / ewt_j),
+ * J(:, j) = (1/inc) f(t, y + inc e_j) + (-(1/inc)) fy.  fy = f(t, y).  Returns 0 or the RHS failure. */
+int orc_jac_dq(const orc_problem *p, double t, const double *y, const double *fy, const double *ewt, double h,
+               double *J);
 
 /* KWH pin entry: converged ionisation state for energy e:
  * out8 = [T, n_H0, n_H+, n_He0, n_He+, n_He++, n_e, g(x_e)]              */

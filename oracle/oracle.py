@@ -21,7 +21,7 @@ REPO = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 
 MODEL_LINEAR, MODEL_ROBERTSON, MODEL_KWH, MODEL_MECH = 0, 1, 2, 3
-LS_DENSE, LS_DIAG = 0, 1
+LS_DENSE, LS_DIAG, LS_DENSE_DQ = 0, 1, 2
 STATUS = {0: "OK", 1: "TOO_MUCH_WORK", 2: "ERR_FAILURE", 3: "CONV_FAILURE", 4: "RHS_FAIL",
           5: "NONFINITE_INPUT"}
 QMAX = 5
@@ -88,6 +88,8 @@ def lib():
             dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int)
             L.orc_wrms.restype = C.c_double
             L.orc_wrms.argtypes = [C.c_int, dp, dp, C.c_int]
+            L.orc_jac_dq.restype = C.c_int
+            L.orc_jac_dq.argtypes = [C.POINTER(Problem), C.c_double, dp, dp, dp, C.c_double, dp]
             L.orc_typical_values.restype = None
             L.orc_typical_values.argtypes = [C.c_int, C.c_int64, dp, dp]
             L.orc_atol_from_typical.restype = None
@@ -333,6 +335,17 @@ def jac(model, y, rho=1.0, fext=None, t=0.0):
     J = np.zeros((model.n, model.n))
     p = model.problem(rho, fext)
     r = lib().orc_jac(C.byref(p), t, _dp(y), _dp(J))
+    return J, r
+
+
+def jac_dq(model, y, fy, ewt, h, rho=1.0, fext=None, t=0.0):
+    """Difference-quotient Jacobian (orc_jac_dq, CVODE's cvLsDenseDQJac)."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    fy = np.ascontiguousarray(fy, dtype=np.float64)
+    ewt = np.ascontiguousarray(ewt, dtype=np.float64)
+    J = np.zeros((model.n, model.n))
+    p = model.problem(rho, fext)
+    r = lib().orc_jac_dq(C.byref(p), t, _dp(y), _dp(fy), _dp(ewt), float(h), _dp(J))
     return J, r
 
 

@@ -168,3 +168,42 @@ def test_kwh_pure_function_and_failure(oracle):
     assert f1[0] == f2[0]
     assert oracle.rhs(m, [0.0], 1e-27)[1] == 1
     assert oracle.rhs(m, [1e30], 1e-27)[1] == 1
+
+
+# ---- difference-quotient Jacobian (CVODE cvLsDenseDQJac) -------------------
+def test_jac_dq_exact_on_linear_and_close_on_robertson(oracle):
+    """DQ columns of a linear f are the exact matrix up to the rounding of one difference quotient; on
+    Robertson (polynomial f) the DQ Jacobian agrees with the analytic one to O(sqrt(u)) relative."""
+    lam = [-1.0, -10.0, -1e4]
+    m = oracle.Model.linear(lam)
+    y = np.array([1.0, 0.5, 2.0])
+    fy, _ = oracle.rhs(m, y)
+    J, r = oracle.jac_dq(m, y, fy, 1.0 / (1e-6 * np.abs(y) + 1e-10), 1e-3)
+    assert r == 0
+    assert np.allclose(J, np.diag(lam), rtol=1e-6, atol=0.0)
+    rob = oracle.Model.robertson()
+    for y in ([0.9, 2e-5, 0.1], [0.3, 1e-6, 0.7], [0.999, 3e-5, 1e-3]):   # interior states (all y_i > 0)
+        y = np.array(y)
+        fy, _ = oracle.rhs(rob, y)
+        Jd, r = oracle.jac_dq(rob, y, fy, 1.0 / (1e-6 * np.abs(y) + 1e-10), 1e-4)
+        Ja, _ = oracle.jac(rob, y)
+        # row-scaled, with a floor for all-zero rows: a zero analytic entry (e.g. d(y3')/dy2 = 6e7 y2 at
+        # y2 = 0) is matched only up to the O(inc) truncation term f'' inc of the one-sided quotient
+        scale = np.maximum(np.abs(Ja).max(axis=1, keepdims=True), 1e-3 * np.abs(Ja).max())
+        assert r == 0 and np.all(np.abs(Jd - Ja) <= 1e-6 * scale)
+
+
+@pytest.mark.parametrize("mech", ["h2_lidryer", "drm19_class"])
+def test_dq_integration_matches_analytic_ac8(oracle, mech):
+    """SPEC AC8: end states with the difference-quotient Jacobian (approaches 3A/3B) agree with the
+    analytic-Jacobian run (2A/2B) within 100 rtol on flame cells (modified Newton tolerates J errors; the
+    error test guards the accuracy)."""
+    from synth import flame_field
+    y, rho, F, prog = flame_field(mech, 8, dt=1e-5)
+    idx = np.arange(0, y.shape[1], 8)
+    m = oracle.Model.mechanism(mech)
+    ya, sa = oracle.integrate_batch(m, y, 0.0, 1e-5, 1e-6, 1e-10, rho=rho, fext_yc=F, cells=idx, threads=8)
+    yd, sd = oracle.integrate_batch(m, y, 0.0, 1e-5, 1e-6, 1e-10, rho=rho, fext_yc=F, cells=idx, threads=8,
+                                    ls=oracle.LS_DENSE_DQ)
+    assert np.all(sa["status"] == 0) and np.all(sd["status"] == 0)
+    assert np.all(np.abs(yd - ya) <= 100 * 1e-6 * np.abs(ya) + 1e-9)
