@@ -282,6 +282,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--kernel", default=None, choices=["thread", "group", "split"],
                     help="per-cell kernel organisation of the mechanism models (default: the library's)")
+    ap.add_argument("--jac", default="analytic", choices=["analytic", "dq"],
+                    help="Jacobian: analytic (2A/2B) or CVODE's difference quotient (3A/3B; SPLIT kernel)")
     args = ap.parse_args()
 
     from paper_2405_01713_b200 import parallel as PL
@@ -326,6 +328,8 @@ def main():
     if args.kernel and mech:
         b.set_kernel(args.kernel)
     b.set_model(model)
+    if args.jac != "analytic":
+        b.set_jacobian(args.jac)
     if glob_mode and world > 1:
         # one lockstep system across ranks: the library's own NCCL communicator carries the norms
         uid = torch.cuda.nccl.unique_id() if rank == 0 else None
@@ -459,7 +463,7 @@ def main():
                                            if glob_mode else f"dp{world} (cells sharded, no collective)"),
                            "l2": "inputs larger than L2 (state %.2f GB per GPU); pristine field restored "
                                  "untimed before each step" % (y0.nbytes / 1e9),
-                           "mechanism": mech},
+                           "mechanism": mech, "jacobian": args.jac},
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": N * world / (e2e_total / args.steps * 1e-3), "unit": UNIT,
                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(y0.nbytes)},

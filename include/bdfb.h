@@ -161,6 +161,19 @@ int bdfb_set_comm(bdfb_batch *b, const void *nccl_unique_id, int32_t nranks, int
  * Returns BDFB_EINVAL for an unknown id, BDFB_ENOMEM.                       */
 int bdfb_set_kernel(bdfb_batch *b, int32_t kernel);
 
+/* Jacobian of the Newton matrix M = I - gamma J:
+ * BDFB_JAC_ANALYTIC (default; the paper's approaches 2A/2B) or
+ * BDFB_JAC_DQ, CVODE's difference-quotient dense Jacobian (approaches 3A/3B,
+ * P:399-401): column j from f(t, y + inc_j e_j) with inc_j = max(sqrt(u)|y_j|,
+ * minInc/ewt_j), minInc = 1000 |h| u n ||f||_WRMS -- n extra RHS evaluations
+ * per Jacobian (not counted in nfe, as in CVODE).  DQ is available for the
+ * mechanism models with the SPLIT kernel in per-cell mode (else
+ * BDFB_EUNSUPPORTED); BDFB_EINVAL for an unknown mode.  Call after
+ * bdfb_set_model / bdfb_set_kernel.                                         */
+#define BDFB_JAC_ANALYTIC 0
+#define BDFB_JAC_DQ 1
+int bdfb_set_jacobian(bdfb_batch *b, int32_t mode);
+
 /* The lane-group size G whose WRMS summation order (reading R15: lane l sums
  * components i = l (mod G) in increasing i, then an xor butterfly G/2..1)
  * the selected model/kernel uses; 1 = plain sequential sum.  0 if no model

@@ -116,6 +116,10 @@ class Batch:
                "split": L.KERNEL_SPLIT}[kernel]
         _check(self._L.bdfb_set_kernel(self.h, kid), self.h)
 
+    def set_jacobian(self, mode):
+        """"analytic" (default) or "dq": CVODE's difference-quotient dense Jacobian (bdfb_set_jacobian)."""
+        _check(self._L.bdfb_set_jacobian(self.h, {"analytic": 0, "dq": 1}[mode]), self.h)
+
     @property
     def wrms_group(self):
         """Lane-group size of the WRMS summation order (reading R15) the selected kernel uses."""

@@ -21,7 +21,7 @@ SYMBOLS = ["bdfb_default_options", "bdfb_create", "bdfb_set_model", "bdfb_set_ce
            "bdfb_integrate_host", "bdfb_get_stats", "bdfb_last_launch_count", "bdfb_last_kernel_ms",
            "bdfb_destroy", "bdfb_last_error", "bdfb_version", "bdfb_eval_rhs", "bdfb_eval_jac",
            "bdfb_lu_factor_solve", "bdfb_probe_fp64", "bdfb_set_comm", "bdfb_set_kernel", "bdfb_wrms_group",
-           "bdfb_phase_ms", "bdfb_minmax", "bdfb_set_atol_typical"]
+           "bdfb_phase_ms", "bdfb_minmax", "bdfb_set_atol_typical", "bdfb_set_jacobian"]
 
 
 class Options(C.Structure):
@@ -78,6 +78,8 @@ def lib():
     L.bdfb_get_stats.argtypes = [vp, C.POINTER(Stats)]
     L.bdfb_last_launch_count.restype = i32
     L.bdfb_last_launch_count.argtypes = [vp]
+    L.bdfb_set_jacobian.restype = C.c_int
+    L.bdfb_set_jacobian.argtypes = [vp, i32]
     L.bdfb_minmax.restype = C.c_int
     L.bdfb_minmax.argtypes = [vp, vp, i32, vp, vp, vp]
     L.bdfb_set_atol_typical.restype = C.c_int

@@ -88,6 +88,7 @@ struct SplitBufs {
   unsigned* cnt;               // [3 (it & 1) + {0, 1, 2}]: setup, Jacobian, K_init list counts of iteration it
   unsigned long long* live;    // [2]: live slots after the K_ctl of iteration it (it & 1)
   long long slots;             // S (multiple of 32)
+  int jac_dq;                  // 1: difference-quotient Jacobian (K_dqjac) instead of the analytic one
 };
 
 template <class Mech, class GM>
@@ -509,6 +510,55 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_kernel(SplitBufs b
     }
     if (g.lane == 0) t->coop = r;
     g.sync();
+  }
+}
+
+// ------------------------------------------------------------------ K_dqjac
+// Difference-quotient Jacobian (CVODE's cvLsDenseDQJac, the paper's approaches 3A/3B; SURVEY row
+// f1), one thread per (Jacobian-list entry, column j): the cell's J is evaluated at yq = zn[0] with
+// fy = the consumed RHS value (fr row); srur = sqrt(u), fnorm = ||fy||_WRMS (sequential, R15 G = 1),
+// minInc = 1000 |h| u n fnorm (1 if fnorm = 0), inc = max(srur |y_j|, minInc / ewt_j),
+// J(:, j) = (1/inc) f(y + inc e_j) + (-(1/inc)) fy, f = the generated RHS + F -- the oracle's orc_jac_dq
+// operation for operation.  An RHS failure marks the cell (TS.coop = 1: a recoverable setup failure).
+template <class Mech, class GM>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, 3) split_dqjac_kernel(SplitBufs b, int it) {
+  using SP = Split<Mech, GM>;
+  constexpr int N = Mech::N;
+  const long long cnt = (long long)b.cnt[3 * (it & 1) + 1] * N, stride = (long long)gridDim.x * BDFB_SPLIT_BLOCK;
+  for (long long t = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; t < cnt; t += stride) {
+    const long long e = t / N;
+    const int j = (int)(t - e * N);
+    const long long slot = b.jlist[e];
+    const typename SP::W w = SP::ws(b, slot);
+    TS* ts = SP::ts(b, slot);
+    double y[N], fy[N], ft[N];
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      y[i] = w.yq(i);
+      fy[i] = w.fr(i);
+      const double p = fy[i] * w.ewt(i);
+      acc = acc + p * p;
+    }
+    const double fnorm = sqrt(acc / (double)N);
+    const double minInc = (fnorm != 0.0) ? (1000.0 * fabs(ts->h) * UROUND * N * fnorm) : 1.0;
+    double yj = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (i == j) yj = y[i];
+    const double inc = fmax(sqrt(UROUND) * fabs(yj), minInc / w.ewt(j));
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (i == j) y[i] = yj + inc;
+    const int rv = Mech::rhs(y, ts->aux, ft);
+    if (rv) {
+      ts->coop = 1;
+      continue;
+    }
+    const double inc_inv = 1.0 / inc;
+    double* Jc = b.J + slot * SP::JREC + (long long)j * N;
+#pragma unroll
+    for (int i = 0; i < N; ++i) Jc[i] = inc_inv * (ft[i] + w.fext(i)) + (-inc_inv) * fy[i];
   }
 }
 

@@ -62,6 +62,7 @@ struct bdfb_batch {
   unsigned long long* h_live = nullptr;   // pinned: live-slot count read back per launch batch
   std::vector<cudaEvent_t> sev;           // split: per-phase timing events of one launch batch
   std::vector<cudaEvent_t> xev;           // split overlap: ordering events between the two streams
+  int jac_mode = BDFB_JAC_ANALYTIC;       // bdfb_set_jacobian
   cudaStream_t st2 = nullptr;             // split overlap: stream of K_jac + K_lu (BDFB_SPLIT_OVERLAP=1)
   double phase_ms[8] = {};                // split: device ms per phase of the last integrate
   int nphases = 0;
@@ -143,6 +144,7 @@ static int prepare_split(bdfb_batch* b) {
     }
     b->sb.slots = S;
   }
+  b->sb.jac_dq = b->jac_mode == BDFB_JAC_DQ ? 1 : 0;
   if (!b->h_live && cudaHostAlloc((void**)&b->h_live, sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess)
     return fail(b, BDFB_ENOMEM, "pinned live counter");
   b->sgeom = gm;
@@ -381,6 +383,16 @@ int bdfb_set_kernel(bdfb_batch* b, int32_t kernel) {
   return b->model >= 0 ? prepare_kernel(b) : BDFB_OK;
 }
 
+int bdfb_set_jacobian(bdfb_batch* b, int32_t mode) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (mode != BDFB_JAC_ANALYTIC && mode != BDFB_JAC_DQ) return fail(b, BDFB_EINVAL, "bad Jacobian mode");
+  if (mode == BDFB_JAC_DQ && !(use_split(b) && b->opt.mode == BDFB_MODE_PER_CELL))
+    return fail(b, BDFB_EUNSUPPORTED, "the difference-quotient Jacobian needs the SPLIT mechanism kernel");
+  b->jac_mode = mode;
+  b->sb.jac_dq = mode == BDFB_JAC_DQ ? 1 : 0;
+  return BDFB_OK;
+}
+
 int32_t bdfb_wrms_group(const bdfb_batch* b) {
   if (!b || b->model < 0) return 0;
   if (b->opt.mode == BDFB_MODE_GLOBAL_NORM) return b->model == BDFB_MODEL_MECH_H2 ? ModelH2::G : ModelDRM19::G;
@@ -545,6 +557,8 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
   const bool needs_aux = (b->model == BDFB_MODEL_NYX_KWH || b->model == BDFB_MODEL_MECH_H2 ||
                           b->model == BDFB_MODEL_MECH_DRM19);
   if (needs_aux && !aux) return fail(b, BDFB_EINVAL, "this model needs aux (density)");
+  if (b->jac_mode == BDFB_JAC_DQ && !(use_split(b) && b->opt.mode == BDFB_MODE_PER_CELL))
+    return fail(b, BDFB_EUNSUPPORTED, "the difference-quotient Jacobian needs the SPLIT mechanism kernel");
   cudaSetDevice(b->device);
   Opts o;
   o.rtol = b->rtol;

@@ -65,6 +65,7 @@ struct SplitK {
     unsigned gjac = (unsigned)((S * GM::G + blk - 1) / blk);
     if (gjac > (unsigned)gm.setup_grid) gjac = (unsigned)gm.setup_grid;
     const unsigned ginit = gs < (unsigned)gm.setup_grid ? gs : (unsigned)gm.setup_grid;   // grid-stride over the list
+    unsigned gdq = (unsigned)gm.rhs_grid;   // K_dqjac: grid-stride over (entry, column)
     unsigned glu = (unsigned)((S * OCT + blk - 1) / blk);
     if (glu > (unsigned)gm.setup_grid) glu = (unsigned)gm.setup_grid;
     unsigned grhs = (unsigned)gm.rhs_grid;
@@ -100,7 +101,10 @@ struct SplitK {
           ss = st2;
           if (events) cudaEventRecord(ev[5], st2);
         }
-        split_jac_kernel<Mech, GM><<<gjac, blk, jac_smem(), ss>>>(b, it);
+        if (b.jac_dq)
+          split_dqjac_kernel<Mech, GM><<<gdq, blk, 0, ss>>>(b, it);
+        else
+          split_jac_kernel<Mech, GM><<<gjac, blk, jac_smem(), ss>>>(b, it);
         if (events) cudaEventRecord(ev[2], ss);
         split_lu_kernel<Mech, GM><<<glu, blk, 0, ss>>>(b, it);
         if (events) cudaEventRecord(ev[3], ss);

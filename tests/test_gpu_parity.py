@@ -363,3 +363,43 @@ def test_integrate_with_typical_atol(oracle, name):
     yg = yd.cpu().numpy()
     tol = 10.0 * (1e-6 * np.abs(yo) + atol[:, None])
     assert np.all(np.abs(yg - yo) <= tol)
+
+
+# ------------------------------------------------------------------ difference-quotient Jacobian (row f1)
+@pytest.mark.parametrize("name", ["h2", "drm19"])
+def test_dq_jacobian_parity(oracle, name):
+    """SPLIT kernel with the difference-quotient Jacobian (bdfb_set_jacobian DQ; approaches 3A/3B)
+    vs the oracle's orc_jac_dq path on identical inputs: end states within 10 (rtol |y| + atol); and vs the
+    oracle's analytic-Jacobian run within 100 rtol (SPEC AC8)."""
+    mech, n = MECH[name]
+    y0, rho, F, prog = flame_field(mech, 16, dt=1e-5)
+    b = P.Batch(y0.shape[1], n, 1e-6, 1e-10)
+    b.set_model(name)
+    b.set_jacobian("dq")
+    cs = b.attach_cell_stats()
+    y = cu(y0)
+    b.integrate(0.0, 1e-5, y, f_ext=cu(F), aux=cu(rho))
+    st = b.stats()
+    assert st["n_failed"] == 0
+    yg = y.cpu().numpy()
+    m = oracle.Model.mechanism(mech)
+    yo, so = oracle.integrate_batch(m, y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho, fext_yc=F, group=b.wrms_group, threads=8,
+                                    ls=oracle.LS_DENSE_DQ)
+    end_state_check(yg, yo, 1e-6, 1e-10)
+    ya, _ = oracle.integrate_batch(m, y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho, fext_yc=F, group=b.wrms_group, threads=8)
+    assert np.all(np.abs(yg - ya) <= 100 * 1e-6 * np.abs(ya) + 1e-9)
+    same = np.mean([all(cs[k].cpu().numpy()[c] == so[k][c] for k in STAT_KEYS) for c in range(y0.shape[1])])
+    print(f"{name} DQ: identical per-cell stats vs the oracle's DQ run {same:.4f}")
+
+
+def test_dq_jacobian_unsupported_paths():
+    """DQ is offered only by the SPLIT mechanism kernel in per-cell mode."""
+    b = P.Batch(64, 10, 1e-6, 1e-10)
+    b.set_kernel("thread")
+    b.set_model("h2")
+    with pytest.raises(RuntimeError):
+        b.set_jacobian("dq")
+    b2 = P.Batch(64, 3, 1e-6, 1e-10)
+    b2.set_model("robertson")
+    with pytest.raises(RuntimeError):
+        b2.set_jacobian("dq")
