@@ -191,8 +191,12 @@ int bdfb_set_cell_stats(bdfb_batch *b, const bdfb_cell_stats *cs);
  *  f_ext : device, N*n fp64 frozen forcing F (same layout), or NULL for 0.
  *  aux   : device, N fp64 per-cell auxiliary input (density for NYX_KWH and
  *          MECH_*), or NULL when the model needs none.
- * Per-cell mode enqueues asynchronously; results are valid when `stream`
- * completes.  Returns 0 on enqueue, < 0 on an argument or launch error.
+ * Per-cell mode with a persistent kernel (THREAD, GROUP, the small models)
+ * enqueues asynchronously; results are valid when `stream` completes.  The
+ * SPLIT kernel (the default for MECH_*) drives its kernel launches from the
+ * host in batches and returns when all cells are done (one 8-byte live-count
+ * read back per batch).  Returns 0 on success / enqueue, < 0 on an argument
+ * or launch error (BDFB_EUNSUPPORTED for a DQ Jacobian without SPLIT).
  * Failed cells are counted by bdfb_get_stats (they are not an error here).
  * Global-norm mode (group models only: MECH_H2, MECH_DRM19) runs the
  * integrator's control loop on the host and returns when done; its
