@@ -11,8 +11,8 @@ The reacting-cell states of the flame template are read from
 synth/data/<mech>_trajectory.npz, written once by synth/make_trajectories.py
 (which integrates a 0-D reactor with the CPU oracle only).
 """
-from .fields import (SEED_BASE, config_seed, flame_field, gaussian, nyx_field, robertson_field, splitmix64,
+from .fields import (SEED_BASE, autoignition_box, config_seed, flame_field, gaussian, nyx_field, robertson_field, splitmix64,
                      uniform)
 
-__all__ = ["SEED_BASE", "config_seed", "splitmix64", "uniform", "gaussian", "robertson_field", "nyx_field",
+__all__ = ["SEED_BASE", "autoignition_box", "config_seed", "splitmix64", "uniform", "gaussian", "robertson_field", "nyx_field",
            "flame_field"]

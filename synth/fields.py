@@ -209,3 +209,23 @@ def stratified_sample(prog, per_class, seed=0):
         u = uniform(seed, ix, 900 + j)
         out.append(ix[np.argsort(u)[:per_class]])
     return np.sort(np.concatenate(out))
+
+
+# ---------------------------------------------------------------- auto-ignition box
+AUTOIGNITION_T = {"h2_lidryer": (900.0, 1300.0), "drm19_class": (1200.0, 1700.0)}
+
+
+def autoignition_box(mech, L, cells=None):
+    """SURVEY §8(d).1 second workload (the paper's batched-solver test): a uniform fresh mixture at
+    1 atm with T rising linearly along x (H2: 900 -> 1300 K; CH4: 1200 -> 1700 K), so part of the domain
+    ignites within the step.  Returns (y [n, M] YC, rho [M]); no forcing."""
+    c_idx = np.arange(L ** 3) if cells is None else np.asarray(cells)
+    Yf, W, T_cold, T_u, rho_u = fresh_state(mech)
+    x, _, _ = grid_xyz(L, c_idx)
+    t0, t1 = AUTOIGNITION_T[mech]
+    T = t0 + (t1 - t0) * (x - 0.5 / L) / (1.0 - 1.0 / L)
+    y = np.empty((len(Yf) + 1, len(c_idx)))
+    y[:-1] = Yf[:, None]
+    y[-1] = T
+    rho = PATM / (RU * T * np.sum(Yf / W))
+    return y, rho

@@ -403,3 +403,23 @@ def test_dq_jacobian_unsupported_paths():
     b2.set_model("robertson")
     with pytest.raises(RuntimeError):
         b2.set_jacobian("dq")
+
+
+# ------------------------------------------------------------------ auto-ignition box
+@pytest.mark.parametrize("name,dt", [("h2", 1e-4), ("drm19", 1e-3)])
+def test_autoignition_box_parity(oracle, name, dt):
+    """The paper's batched-solver test workload: a uniform mixture with T rising along x, so part of the
+    domain ignites within the step (the stiffest cells of the batch): SPLIT kernel vs the oracle within
+    10 (rtol |y| + atol) per cell and component, identical statuses, sum_k Y_k conserved on both sides."""
+    from synth import autoignition_box
+    mech, n = MECH[name]
+    y0, rho = autoignition_box(mech, 16)
+    yg, sg, st = run_gpu(name, n, y0, dt, 1e-6, 1e-10, rho=rho)
+    yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, dt, 1e-6, 1e-10, rho=rho,
+                                    group=st["group"], threads=8)
+    assert np.array_equal(sg["status"], so["status"]) and st["n_failed"] == 0
+    end_state_check(yg, yo, 1e-6, 1e-10)
+    rise = yg[-1] - y0[-1]
+    assert np.mean(rise > 100.0) > 0.05 and np.mean(rise < 100.0) > 0.05, "the step must straddle ignition"
+    s0 = y0[:-1].sum(axis=0)
+    assert np.abs(yg[:-1].sum(axis=0) - s0).max() <= 1e-12 and np.abs(yo[:-1].sum(axis=0) - s0).max() <= 1e-12
