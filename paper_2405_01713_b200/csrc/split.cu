@@ -70,6 +70,8 @@ struct SplitK {
     if (glu > (unsigned)gm.setup_grid) glu = (unsigned)gm.setup_grid;
     unsigned grhs = (unsigned)gm.rhs_grid;
     if (grhs > gs) grhs = gs;
+    if (const char* g = getenv("BDFB_SPLIT_RHS_FULLGRID"))   // experiments: one thread per slot
+      if (atoi(g) == 1) grhs = gs;
     size_t sm = ctl_smem();
     if (const char* pad = getenv("BDFB_SPLIT_CTL_SMEM")) {  // experiments: cap the resident K_ctl blocks
       const size_t want = (size_t)strtoul(pad, nullptr, 10);
