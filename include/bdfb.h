@@ -82,10 +82,11 @@ extern "C" {
                                   per-thread-slot device workspace (csrc/bdf_tpc.cuh)    */
 #define BDFB_KERNEL_GROUP 2    /* one cell per group of 16/32 lanes, state in shared
                                   memory (csrc/bdf_group.cuh; round-1 design)           */
-#define BDFB_KERNEL_SPLIT 3    /* slot pool in HBM, two kernels per trip: group-per-cell
-                                  control (Newton, LU, error test, step/order) and
-                                  thread-per-cell generated RHS (csrc/bdf_split.cuh);
-                                  bdfb_integrate is synchronous (host launch loop)      */
+#define BDFB_KERNEL_SPLIT 3    /* slot pool in HBM, four kernels per trip: thread-per-cell
+                                  control + Newton solve (K_ctl), group Jacobian (K_jac),
+                                  8-lane LU (K_lu), thread-per-cell generated RHS (K_rhs)
+                                  (csrc/bdf_split.cuh); bdfb_integrate is synchronous:
+                                  a host launch loop, one live-count readback per 16 trips */
 
 typedef struct bdfb_batch bdfb_batch;
 
@@ -271,7 +272,8 @@ const char *bdfb_version(void);
  * They run the SAME device functions the integrator uses.                  */
 
 /* f = R(t, y) + F for every cell (YC layout).  status: device int32[N] or
- * NULL (0 = ok, 1 = recoverable RHS failure).                              */
+ * NULL (0 = ok, 1 = recoverable RHS failure).  BDFB_EINVAL if the model
+ * needs aux (NYX_KWH, MECH_*) and aux is NULL (also for bdfb_eval_jac).     */
 int bdfb_eval_rhs(bdfb_batch *b, double t, const double *y, const double *f_ext,
                   const double *aux, double *f, int32_t *status, void *stream);
 
@@ -290,6 +292,16 @@ int bdfb_eval_jac(bdfb_batch *b, double t, const double *y, const double *aux, d
  * info[c] (device int32: 0, or k+1 when pivot k is exactly zero).           */
 int bdfb_lu_factor_solve(int32_t n, int64_t N, double *M, int32_t *piv, double *b,
                          int32_t *info, void *stream);
+
+/* The SAME batched LU factor + solve as the default SPLIT integrator's hot
+ * path (listing LU_FACTOR / LU_SOLVE; reading R16): oct_factor
+ * (8 lanes per cell, rows in registers, as the K_lu kernel) into K_lu's
+ * column-major record, then the thread-level forward/back substitutions of
+ * K_ctl's Newton solve.  Arguments and layouts as bdfb_lu_factor_solve;
+ * n in {2, 4, 6, 8, 10, 12, 16, 22, 32} (else BDFB_EUNSUPPORTED).  Uses
+ * stream-ordered device scratch (N records) for the duration of the call.   */
+int bdfb_split_lu_factor_solve(int32_t n, int64_t N, double *M, int32_t *piv, double *b,
+                               int32_t *info, void *stream);
 
 /* FP64 roofline probe: runs a DFMA-throughput kernel (all SMs, 8 independent
  * chains per thread) for about `ms` milliseconds on `device` and returns the

@@ -136,6 +136,14 @@ double orc_root(double x, int L)
   return ldexp(t * ROOT_C[L][r], k);
 }
 
+/* x^(1/L) as the step-size controller uses it: plain mode (o->plain) calls
+ * libm pow(x, 1.0/L) exactly as CVODE does; otherwise the fixed IEEE
+ * sequence of reading R25 (bit-reproducible on the GPU). */
+static double eta_root(int plain, double x, int L)
+{
+  return plain ? pow(x, 1.0 / L) : orc_root(x, L);
+}
+
 /* WRMS norm (Eq. 3).  Global mode: N = nt (reading R14) and the batch sum is
  * formed in a specified order (reading R15): per-cell sums in the group order,
  * accumulated sequentially over blocks of ORC_GBLK consecutive cells, block
@@ -413,7 +421,10 @@ static int lsolve(cell *c, double *b)
 {
   int n = c->n;
   if (c->o->ls != ORC_LS_DIAG) {
-    for (long k = 0; k < c->ncell; ++k) orc_lu_solve(n, c->M + k * n * n, c->piv + k * n, b + k * n);
+    for (long k = 0; k < c->ncell; ++k) {
+      if (c->o->plain) orc_lu_solve_div(n, c->M + k * n * n, c->piv + k * n, b + k * n);
+      else orc_lu_solve(n, c->M + k * n * n, c->piv + k * n, b + k * n);
+    }
     if (c->gamrat != 1.0) {
       double s = 2.0 / (1.0 + c->gamrat);
       for (long i = 0; i < c->nt; ++i) b[i] = s * b[i];
@@ -489,68 +500,85 @@ static int newton(cell *c, int nflag)
   }
 }
 
-/* SET_ETA (cvSetEta) */
-static void set_eta(cell *c)
+/* SET_ETA (cvSetEta): eta < THRESH keeps h; else cap by etamax and hmax */
+static double set_eta_scalar(double eta, double etamax, double h, double hmax, double *hprime)
 {
-  if (c->eta < THRESH) {
-    c->eta = 1.0;
-    c->hprime = c->h;
-  } else {
-    c->eta = fmin(c->eta, c->etamax);
-    if (c->o->hmax > 0.0) c->eta = c->eta / fmax(1.0, fabs(c->h) * c->eta / c->o->hmax);
-    c->hprime = c->h * c->eta;
+  if (eta < THRESH) {
+    *hprime = h;
+    return 1.0;
   }
+  eta = fmin(eta, etamax);
+  if (hmax > 0.0) eta = eta / fmax(1.0, fabs(h) * eta / hmax);
+  *hprime = h * eta;
+  return eta;
 }
 
-/* PREPARE_NEXT (cvPrepareNextStep + cvChooseEta) */
+/* PREPARE_NEXT scalar part (cvPrepareNextStep + cvChooseEta + cvSetEta),
+ * exported for the controller pins.  in/out *qwait; dsm = ||LTE|| at order q;
+ * ddn = ||zn[q]|| tq[1] (used iff q > 1), dup = ||acor - c zn[qmax]|| tq[3]
+ * (used iff have_up); both only consulted when *qwait == 0.  Returns eta,
+ * sets *qprime and *hprime.  Tie-break (reading R8): q, then q-1, then q+1. */
+double orc_choose_eta(int q, int *qwait, double etamax, double h, double hmax, double dsm, double ddn,
+                      int have_up, double dup, int plain, int *qprime, double *hprime)
+{
+  const int L = q + 1;
+  if (etamax == 1.0) {
+    *qwait = *qwait > 2 ? *qwait : 2;
+    *qprime = q;
+    *hprime = h;
+    return 1.0;
+  }
+  double etaq = 1.0 / (eta_root(plain, BIAS2 * dsm, L) + ADDON);
+  if (*qwait != 0) {
+    *qprime = q;
+    return set_eta_scalar(etaq, etamax, h, hmax, hprime);
+  }
+  *qwait = 2;
+  double etaqm1 = 0.0, etaqp1 = 0.0;
+  if (q > 1) etaqm1 = 1.0 / (eta_root(plain, BIAS1 * ddn, q) + ADDON);
+  if (have_up) etaqp1 = 1.0 / (eta_root(plain, BIAS3 * dup, L + 1) + ADDON);
+  double etam = fmax(etaqm1, fmax(etaq, etaqp1));
+  double eta;
+  if (etam < THRESH) {
+    eta = 1.0;
+    *qprime = q;
+  } else if (etam == etaq) {
+    eta = etaq;
+    *qprime = q;
+  } else if (etam == etaqm1) {
+    eta = etaqm1;
+    *qprime = q - 1;
+  } else {
+    eta = etaqp1;
+    *qprime = q + 1;
+  }
+  return set_eta_scalar(eta, etamax, h, hmax, hprime);
+}
+
+/* PREPARE_NEXT (cvPrepareNextStep + cvChooseEta): the two extra norms, then
+ * the scalar choice above; zn[qmax] = acor when the order is raised. */
 static void prepare_next(cell *c, double dsm)
 {
   long n = c->nt;
-  if (c->etamax == 1.0) {
-    c->qwait = c->qwait > 2 ? c->qwait : 2;
-    c->qprime = c->q;
-    c->hprime = c->h;
-    c->eta = 1.0;
-    return;
+  double ddn = 0.0, dup = 0.0;
+  int have_up = 0;
+  if (c->etamax != 1.0 && c->qwait == 0) {
+    if (c->q > 1) ddn = wrms(c, c->zn[c->q]) * c->tq[1];
+    if (c->q != c->qmax && c->saved_tq5 != 0.0) {
+      double hr = c->h / c->tau[2];
+      double pw = 1.0;
+      for (int k = 0; k < c->L; ++k) pw = pw * hr;
+      double cquot = (c->tq[5] / c->saved_tq5) * pw;
+      for (long i = 0; i < n; ++i) c->tmp[i] = -cquot * c->zn[c->qmax][i] + c->acor[i];
+      dup = wrms(c, c->tmp) * c->tq[3];
+      have_up = 1;
+    }
   }
-  double etaq = 1.0 / (orc_root(BIAS2 * dsm, c->L) + ADDON);
-  if (c->qwait != 0) {
-    c->eta = etaq;
-    c->qprime = c->q;
-    set_eta(c);
-    return;
-  }
-  c->qwait = 2;
-  double etaqm1 = 0.0, etaqp1 = 0.0;
-  if (c->q > 1) {
-    double ddn = wrms(c, c->zn[c->q]) * c->tq[1];
-    etaqm1 = 1.0 / (orc_root(BIAS1 * ddn, c->q) + ADDON);
-  }
-  if (c->q != c->qmax && c->saved_tq5 != 0.0) {
-    double hr = c->h / c->tau[2];
-    double pw = 1.0;
-    for (int k = 0; k < c->L; ++k) pw = pw * hr;
-    double cquot = (c->tq[5] / c->saved_tq5) * pw;
-    for (long i = 0; i < n; ++i) c->tmp[i] = -cquot * c->zn[c->qmax][i] + c->acor[i];
-    double dup = wrms(c, c->tmp) * c->tq[3];
-    etaqp1 = 1.0 / (orc_root(BIAS3 * dup, c->L + 1) + ADDON);
-  }
-  double etam = fmax(etaqm1, fmax(etaq, etaqp1));
-  if (etam < THRESH) {
-    c->eta = 1.0;
-    c->qprime = c->q;
-  } else if (etam == etaq) {
-    c->eta = etaq;
-    c->qprime = c->q;
-  } else if (etam == etaqm1) {
-    c->eta = etaqm1;
-    c->qprime = c->q - 1;
-  } else {
-    c->eta = etaqp1;
-    c->qprime = c->q + 1;
+  int q0 = c->q;
+  c->eta = orc_choose_eta(c->q, &c->qwait, c->etamax, c->h, c->o->hmax, dsm, ddn, have_up, dup, c->o->plain,
+                          &c->qprime, &c->hprime);
+  if (c->qprime == q0 + 1)
     for (long i = 0; i < n; ++i) c->zn[c->qmax][i] = c->acor[i];
-  }
-  set_eta(c);
 }
 
 /* cvHin: initial step estimate (reading R9) */
@@ -658,7 +686,7 @@ static int step(cell *c, double tf)
     if (fabs(c->h) <= c->o->hmin * (1.0 + UROUND) || nef == MXNEF) return ORC_ERR_FAILURE;
     c->etamax = 1.0;
     if (nef <= MXNEF1) {
-      c->eta = 1.0 / (orc_root(BIAS2 * dsm, c->L) + ADDON);
+      c->eta = 1.0 / (eta_root(c->o->plain, BIAS2 * dsm, c->L) + ADDON);
       c->eta = fmax(ETAMIN, fmax(c->eta, c->o->hmin / fabs(c->h)));
       if (nef >= SMALL_NEF) c->eta = fmin(c->eta, ETAMXF);
       rescale(c);
@@ -784,6 +812,49 @@ int orc_integrate(const orc_problem *p, const orc_opts *o, double t0, double tf,
   run(c, t0, tf, y, tr);
   *st = c->st;
   return c->st.status;
+}
+
+/* One NEWTON solve of the listing on a given predicted state, for the
+ * Newton replay pin: nst = 0, so the matrix is set up and J
+ * evaluated at y = zn0 (ycor = 0), gamma = h rl1, gamrat = 1, R = 1,
+ * tol = the caller's (tq[4]).  Outputs acor (= ycor at convergence), acnrm,
+ * the number of Newton iterations and RHS evaluations.  Returns 0 (converged),
+ * 1 (recoverable failure) or 2 (unrecoverable RHS failure).               */
+int orc_newton_once(const orc_problem *p, const orc_opts *o, double tn, double h, double rl1, double tol,
+                    const double *zn0, const double *zn1, const double *ewt, double *acor, double *acnrm,
+                    int *nni, int *nfe)
+{
+  cellbuf B;
+  cell C;
+  cell *c = &C;
+  memset(c, 0, sizeof(*c));
+  memset(&B, 0, sizeof(B));
+  c->p = p; c->o = o; c->n = p->n;
+  c->ncell = 1; c->nt = p->n; c->global = 0;
+  c->qmax = ORC_QMAX;
+  for (int j = 0; j <= ORC_QMAX; ++j) c->zn[j] = B.zn[j];
+  c->ewt = B.ewt; c->acor = B.acor; c->y = B.y; c->ftemp = B.ftemp; c->tmp = B.tmp;
+  c->ycor = B.ycor; c->G = B.G; c->J = B.J; c->M = B.M; c->piv = B.piv; c->Minv = B.Minv;
+  for (int i = 0; i < c->n; ++i) {
+    c->zn[0][i] = zn0[i];
+    c->zn[1][i] = zn1[i];
+    c->ewt[i] = ewt[i];
+  }
+  c->tn = tn;
+  c->h = h;
+  c->q = 1;
+  c->rl1 = rl1;
+  c->gamma = h * rl1;
+  c->gammap = c->gamma;
+  c->gamrat = 1.0;
+  c->crate = 1.0;
+  c->tq[4] = tol;
+  int r = newton(c, FIRST_CALL);
+  for (int i = 0; i < c->n; ++i) acor[i] = c->acor[i];
+  *acnrm = c->acnrm;
+  *nni = c->st.nni;
+  *nfe = c->st.nfe;
+  return r;
 }
 
 /* Global-norm mode (listing "Global-norm variant"): the N cells

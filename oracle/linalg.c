@@ -103,6 +103,25 @@ void orc_lu_solve(int n, const double *LU, const int *piv, double *b)
   b[0] = b[0] * (1.0 / LU[0]);
 }
 
+/* LU_SOLVE exactly as the listing writes it (plain mode): b[k] /= U[k][k]
+ * (true division) instead of the multiplication by 1/U[k][k] of reading R16. */
+void orc_lu_solve_div(int n, const double *LU, const int *piv, double *b)
+{
+  for (int k = 0; k < n; ++k) {
+    int p = piv[k];
+    if (p != k) { double t = b[k]; b[k] = b[p]; b[p] = t; }
+  }
+  for (int k = 0; k < n - 1; ++k)
+    for (int i = k + 1; i < n; ++i)
+      b[i] = fma(-LU[i * n + k], b[k], b[i]);
+  for (int k = n - 1; k > 0; --k) {
+    b[k] = b[k] / LU[k * n + k];
+    for (int i = 0; i < k; ++i)
+      b[i] = fma(-LU[i * n + k], b[k], b[i]);
+  }
+  b[0] = b[0] / LU[0];
+}
+
 /* Eq. 7: typical value = midpoint of the component's range over the whole domain. */
 void orc_typical_values(int n, int64_t ncells, const double *y, double *tv)
 {

@@ -109,6 +109,10 @@ typedef struct {
   double hmin, hmax;     /* hmax <= 0 means infinity */
   int ls;                /* ORC_LS_DENSE | ORC_LS_DIAG | ORC_LS_DENSE_DQ */
   int group;             /* G: WRMS summation order emulation (R15); 1 = sequential */
+  int plain;             /* 1: the listing's plain arithmetic -- libm pow(x, 1.0/L) for the step-size
+                            factors and true division in LU_SOLVE -- instead of readings R25/R16 (the
+                            GPU's division-free root and reciprocal-multiply solve).  The GPU must match
+                            both modes within the end-state band; it is bit-identical to plain = 0 only. */
 } orc_opts;
 
 typedef struct {
@@ -145,6 +149,21 @@ void orc_atol_from_typical(int n, const double *tv, double eta, double floor_, d
 double orc_wrms_sum(int n, const double *v, const double *w, int group);
 int orc_lu_factor(int n, double *M /* row-major n*n, in/out */, int *piv);
 void orc_lu_solve(int n, const double *LU, const int *piv, double *b);
+/* the listing's LU_SOLVE with true division b[k] /= U[k][k] (plain mode) */
+void orc_lu_solve_div(int n, const double *LU, const int *piv, double *b);
+
+/* PREPARE_NEXT scalar part (cvChooseEta + cvSetEta) for the controller pins:
+ * q, *qwait (in/out), etamax, h, hmax (<= 0: none), dsm = ||LTE||, ddn =
+ * ||zn[q]|| tq[1] (q > 1), dup = ||acor - c zn[qmax]|| tq[3] (iff have_up),
+ * plain: pow instead of R25.  Returns eta; sets *qprime, *hprime.          */
+double orc_choose_eta(int q, int *qwait, double etamax, double h, double hmax, double dsm, double ddn,
+                      int have_up, double dup, int plain, int *qprime, double *hprime);
+
+/* One Newton solve of the listing (forced matrix setup with J at zn0) for
+ * the Newton replay pin; see bdf.c.  Returns 0 / 1 (recoverable) / 2.      */
+int orc_newton_once(const orc_problem *p, const orc_opts *o, double tn, double h, double rl1, double tol,
+                    const double *zn0, const double *zn1, const double *ewt, double *acor, double *acnrm,
+                    int *nni, int *nfe);
 
 /* f = R(t,y) + f_ext.  Returns 0, or >0 for a recoverable RHS failure. */
 int orc_rhs(const orc_problem *p, double t, const double *y, double *f);

@@ -58,7 +58,7 @@ class Problem(C.Structure):
 class Opts(C.Structure):
     _fields_ = [("rtol", C.c_double), ("atol", C.POINTER(C.c_double)), ("qmax", C.c_int),
                 ("mxstep", C.c_int64), ("h0", C.c_double), ("hmin", C.c_double), ("hmax", C.c_double),
-                ("ls", C.c_int), ("group", C.c_int)]
+                ("ls", C.c_int), ("group", C.c_int), ("plain", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -98,6 +98,16 @@ def lib():
             L.orc_lu_factor.argtypes = [C.c_int, dp, ip]
             L.orc_lu_solve.restype = None
             L.orc_lu_solve.argtypes = [C.c_int, dp, ip, dp]
+            L.orc_lu_solve_div.restype = None
+            L.orc_lu_solve_div.argtypes = [C.c_int, dp, ip, dp]
+            L.orc_choose_eta.restype = C.c_double
+            L.orc_choose_eta.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_double, C.c_double, C.c_double,
+                                         C.c_double, C.c_double, C.c_int, C.c_double, C.c_int,
+                                         C.POINTER(C.c_int), dp]
+            L.orc_newton_once.restype = C.c_int
+            L.orc_newton_once.argtypes = [C.POINTER(Problem), C.POINTER(Opts), C.c_double, C.c_double,
+                                          C.c_double, C.c_double, dp, dp, dp, dp, dp, C.POINTER(C.c_int),
+                                          C.POINTER(C.c_int)]
             L.orc_rhs.restype = C.c_int
             L.orc_rhs.argtypes = [C.POINTER(Problem), C.c_double, dp, dp]
             L.orc_rhs_scale.restype = C.c_int
@@ -163,12 +173,40 @@ def lu_factor(M):
     return M, piv, info
 
 
-def lu_solve(LU, piv, b):
+def lu_solve(LU, piv, b, plain=False):
+    """LU_SOLVE: reciprocal-multiply back substitution (R16), or true division when plain."""
     LU = np.ascontiguousarray(LU, dtype=np.float64)
     piv = np.ascontiguousarray(piv, dtype=np.int32)
     b = np.array(b, dtype=np.float64, copy=True)
-    lib().orc_lu_solve(LU.shape[0], _dp(LU), _ip(piv), _dp(b))
+    (lib().orc_lu_solve_div if plain else lib().orc_lu_solve)(LU.shape[0], _dp(LU), _ip(piv), _dp(b))
     return b
+
+
+def choose_eta(q, qwait, dsm, ddn=0.0, dup=None, etamax=10.0, h=1.0, hmax=0.0, plain=False):
+    """PREPARE_NEXT scalar part (orc_choose_eta): returns (eta, qprime, hprime, qwait_out)."""
+    qw = C.c_int(int(qwait))
+    qp = C.c_int(0)
+    hp = C.c_double(0.0)
+    eta = lib().orc_choose_eta(int(q), C.byref(qw), float(etamax), float(h), float(hmax), float(dsm), float(ddn),
+                               0 if dup is None else 1, 0.0 if dup is None else float(dup), int(plain),
+                               C.byref(qp), C.byref(hp))
+    return eta, qp.value, hp.value, qw.value
+
+
+def newton_once(model, zn0, zn1, ewt, h, rl1, tol, rho=1.0, fext=None, tn=0.0, atol=1e-10, rtol=1e-6):
+    """One NEWTON solve of the listing with a forced matrix setup (orc_newton_once).
+    Returns (status, acor, acnrm, nni, nfe)."""
+    zn0 = np.ascontiguousarray(zn0, dtype=np.float64)
+    zn1 = np.ascontiguousarray(zn1, dtype=np.float64)
+    ewt = np.ascontiguousarray(ewt, dtype=np.float64)
+    p = model.problem(rho, fext)
+    o = make_opts(model.n, rtol, atol, ls=LS_DENSE)
+    acor = np.zeros(model.n)
+    acn = C.c_double(0.0)
+    nni, nfe = C.c_int(0), C.c_int(0)
+    r = lib().orc_newton_once(C.byref(p), C.byref(o), float(tn), float(h), float(rl1), float(tol), _dp(zn0),
+                              _dp(zn1), _dp(ewt), _dp(acor), C.byref(acn), C.byref(nni), C.byref(nfe))
+    return r, acor, acn.value, nni.value, nfe.value
 
 
 def root(x, L):
@@ -357,9 +395,11 @@ def kwh_state(model, e, rho):
     return dict(zip(["T", "nH0", "nHp", "nHe0", "nHep", "nHepp", "ne", "g"], out)), r
 
 
-def make_opts(n, rtol, atol, qmax=5, mxstep=10000, h0=0.0, hmin=0.0, hmax=0.0, ls=LS_DENSE, group=1):
+def make_opts(n, rtol, atol, qmax=5, mxstep=10000, h0=0.0, hmin=0.0, hmax=0.0, ls=LS_DENSE, group=1, plain=False):
+    """plain=True: the listing's plain arithmetic (libm pow roots, true division in LU_SOLVE) instead of
+    readings R25/R16 -- the CUDA path must match both within the end-state band."""
     at = np.ascontiguousarray(np.broadcast_to(np.asarray(atol, dtype=np.float64), (n,)))
-    o = Opts(rtol, _dp(at), qmax, mxstep, h0, hmin, hmax, ls, group)
+    o = Opts(rtol, _dp(at), qmax, mxstep, h0, hmin, hmax, ls, group, 1 if plain else 0)
     o._keep = at
     return o
 

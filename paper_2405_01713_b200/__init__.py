@@ -58,11 +58,50 @@ def _ptr(t):
     raise TypeError(f"unsupported buffer {type(t)}")
 
 
-def _stream(stream):
+def _dev(t, batch, numel, name, dtype="f64", optional=True):
+    """Validated device pointer for the C ABI (which takes no lengths): a contiguous CUDA tensor on the
+    batch's device with the expected dtype and element count; None passes through when optional."""
+    import torch
+    if t is None:
+        if optional:
+            return None
+        raise ValueError(f"{name} is required")
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.device.index != batch.device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the batch on cuda:{batch.device}")
+    want = {"f64": torch.float64, "i32": torch.int32}[dtype]
+    if t.dtype != want:
+        raise TypeError(f"{name} must be {want}, got {t.dtype}")
+    if t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _host(a, numel, name, optional=True):
+    """Validated host buffer (numpy float64 or CPU tensor) of numel elements."""
+    if a is None:
+        if optional:
+            return None
+        raise ValueError(f"{name} is required")
+    if hasattr(a, "data_ptr"):
+        import torch
+        if a.is_cuda or a.dtype != torch.float64 or a.numel() != numel or not a.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous CPU float64 tensor of {numel} elements")
+        return C.c_void_p(a.data_ptr())
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.size != numel or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{name} must be a C-contiguous float64 array of {numel} elements")
+    return C.c_void_p(a.ctypes.data)
+
+
+def _stream(stream, device=None):
+    """The caller's stream; default: torch's current stream on `device` (the batch's device)."""
     if stream is None:
         import torch
         if torch.cuda.is_available():
-            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+            return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
         return None
     if hasattr(stream, "cuda_stream"):
         return C.c_void_p(stream.cuda_stream)
@@ -156,14 +195,18 @@ class Batch:
     def integrate(self, t0, tf, y, f_ext=None, aux=None, layout="YC", stream=None):
         """Advance every cell from t0 to tf in place (y: device fp64, [n, N] for YC or [N, n] for CY)."""
         lay = L.LAYOUT_YC if layout == "YC" else L.LAYOUT_CY
-        _check(self._L.bdfb_integrate(self.h, float(t0), float(tf), _ptr(y), _ptr(f_ext), _ptr(aux), lay,
-                                      _stream(stream)), self.h)
+        nn = self.n * self.n_cells
+        _check(self._L.bdfb_integrate(self.h, float(t0), float(tf), _dev(y, self, nn, "y", optional=False),
+                                      _dev(f_ext, self, nn, "f_ext"), _dev(aux, self, self.n_cells, "aux"), lay,
+                                      _stream(stream, self.device)), self.h)
 
     def integrate_host(self, t0, tf, y, f_ext=None, aux=None, layout="YC", stream=None):
         """End-to-end: host (preferably pinned) buffers in, y copied back; synchronous."""
         lay = L.LAYOUT_YC if layout == "YC" else L.LAYOUT_CY
-        _check(self._L.bdfb_integrate_host(self.h, float(t0), float(tf), _ptr(y), _ptr(f_ext), _ptr(aux), lay,
-                                           _stream(stream)), self.h)
+        nn = self.n * self.n_cells
+        _check(self._L.bdfb_integrate_host(self.h, float(t0), float(tf), _host(y, nn, "y", optional=False),
+                                           _host(f_ext, nn, "f_ext"), _host(aux, self.n_cells, "aux"), lay,
+                                           _stream(stream, self.device)), self.h)
 
     def stats(self):
         s = L.Stats()
@@ -179,7 +222,8 @@ class Batch:
         lo = torch.empty(self.n, dtype=torch.float64, device=y.device)
         hi = torch.empty_like(lo)
         lay = L.LAYOUT_YC if layout == "YC" else L.LAYOUT_CY
-        _check(self._L.bdfb_minmax(self.h, _ptr(y), lay, _ptr(lo), _ptr(hi), _stream(stream)), self.h)
+        _check(self._L.bdfb_minmax(self.h, _dev(y, self, self.n * self.n_cells, "y", optional=False), lay, _ptr(lo),
+                                   _ptr(hi), _stream(stream, self.device)), self.h)
         return lo, hi
 
     def set_typical_atol(self, y, eta=1e-10, floor=1e-30, layout="YC", group=None, stream=None):
@@ -219,30 +263,38 @@ class Batch:
 def eval_rhs(batch, y, f_ext=None, aux=None, t=0.0, stream=None):
     """f = R(t, y) + F for every cell with the integrator's device RHS (YC layout)."""
     import torch
+    nn = batch.n * batch.n_cells
+    yp = _dev(y, batch, nn, "y", optional=False)
     f = torch.empty_like(y)
     st = torch.empty(batch.n_cells, dtype=torch.int32, device=y.device)
-    _check(batch._L.bdfb_eval_rhs(batch.h, float(t), _ptr(y), _ptr(f_ext), _ptr(aux), _ptr(f), _ptr(st),
-                                  _stream(stream)), batch.h)
+    _check(batch._L.bdfb_eval_rhs(batch.h, float(t), yp, _dev(f_ext, batch, nn, "f_ext"),
+                                  _dev(aux, batch, batch.n_cells, "aux"), _ptr(f), _ptr(st),
+                                  _stream(stream, batch.device)), batch.h)
     return f, st
 
 
 def eval_jac(batch, y, aux=None, t=0.0, stream=None):
     """J[i, j, c] = dR_i/dy_j of every cell with the integrator's device Jacobian."""
     import torch
+    yp = _dev(y, batch, batch.n * batch.n_cells, "y", optional=False)
     J = torch.empty((batch.n, batch.n, batch.n_cells), dtype=torch.float64, device=y.device)
-    _check(batch._L.bdfb_eval_jac(batch.h, float(t), _ptr(y), _ptr(aux), _ptr(J), _stream(stream)), batch.h)
+    _check(batch._L.bdfb_eval_jac(batch.h, float(t), yp, _dev(aux, batch, batch.n_cells, "aux"), _ptr(J),
+                                  _stream(stream, batch.device)), batch.h)
     return J
 
 
-def lu_factor_solve(M, b, stream=None):
+def lu_factor_solve(M, b, stream=None, routine="tpc"):
     """Batched LU with partial pivoting + solve: M [n, n, N], b [n, N] (cuda fp64).
-    Returns (LU, piv, x, info) with LAPACK getrf/getrs conventions."""
+    Returns (LU, piv, x, info) with LAPACK getrf/getrs conventions.
+    routine: "tpc" (bdfb_lu_factor_solve: the thread-per-cell / small-model routine) or "split"
+    (bdfb_split_lu_factor_solve: the default SPLIT integrator's oct_factor + Newton-solve substitutions)."""
     import torch
     n, N = b.shape
     LU = M.clone().contiguous()
     x = b.clone().contiguous()
     piv = torch.zeros((n, N), dtype=torch.int32, device=b.device)
     info = torch.zeros(N, dtype=torch.int32, device=b.device)
-    _check(L.lib().bdfb_lu_factor_solve(int(n), int(N), _ptr(LU), _ptr(piv), _ptr(x), _ptr(info),
+    fn = L.lib().bdfb_split_lu_factor_solve if routine == "split" else L.lib().bdfb_lu_factor_solve
+    _check(fn(int(n), int(N), _ptr(LU), _ptr(piv), _ptr(x), _ptr(info),
                                         _stream(stream)))
     return LU, piv, x, info

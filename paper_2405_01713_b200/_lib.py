@@ -21,7 +21,8 @@ SYMBOLS = ["bdfb_default_options", "bdfb_create", "bdfb_set_model", "bdfb_set_ce
            "bdfb_integrate_host", "bdfb_get_stats", "bdfb_last_launch_count", "bdfb_last_kernel_ms",
            "bdfb_destroy", "bdfb_last_error", "bdfb_version", "bdfb_eval_rhs", "bdfb_eval_jac",
            "bdfb_lu_factor_solve", "bdfb_probe_fp64", "bdfb_set_comm", "bdfb_set_kernel", "bdfb_wrms_group",
-           "bdfb_phase_ms", "bdfb_minmax", "bdfb_set_atol_typical", "bdfb_set_jacobian"]
+           "bdfb_phase_ms", "bdfb_minmax", "bdfb_set_atol_typical", "bdfb_set_jacobian",
+           "bdfb_split_lu_factor_solve"]
 
 
 class Options(C.Structure):
@@ -100,6 +101,8 @@ def lib():
     L.bdfb_eval_jac.argtypes = [vp, dp, vp, vp, vp, vp]
     L.bdfb_lu_factor_solve.restype = C.c_int
     L.bdfb_lu_factor_solve.argtypes = [i32, i64, vp, vp, vp, vp, vp]
+    L.bdfb_split_lu_factor_solve.restype = C.c_int
+    L.bdfb_split_lu_factor_solve.argtypes = [i32, i64, vp, vp, vp, vp, vp]
     L.bdfb_set_comm.restype = C.c_int
     L.bdfb_set_comm.argtypes = [vp, vp, i32, i32, i64]
     L.bdfb_set_kernel.restype = C.c_int

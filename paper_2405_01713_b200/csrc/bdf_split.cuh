@@ -91,6 +91,51 @@ struct SplitBufs {
   int jac_dq;                  // 1: difference-quotient Jacobian (K_dqjac) instead of the analytic one
 };
 
+// Substitutions of LU_SOLVE (listing; reading R16) on a column-major LU
+// record (factors in pivoted row order | 1/U_kk | perm), b already permuted:
+// unit-L forward substitution column by column, then the back substitution
+// with the reciprocal diagonal -- the operations and order of the oracle's
+// orc_lu_solve.  Shared by the Newton solve of K_ctl and the LU diagnostic.
+template <int N>
+__device__ __forceinline__ void lurec_substitute(const double* __restrict__ lu, double (&b)[N]) {
+  constexpr int LU_INVD = N * N;
+  const double2* col = reinterpret_cast<const double2*>(lu);
+#pragma unroll
+  for (int k = 0; k < N - 1; ++k) {           // unit-L forward substitution, column k
+    double c[N];
+#pragma unroll
+    for (int h = (k + 1) / 2; h < N / 2; ++h) {
+      const double2 v = col[(k * N) / 2 + h];
+      c[2 * h] = v.x;
+      c[2 * h + 1] = v.y;
+    }
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) b[i] = fma(-c[i], b[k], b[i]);
+  }
+  const double2* inv2 = reinterpret_cast<const double2*>(lu + LU_INVD);
+  double inv[N];
+#pragma unroll
+  for (int h = 0; h < N / 2; ++h) {
+    const double2 v = inv2[h];
+    inv[2 * h] = v.x;
+    inv[2 * h + 1] = v.y;
+  }
+#pragma unroll
+  for (int k = N - 1; k > 0; --k) {           // back substitution, column k, reciprocal diagonal
+    b[k] = b[k] * inv[k];
+    double c[N];
+#pragma unroll
+    for (int h = 0; h < (k + 1) / 2; ++h) {
+      const double2 v = col[(k * N) / 2 + h];
+      c[2 * h] = v.x;
+      c[2 * h + 1] = v.y;
+    }
+#pragma unroll
+    for (int i = 0; i < k; ++i) b[i] = fma(-c[i], b[k], b[i]);
+  }
+  b[0] = b[0] * inv[0];
+}
+
 template <class Mech, class GM>
 struct Split {
   static constexpr int N = Mech::N;
@@ -119,41 +164,7 @@ struct Split {
     const int* perm = reinterpret_cast<const int*>(lu + LU_PERM);
 #pragma unroll
     for (int i = 0; i < N; ++i) b[i] = -w.del(perm[i]);
-    const double2* col = reinterpret_cast<const double2*>(lu);
-#pragma unroll
-    for (int k = 0; k < N - 1; ++k) {           // unit-L forward substitution, column k
-      double c[N];
-#pragma unroll
-      for (int h = (k + 1) / 2; h < N / 2; ++h) {
-        const double2 v = col[(k * N) / 2 + h];
-        c[2 * h] = v.x;
-        c[2 * h + 1] = v.y;
-      }
-#pragma unroll
-      for (int i = k + 1; i < N; ++i) b[i] = fma(-c[i], b[k], b[i]);
-    }
-    const double2* inv2 = reinterpret_cast<const double2*>(lu + LU_INVD);
-    double inv[N];
-#pragma unroll
-    for (int h = 0; h < N / 2; ++h) {
-      const double2 v = inv2[h];
-      inv[2 * h] = v.x;
-      inv[2 * h + 1] = v.y;
-    }
-#pragma unroll
-    for (int k = N - 1; k > 0; --k) {           // back substitution, column k, reciprocal diagonal
-      b[k] = b[k] * inv[k];
-      double c[N];
-#pragma unroll
-      for (int h = 0; h < (k + 1) / 2; ++h) {
-        const double2 v = col[(k * N) / 2 + h];
-        c[2 * h] = v.x;
-        c[2 * h + 1] = v.y;
-      }
-#pragma unroll
-      for (int i = 0; i < k; ++i) b[i] = fma(-c[i], b[k], b[i]);
-    }
-    b[0] = b[0] * inv[0];
+    lurec_substitute<N>(lu, b);
     if (s.gamrat != 1.0) {
       const double sc = 2.0 / (1.0 + s.gamrat);
 #pragma unroll

@@ -1,10 +1,13 @@
 // bdfb.cu -- C ABI of libbdfb (declared and documented in include/bdfb.h).
 //
-// Owns the workspace (allocated once in bdfb_create), the model selection and
-// the launch configuration of the persistent per-cell integrator kernel
-// (bdf_cell.cuh).  No allocation, host round trip or synchronisation happens
-// inside bdfb_integrate: one kernel launch + two tiny memsets on the caller's
-// stream.
+// Owns the workspace (allocated once in bdfb_create / bdfb_set_model /
+// bdfb_set_kernel; never in bdfb_integrate), the model selection and the
+// launch configuration of the per-cell kernels.  The persistent kernels
+// (bdf_cell.cuh models, THREAD, GROUP) are one launch plus two tiny memsets
+// on the caller's stream; the default SPLIT organisation for the mechanism
+// models (split.cu) is a host-driven loop of 4 kernels per trip that reads
+// one live-slot count back every 16 trips and returns when every cell is
+// done; the global-norm mode is a host control loop (global_host.cuh).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -547,6 +550,11 @@ extern "C" int bdfb_set_comm(bdfb_batch* b, const void* nccl_unique_id, int32_t 
   return BDFB_OK;
 }
 
+// models whose RHS reads the per-cell aux input (density)
+static bool model_needs_aux(int model) {
+  return model == BDFB_MODEL_NYX_KWH || model == BDFB_MODEL_MECH_H2 || model == BDFB_MODEL_MECH_DRM19;
+}
+
 extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, const double* f_ext,
                               const double* aux, int32_t layout, void* stream) {
   if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
@@ -554,9 +562,7 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
   if (!y) return fail(b, BDFB_EINVAL, "y is NULL");
   if (!(tf > t0) || !isfinite(t0) || !isfinite(tf)) return fail(b, BDFB_EINVAL, "need finite tf > t0");
   if (layout != BDFB_LAYOUT_YC && layout != BDFB_LAYOUT_CY) return fail(b, BDFB_EINVAL, "bad layout");
-  const bool needs_aux = (b->model == BDFB_MODEL_NYX_KWH || b->model == BDFB_MODEL_MECH_H2 ||
-                          b->model == BDFB_MODEL_MECH_DRM19);
-  if (needs_aux && !aux) return fail(b, BDFB_EINVAL, "this model needs aux (density)");
+  if (model_needs_aux(b->model) && !aux) return fail(b, BDFB_EINVAL, "this model needs aux (density)");
   if (b->jac_mode == BDFB_JAC_DQ && !(use_split(b) && b->opt.mode == BDFB_MODE_PER_CELL))
     return fail(b, BDFB_EUNSUPPORTED, "the difference-quotient Jacobian needs the SPLIT mechanism kernel");
   cudaSetDevice(b->device);
@@ -773,6 +779,7 @@ extern "C" int bdfb_eval_rhs(bdfb_batch* b, double t, const double* y, const dou
   if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
   if (b->model < 0) return fail(b, BDFB_ENOMODEL, "bdfb_set_model not called");
   if (!y || !f) return fail(b, BDFB_EINVAL, "y/f NULL");
+  if (model_needs_aux(b->model) && !aux) return fail(b, BDFB_EINVAL, "this model needs aux (density)");
   cudaSetDevice(b->device);
   cudaStream_t st = (cudaStream_t)stream;
   switch (b->model) {
@@ -794,6 +801,7 @@ extern "C" int bdfb_eval_jac(bdfb_batch* b, double t, const double* y, const dou
   if (b->model < 0) return fail(b, BDFB_ENOMODEL, "bdfb_set_model not called");
   if (!y || !J) return fail(b, BDFB_EINVAL, "y/J NULL");
   if (b->model == BDFB_MODEL_NYX_KWH) return fail(b, BDFB_EUNSUPPORTED, "CVDiag model has no Jacobian");
+  if (model_needs_aux(b->model) && !aux) return fail(b, BDFB_EINVAL, "this model needs aux (density)");
   cudaSetDevice(b->device);
   cudaStream_t st = (cudaStream_t)stream;
   switch (b->model) {
@@ -907,6 +915,22 @@ extern "C" int bdfb_lu_factor_solve(int32_t n, int64_t N, double* M, int32_t* pi
 #undef LU_CASE
   }
   return fail(nullptr, BDFB_EUNSUPPORTED, "n not instantiated (1-8,10,12,16,22,32)");
+}
+
+extern "C" int bdfb_split_lu_factor_solve(int32_t n, int64_t N, double* M, int32_t* piv, double* b, int32_t* info,
+                                          void* stream) {
+  if (N < 1 || !M || !piv || !b || !info) return fail(nullptr, BDFB_EINVAL, "bad LU arguments");
+  if (!(n == 2 || n == 4 || n == 6 || n == 8 || n == 10 || n == 12 || n == 16 || n == 22 || n == 32))
+    return fail(nullptr, BDFB_EUNSUPPORTED, "n not instantiated for the SPLIT LU (2,4,6,8,10,12,16,22,32)");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* rec = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&rec, sizeof(double) * split_lu_rec_doubles(n) * (size_t)N, st);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMallocAsync (LU records)");
+  e = split_lu_diag(n, N, M, piv, b, info, rec, st);
+  cudaError_t e2 = cudaFreeAsync(rec, st);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "split LU diagnostic launch");
+  if (e2 != cudaSuccess) return cuda_fail(nullptr, e2, "cudaFreeAsync");
+  return BDFB_OK;
 }
 
 // ------------------------------------------------------------ FP64 probe

@@ -142,10 +142,90 @@ struct SplitK {
   }
 };
 
+// LU diagnostic: the SPLIT path's own factor/solve routines on identical inputs
+// (oct_factor, 8 lanes per cell, as K_lu; the record layout of K_lu; the
+// thread-level substitutions of K_ctl's Newton solve, lurec_substitute).
+// M[(i n + j) N + c] in, LAPACK getrf factors out (rows in pivoted order);
+// piv: getrf swap indices derived from the row permutation; b: solution.
+template <int NN>
+__global__ void __launch_bounds__(128) split_lu_diag_kernel(long long N, double* M, int* piv, double* b, int* info,
+                                                            double* rec) {
+  constexpr int R = (NN + OCT - 1) / OCT, LUREC = (NN * NN + NN + (NN + 1) / 2 + 3) / 4 * 4;
+  constexpr int LU_INVD = NN * NN, LU_PERM = NN * NN + NN;
+  const int lane = threadIdx.x & 31, gl = lane & (OCT - 1);
+  const unsigned gmask = 0xffu << (lane & ~(OCT - 1));
+  const long long c = ((long long)blockIdx.x * 128 + threadIdx.x) / OCT;
+  if (c >= N) return;                         // whole groups exit together (N is per group)
+  double* lu = rec + c * LUREC;
+  double a[R][NN];
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int r = gl + OCT * s;
+#pragma unroll
+    for (int j = 0; j < NN; ++j) a[s][j] = (r < NN) ? M[((long long)r * NN + j) * N + c] : 0.0;
+  }
+  int pos[R];
+  double dinv[R];
+  const int inf = oct_factor<NN>(gmask, gl, a, pos, dinv);
+  if (!inf) {
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int r = gl + OCT * s;
+      if (r < NN) {
+#pragma unroll
+        for (int j = 0; j < NN; ++j) lu[j * NN + pos[s]] = a[s][j];
+        lu[LU_INVD + pos[s]] = dinv[s];
+        reinterpret_cast<int*>(lu + LU_PERM)[pos[s]] = r;
+      }
+    }
+  }
+  __syncwarp(gmask);
+  if (gl != 0) return;
+  info[c] = inf;
+  if (inf) return;
+  const int* perm = reinterpret_cast<const int*>(lu + LU_PERM);
+  double x[NN];
+#pragma unroll
+  for (int i = 0; i < NN; ++i) x[i] = b[(long long)perm[i] * N + c];
+  lurec_substitute<NN>(lu, x);
+  for (int i = 0; i < NN; ++i) {
+    b[(long long)i * N + c] = x[i];
+    for (int j = 0; j < NN; ++j) M[((long long)i * NN + j) * N + c] = lu[j * NN + i];
+  }
+  // getrf swap sequence of the permutation: at step k the row perm[k] sits at position where[perm[k]]
+  int cur[NN], where[NN];
+  for (int i = 0; i < NN; ++i) cur[i] = where[i] = i;
+  for (int k = 0; k < NN; ++k) {
+    const int p = where[perm[k]];
+    piv[(long long)k * N + c] = p;
+    const int rk = cur[k], rp = cur[p];
+    cur[k] = rp;
+    cur[p] = rk;
+    where[rp] = k;
+    where[rk] = p;
+  }
+}
+
 using KH2 = SplitK<Tpc_h2_lidryer, ModelMech<mech_h2_lidryer::Traits>>;
 using KDRM = SplitK<Tpc_drm19_class, ModelMech<mech_drm19_class::Traits>>;
 
 }  // namespace
+
+cudaError_t split_lu_diag(int n, long long N, double* M, int* piv, double* b, int* info, double* rec,
+                          cudaStream_t st) {
+  const unsigned g = (unsigned)((N * OCT + 127) / 128);
+  switch (n) {
+#define BDFB_LU_DIAG(NN) \
+  case NN: split_lu_diag_kernel<NN><<<g, 128, 0, st>>>(N, M, piv, b, info, rec); break;
+    BDFB_LU_DIAG(2) BDFB_LU_DIAG(4) BDFB_LU_DIAG(6) BDFB_LU_DIAG(8) BDFB_LU_DIAG(10) BDFB_LU_DIAG(12)
+    BDFB_LU_DIAG(16) BDFB_LU_DIAG(22) BDFB_LU_DIAG(32)
+#undef BDFB_LU_DIAG
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+size_t split_lu_rec_doubles(int n) { return (size_t)((n * n + n + (n + 1) / 2 + 3) / 4 * 4); }
 
 cudaError_t split_geometry(int mech, int device, SplitGeom* gm) {
   switch (mech) {

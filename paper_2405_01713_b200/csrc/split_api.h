@@ -33,4 +33,11 @@ cudaError_t split_integrate(int mech, const Opts& o, double* y, const double* fe
                             cudaStream_t st, int* launches, cudaEvent_t* events, double* phase_ms,
                             cudaStream_t st2, cudaEvent_t* xev);
 
+// LU diagnostic with the SPLIT path's routines (oct_factor + the Newton
+// solve's substitutions); n in {2,4,6,8,10,12,16,22,32}; rec: N *
+// split_lu_rec_doubles(n) doubles of device scratch.
+cudaError_t split_lu_diag(int n, long long N, double* M, int* piv, double* b, int* info, double* rec,
+                          cudaStream_t st);
+size_t split_lu_rec_doubles(int n);
+
 }  // namespace bdfb

@@ -74,6 +74,36 @@ def test_lu_bit_identical(oracle, n):
         assert np.array_equal(x[:, c], oracle.lu_solve(LUo, pivo, b[:, c])), c
 
 
+@pytest.mark.parametrize("n", [2, 4, 8, 10, 16, 22, 32])
+def test_split_lu_bit_identical(oracle, n):
+    """The default SPLIT integrator's own LU (oct_factor, 8 lanes per cell, K_lu's record layout) and the
+    substitutions of its Newton solve (K_ctl) vs LU_FACTOR / LU_SOLVE: identical pivots, bit-identical
+    factors and solutions (reading R16), pivot ties and exact zero pivots included (north_star: LU solve
+    within 1e-12 on identical inputs; this is exact)."""
+    rng = np.random.default_rng(1000 + n)
+    N = 4096 + 29
+    M = rng.standard_normal((n, n, N)) * 10.0 ** rng.uniform(-3, 3, (n, 1, N))
+    b = rng.standard_normal((n, N))
+    M[:, :, 5] = M[:, :, 6]
+    M[0, :, 5] = M[1, :, 5]                  # exact duplicate rows: pivot ties
+    M[:, 0, 7] = 0.0                          # zero first column: singular at k = 0
+    M[:, n // 2, 8] = 0.0                     # singular later
+    M[:, :, 9] = np.abs(M[:, :, 9])           # all-positive: ties in |.| broken by position only
+    M[1, 0, 10] = -M[0, 0, 10]                # |a| tie between rows 0 and 1
+    LU, piv, x, info = (t.cpu().numpy() for t in P.lu_factor_solve(cu(M), cu(b), routine="split"))
+    for c in range(N):
+        LUo, pivo, io = oracle.lu_factor(M[:, :, c])
+        assert info[c] == io, c
+        if io:
+            continue
+        assert np.array_equal(piv[:, c], pivo), c
+        assert np.array_equal(LU[:, :, c], LUo), c
+        assert np.array_equal(x[:, c], oracle.lu_solve(LUo, pivo, b[:, c])), c
+        if c % 512 == 0:   # and within rounding of the plain (true-division) solve
+            np.testing.assert_allclose(x[:, c], oracle.lu_solve(LUo, pivo, b[:, c], plain=True),
+                                       rtol=1e-12 * max(1.0, float(np.linalg.cond(M[:, :, c]))) , atol=0)
+
+
 # ------------------------------------------------------------------ RHS / J
 def model_states(name, count, seed=7):
     if name == "robertson":
@@ -102,7 +132,7 @@ def oracle_model(oracle, name):
                                          ("h2", "group"), ("h2", "split"), ("drm19", "thread"), ("drm19", "group"),
                                          ("drm19", "split")])
 def test_rhs_parity(oracle, name, kernel):
-    y, rho, F = model_states(name, 32768)
+    y, rho, F = model_states(name, 131072 if name in ("h2", "drm19") and kernel == "split" else 32768)
     n, N = y.shape
     b = P.Batch(N, n, 1e-6, 1e-10)
     b.set_kernel(kernel)
@@ -110,7 +140,9 @@ def test_rhs_parity(oracle, name, kernel):
     f, st = P.eval_rhs(b, cu(y), f_ext=cu(F), aux=cu(rho))
     f, st = f.cpu().numpy(), st.cpu().numpy()
     m = oracle_model(oracle, name)
-    idx = np.arange(N) if N <= 4096 else np.sort(np.random.default_rng(1).choice(N, 4096, replace=False))
+    # every state for the default kernel of the mechanisms (>= 1e5 states), else a sample
+    full = kernel == "split" or N <= 4096
+    idx = np.arange(N) if full else np.sort(np.random.default_rng(1).choice(N, 4096, replace=False))
     worst = 0.0
     for c in idx:
         r = rho[c] if rho is not None else 1.0
@@ -156,6 +188,9 @@ def test_robertson_c1_bit_identical(oracle):
         yg, sg, st = run_gpu("robertson", 3, y0, 40.0, rtol, atol)
         yo, so = oracle.integrate_batch(oracle.Model.robertson(), y0, 0.0, 40.0, rtol, atol, threads=8)
         end_state_check(yg, yo, rtol, np.broadcast_to(np.asarray(atol, dtype=float), (3,))[:, None])
+        # the plain-arithmetic oracle (libm pow roots, true division): same band, no bit identity expected
+        yp, _ = oracle.integrate_batch(oracle.Model.robertson(), y0, 0.0, 40.0, rtol, atol, threads=8, plain=True)
+        end_state_check(yg, yp, rtol, np.broadcast_to(np.asarray(atol, dtype=float), (3,))[:, None])
         assert np.abs(yg.sum(axis=0) - y0.sum(axis=0)).max() <= 1e-14
         assert st["n_failed"] == 0 and st["n_cells"] == 1024
         for k in STAT_KEYS:
@@ -188,17 +223,61 @@ def test_flame_parity(oracle, name, dt, kernel):
     same = np.mean([all(sg[k][c] == so[k][c] for k in STAT_KEYS) for c in range(y0.shape[1])])
     print(f"{name} dt={dt} {kernel}: identical per-cell stats {same:.4f}")
     assert same > 0.95
+    if kernel == "split":   # the plain-arithmetic oracle (libm pow roots, true division): same band
+        yp, _ = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, dt, 1e-6, 1e-10, rho=rho, fext_yc=F,
+                                       group=st["group"], threads=8, plain=True)
+        end_state_check(yg, yp, 1e-6, 1e-10)
 
 
-def test_mass_conservation_both_sides(oracle):
-    """F_Y = 0 (only F_T forcing): sum_k Y_k is conserved to round-off on both sides."""
-    y0, rho, F, prog = flame_field("drm19_class", 8, dt=1e-5)
-    yg, _, st = run_gpu("drm19", 22, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
-    yo, _ = oracle.integrate_batch(oracle.Model.mechanism("drm19_class"), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho,
+@pytest.mark.parametrize("name", ["h2", "drm19"])
+def test_flame_parity_slot_reuse(oracle, name, monkeypatch):
+    """SPLIT with a small slot pool (64 slots for 4096 cells): every slot stores a finished cell and loads the
+    next one into a dirty record many times; results must equal the oracle's as with one cell per slot."""
+    monkeypatch.setenv("BDFB_SPLIT_SLOTS", "64")
+    mech, n = MECH[name]
+    y0, rho, F, prog = flame_field(mech, 16, dt=1e-5)
+    yg, sg, st = run_gpu(name, n, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F, kernel="split")
+    yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho, fext_yc=F,
+                                    group=st["group"], threads=8)
+    assert st["n_failed"] == 0 and np.array_equal(sg["status"], so["status"])
+    end_state_check(yg, yo, 1e-6, 1e-10)
+    monkeypatch.delenv("BDFB_SPLIT_SLOTS")
+    yd, _, _ = run_gpu(name, n, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F, kernel="split")
+    assert np.array_equal(yd, yg)         # the pool size never changes a result
+
+
+def element_matrix(mech):
+    """E[j, k] / W_k: moles of element j per gram of species k (problem data: the table's compositions)."""
+    t = oracle_table(mech)
+    els = sorted({e for s in t["species"] for e in s["composition"]})
+    E = np.array([[s["composition"].get(e, 0) / s["W"] for s in t["species"]] for e in els])
+    return els, E
+
+
+def oracle_table(mech):
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "mechanisms",
+                                       mech + ".json")))
+
+
+@pytest.mark.parametrize("name", ["h2", "drm19"])
+def test_mass_and_element_conservation_both_sides(oracle, name):
+    """F_Y = 0 (only F_T forcing): sum_k Y_k and every element sum sum_k E_jk Y_k / W_k are linear invariants
+    (c.f = 0), conserved to round-off on both sides."""
+    mech, n = MECH[name]
+    y0, rho, F, prog = flame_field(mech, 8, dt=1e-5)
+    yg, _, st = run_gpu(name, n, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
+    yo, _ = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho,
                                    fext_yc=F, group=st["group"], threads=8)
     s0 = y0[:-1].sum(axis=0)
     assert np.abs(yg[:-1].sum(axis=0) - s0).max() <= 1e-13
     assert np.abs(yo[:-1].sum(axis=0) - s0).max() <= 1e-13
+    els, E = element_matrix(mech)
+    e0 = E @ y0[:-1]
+    scale = np.abs(E) @ np.abs(y0[:-1])
+    for side in (yg, yo):
+        assert np.all(np.abs(E @ side[:-1] - e0) <= 1e-13 * scale), els
 
 
 # ------------------------------------------------------------------ edge cases
@@ -257,7 +336,7 @@ def test_full_size_c3_sampled(oracle):
     yg, sg, st = run_gpu("h2", n, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
     G = st["group"]
     assert st["n_failed"] == 0 and st["n_cells"] == 64 ** 3
-    idx = stratified_sample(prog, 300)
+    idx = stratified_sample(prog, 4000)
     yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, 1e-5, 1e-6, 1e-10, rho=rho, fext_yc=F,
                                     group=G, threads=8, cells=idx)
     end_state_check(yg[:, idx], yo, 1e-6, 1e-10)
@@ -287,21 +366,46 @@ def test_global_norm_mode_parity(oracle, name, L, dt):
 
 
 def test_full_size_c4_sampled(oracle):
-    """C4 at its BASELINE size (256^3 = 16.7M DRM19-class cells) in exactly the launch
-    configuration bench.py times (default thread-per-cell kernel, one persistent launch);
-    end-state parity on a stratified sample the oracle integrates cell by cell, plus the
-    conservation check (sum_k Y_k, F_Y = 0) on every cell."""
+    """C4 at its BASELINE size (256^3 = 16.7M DRM19-class cells) in exactly the launch configuration bench.py
+    times (the default per-cell kernel); end-state parity on the SURVEY §8(d).3 stratified 65,536-cell sample
+    (equal quotas of fresh, reacting and burnt cells) that the oracle integrates cell by cell, plus the
+    conservation checks (sum_k Y_k and element sums, F_Y = 0) on every cell.  Reports the identical-stats
+    fraction, the |dy|/tol distribution and the number of cells outside the bar (decision flips) to
+    gpurun_out/c4_parity_report.json."""
+    import json
+    import os
+    import time
     mech, n = MECH["drm19"]
     y0, rho, F, prog = flame_field(mech, 256, dt=1e-5)
     yg, sg, st = run_gpu("drm19", n, y0, 1e-5, 1e-6, 1e-10, rho=rho, F=F)
     assert st["n_failed"] == 0 and st["n_cells"] == 256 ** 3
     s0 = y0[:-1].sum(axis=0)
     assert np.abs(yg[:-1].sum(axis=0) - s0).max() <= 1e-13
-    idx = stratified_sample(prog, 240)
+    els, E = element_matrix(mech)
+    for j in range(len(els)):     # element sums on every cell (row by row to bound host memory)
+        e0 = E[j] @ y0[:-1]
+        assert np.all(np.abs(E[j] @ yg[:-1] - e0) <= 1e-13 * (np.abs(E[j]) @ np.abs(y0[:-1]))), els[j]
+    idx = stratified_sample(prog, 65536 // 3)
+    t0 = time.time()
     yo, so = oracle.integrate_batch(oracle.Model.mechanism(mech), y0[:, idx], 0.0, 1e-5, 1e-6, 1e-10, rho=rho[idx],
-                                    fext_yc=F[:, idx], group=st["group"], threads=8)
-    end_state_check(yg[:, idx], yo, 1e-6, 1e-10)
+                                    fext_yc=F[:, idx], group=st["group"], threads=os.cpu_count() or 8)
+    t_orc = time.time() - t0
+    tol = 10.0 * (1e-6 * np.abs(yo) + 1e-10)
+    ratio = (np.abs(yg[:, idx] - yo) / tol).max(axis=0)
+    same = np.ones(len(idx), bool)
+    for k in STAT_KEYS:
+        same &= sg[k][idx] == so[k]
+    rep = {"cells": int(len(idx)), "identical_stats_fraction": float(same.mean()),
+           "outside_bar": int((ratio > 1.0).sum()), "max_ratio": float(ratio.max()),
+           "ratio_quantiles": {q: float(np.quantile(ratio, float(q))) for q in ("0.5", "0.9", "0.99", "0.999")},
+           "ratio_histogram_log10": np.histogram(np.log10(np.maximum(ratio, 1e-20)), bins=np.arange(-20, 2))[0].tolist(),
+           "oracle_seconds": t_orc, "oracle_threads": os.cpu_count()}
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/c4_parity_report.json", "w") as f:
+        json.dump(rep, f, indent=1)
+    print("C4 65536-cell parity:", rep)
     assert np.array_equal(sg["status"][idx], so["status"])
+    end_state_check(yg[:, idx], yo, 1e-6, 1e-10)
 
 
 def test_full_size_c2_sampled(oracle):
@@ -310,7 +414,7 @@ def test_full_size_c2_sampled(oracle):
     dt = 3e15
     yg, sg, st = run_gpu("nyx_kwh", 1, e, dt, 1e-6, 1e-10, rho=rho, F=fe)
     assert st["n_cells"] == 128 ** 3
-    idx = np.sort(np.random.default_rng(7).choice(128 ** 3, 2000, replace=False))
+    idx = np.sort(np.random.default_rng(7).choice(128 ** 3, 20000, replace=False))
     yo, so = oracle.integrate_batch(oracle.Model.nyx_kwh(), e[:, idx], 0.0, dt, 1e-6, 1e-10, rho=rho[idx],
                                     fext_yc=fe[:, idx], threads=8)
     assert np.array_equal(sg["status"][idx], so["status"])
@@ -419,6 +523,9 @@ def test_autoignition_box_parity(oracle, name, dt):
                                     group=st["group"], threads=8)
     assert np.array_equal(sg["status"], so["status"]) and st["n_failed"] == 0
     end_state_check(yg, yo, 1e-6, 1e-10)
+    yp, _ = oracle.integrate_batch(oracle.Model.mechanism(mech), y0, 0.0, dt, 1e-6, 1e-10, rho=rho,
+                                   group=st["group"], threads=8, plain=True)
+    end_state_check(yg, yp, 1e-6, 1e-10)
     rise = yg[-1] - y0[-1]
     assert np.mean(rise > 100.0) > 0.05 and np.mean(rise < 100.0) > 0.05, "the step must straddle ignition"
     s0 = y0[:-1].sum(axis=0)
