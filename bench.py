@@ -6,9 +6,11 @@ A "step" is one outer fluid step of the hot path: bdfb_integrate of every cell
 of the workload from t0 to t0 + dt_CFD (per-cell BDF: RHS, Jacobian, Newton,
 LU, WRMS, step/order control -- SURVEY.md §8(a)), restarted each step from the
 same pristine synthetic field (copied in untimed; the state alone is 2.9 GB,
-far larger than the 126 MB L2).  Multi-GPU (torchrun): every rank integrates
-its own slab of cells (weak scaling, no collective on the data path); the
-timed total is the max over ranks.
+far larger than the 126 MB L2).  Multi-GPU (torchrun): by default the config's
+fixed grid is dealt over the ranks in block-cyclic 16^3 tiles (strong scaling,
+BASELINE "256^3 cells sharded over 2/4/8 B200"; --scaling weak gives every rank
+a full grid); no collective on the data path; the timed duration is the max
+over ranks and value = all ranks' cells / that time.
 
 The JSON line carries the device-timed value, the FP64 roofline of the
 integrator kernel, the CPU oracle timed on the host cores (cpu_baseline), an
@@ -56,19 +58,55 @@ UNIT = "cells/s"
 FP64_FMA_PER_SM_CLK = 64        # B200 FP64 units per SM (sm_100a): 148 x 64 x 2 x 1.965 GHz = 37.2 TF
 SMS = 148
 SM_MAX_MHZ = 1965.0
-TRANSC_FLOPS = 20               # FP64 flops charged per exp/log
+# FP64 flops charged per exp / log call ("weighted by its FP64-pipe instruction count, measured
+# once on the box"): 2 DFMA + DADD + DMUL executed per call of the GPU's exp (fexp) and log, from ncu on
+# exp/probe/transc_probe.cu (profiles/r2/transc_weights.json); fallback: the static SASS counts of the same probe.
+TRANSC_STATIC = {"exp": 31, "log": 46, "source": "static SASS count of exp/probe/transc_probe.cu (cuobjdump)"}
+
+
+def transc_weights():
+    try:
+        with open(os.path.join(REPO, "profiles", "r2", "transc_weights.json")) as f:
+            w = json.load(f)
+        # the logs of the definition are one ln T per RHS plus log10 (Troe); charged at the log10 cost
+        return {"exp": float(w["fexp"]["flops_per_call"]), "log": float(w["log10"]["flops_per_call"]),
+                "source": "ncu executed 2 DFMA + DADD + DMUL per call of fexp / log10 "
+                          "(profiles/r2/transc_weights.json)"}
+    except Exception:
+        return dict(TRANSC_STATIC)
+
+
+def _gen_counts(mech):
+    hdr = open(os.path.join(REPO, "paper_2405_01713_b200", "csrc", "gen", f"mech_{mech}.cuh")).read()
+    return lambda k: int(re.search(rf"{k} = (\d+)", hdr).group(1))  # noqa: E731
 
 
 # ------------------------------------------------------------------ inputs
-def make_inputs(cfg, rank=0, cells_per_rank=None, world=1):
-    """This rank's slab of the seeded field (paper_2405_01713_b200.parallel.shard)."""
-    from paper_2405_01713_b200.parallel import shard
+def rank_cells(cfg, rank=0, world=1, scaling="strong", cells_per_rank=None):
+    """Global cell indices this rank integrates.  strong: the config's fixed grid shared by the ranks -- 16^3
+    tiles dealt block-cyclically (parallel.block_cyclic_cells) for the per-cell grids, contiguous
+    256-aligned slabs for the global-norm batch and C1's 1024 cells; weak: `cells_per_rank` (default the
+    config's grid) per rank, rank r owning global cells r N .. (r+1) N - 1 of one larger seeded field."""
+    from paper_2405_01713_b200 import parallel as PL
+    L = CONFIGS[cfg][3]
+    total = 1024 if cfg == "C1" else L ** 3
+    if scaling == "weak" or cells_per_rank:
+        N = cells_per_rank or total
+        return np.arange(*PL.shard(rank, world, N)), N * world
+    if world == 1:
+        return np.arange(total), total
+    if cfg == "C1" or cfg in GLOBAL_CFGS:
+        return np.arange(*PL.contiguous_cells(rank, world, total, 1 if cfg == "C1" else 256)), total
+    return PL.block_cyclic_cells(rank, world, L, 16), total
+
+
+def make_inputs(cfg, rank=0, cells_per_rank=None, world=1, scaling="strong"):
+    """This rank's cells of the seeded field (identical values under any partition: synth is counter-based)."""
     from synth import flame_field, nyx_field, robertson_field
     model, mech, n, L, dt, rtol, atol, _ = CONFIGS[cfg]
-    N = cells_per_rank or (1024 if cfg == "C1" else L ** 3)
-    cells = np.arange(*shard(rank, world, N))
+    cells, total = rank_cells(cfg, rank, world, scaling, cells_per_rank)
     if cfg == "C1":
-        return robertson_field(N * world, cells=cells), None, None, np.arange(N)
+        return robertson_field(total, cells=cells), None, None, np.arange(len(cells))
     if cfg == "C2":
         e, rho, fe = nyx_field(L, cells=cells, dt=dt)
         return e, rho, fe, None
@@ -76,26 +114,40 @@ def make_inputs(cfg, rank=0, cells_per_rank=None, world=1):
     return y, rho, F, prog
 
 
-def flop_model(cfg, st):
-    """Algorithmic FP64 flops of one launch from the aggregate per-cell statistics."""
+def unit_flops(cfg):
+    """Algorithmic FP64 flops per unit of work: one RHS, one Jacobian, one matrix setup
+    (M = I - gamma J and the reciprocal-multiply LU), one Newton solve (+ its vector updates and norm),
+    one attempt (predict, weights, coefficients, error test), one accepted step (completion, PREPARE_NEXT)."""
     model, mech, n, *_ = CONFIGS[cfg]
+    w = transc_weights()
     if mech:
-        hdr = open(os.path.join(REPO, "paper_2405_01713_b200", "csrc", "gen", f"mech_{mech}.cuh")).read()
-        g = lambda k: int(re.search(rf"{k} = (\d+)", hdr).group(1))  # noqa: E731
-        f_rhs = g("FLOPS_RHS_ARITH") + TRANSC_FLOPS * g("RHS_TRANSCENDENTALS")
-        f_jac = g("FLOPS_JAC_ARITH") + TRANSC_FLOPS * g("JAC_TRANSCENDENTALS")
+        g = _gen_counts(mech)
+        f_rhs = g("FLOPS_RHS_ARITH") + w["exp"] * g("RHS_EXPS") + w["log"] * g("RHS_LOGS")
+        f_jac = g("FLOPS_JAC_ARITH") + w["exp"] * g("JAC_EXPS") + w["log"] * g("JAC_LOGS")
     elif model == "robertson":
         f_rhs, f_jac = 12, 10
     else:  # nyx_kwh: ~12 regula-falsi evaluations x (~16 transcendental + 40 arith) + cooling sum
-        f_rhs, f_jac = 12 * (16 * TRANSC_FLOPS + 40) + 20 * TRANSC_FLOPS + 60, 0
-    f_lu = (2 * (n - 1) * n * (2 * n - 1)) // 6 + n * (n - 1) // 2 + n + 2 * n * n
-    f_sol = 2 * n * n - n
+        f_rhs, f_jac = 12 * (16 * w["exp"] + 40) + 20 * w["exp"] + 60, 0
+    return {"rhs": f_rhs, "jac": f_jac, "setup": (2 * (n - 1) * n * (2 * n - 1)) // 6 + n * (n - 1) // 2 + n + 2 * n * n,
+            "solve": 2 * n * n - n + 9 * n, "attempt": 26 * n + 60, "step": 11 * n + 80}
+
+
+def phase_flops(cfg, st):
+    """Algorithmic FP64 flops of one integrate per SPLIT kernel phase (the whole step is their sum):
+    K_rhs = nfe F_rhs, K_jac = nje F_jac, K_lu = nsetups F_setup, K_ctl = Newton solves + vector passes +
+    control.  Global-norm mode: batch counters, every batch step does the work for every cell."""
+    u = unit_flops(cfg)
     att = st["nst"] + st["netf"] + st["ncfn"]
-    f = (st["nfe"] * f_rhs + st["nje"] * f_jac + st["nsetups"] * f_lu + st["nni"] * (f_sol + 9 * n) +
-         att * (6 * n + 20 * n + 60) + st["nst"] * (8 * n + 3 * n + 80))
-    if cfg in GLOBAL_CFGS:      # batch counters: every batch step does the work for every cell
-        f *= st["n_cells"]
-    return f
+    ph = {"rhs": st["nfe"] * u["rhs"], "jac": st["nje"] * u["jac"], "lu": st["nsetups"] * u["setup"],
+          "ctl": st["nni"] * u["solve"] + att * u["attempt"] + st["nst"] * u["step"]}
+    if cfg in GLOBAL_CFGS:
+        ph = {k: v * st["n_cells"] for k, v in ph.items()}
+    return ph
+
+
+def flop_model(cfg, st):
+    """Algorithmic FP64 flops of one integrate (whole step) from the aggregate per-cell statistics."""
+    return sum(phase_flops(cfg, st).values())
 
 
 def hbm_bytes_global(cfg, st):
@@ -125,14 +177,6 @@ def ctl_bytes(cfg, st):
     visits = st["nfe"] + st["nsetups"]
     return (visits * 2 * TS_RECORD_BYTES + st["nfe"] * (32 * n + 4) + st["nni"] * (8 * n * n + 12 * n + 48 * n) +
             att * (16 * (QBAR + 1) * n + 32 * n) + st["nst"] * 32 * n // (QBAR + 1))
-
-
-def rhs_flops(cfg, st):
-    """Algorithmic FP64 flops of the RHS evaluations (the K_rhs kernel of SPLIT)."""
-    model, mech, n, *_ = CONFIGS[cfg]
-    hdr = open(os.path.join(REPO, "paper_2405_01713_b200", "csrc", "gen", f"mech_{mech}.cuh")).read()
-    g = lambda k: int(re.search(rf"{k} = (\d+)", hdr).group(1))  # noqa: E731
-    return st["nfe"] * (g("FLOPS_RHS_ARITH") + TRANSC_FLOPS * g("RHS_TRANSCENDENTALS"))
 
 
 def hbm_peak():
@@ -278,7 +322,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cells", type=int, default=0, help="override cells per rank (debug)")
+    ap.add_argument("--cells", type=int, default=0, help="override cells per rank (debug; implies weak scaling)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's fixed grid dealt over the ranks in block-cyclic 16^3 tiles "
+                         "(BASELINE: 256^3 sharded over 2/4/8 GPUs); weak: one full grid per rank")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--kernel", default=None, choices=["thread", "group", "split"],
                     help="per-cell kernel organisation of the mechanism models (default: the library's)")
@@ -301,7 +348,7 @@ def main():
         val = m * len(times) / tt
         line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / len(times),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": {"workload": desc, "sample_cells_per_step": m},
                 "cpu_baseline": {"value": val, "unit": UNIT, "cores": thr, "kind": "oracle",
                                  "sample": (f"first {m} cells of the {cfg} field as one lockstep batch per step"
@@ -321,7 +368,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    y0, rho, F, prog = make_inputs(cfg, rank, args.cells or None, world)
+    scaling = "weak" if args.cells else args.scaling
+    y0, rho, F, prog = make_inputs(cfg, rank, args.cells or None, world, scaling)
     N = y0.shape[1]
     glob_mode = cfg in GLOBAL_CFGS
     b = P.Batch(N, n, rtol, atol, device=local, mode=P.MODE_GLOBAL_NORM if glob_mode else P.MODE_PER_CELL)
@@ -335,7 +383,7 @@ def main():
         uid = torch.cuda.nccl.unique_id() if rank == 0 else None
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
-        b.set_comm(obj[0], world, rank, N * world)
+        b.set_comm(obj[0], world, rank, rank_cells(cfg, rank, world, scaling, args.cells or None)[1])
     y_pristine = torch.tensor(y0, device=dev)
     y = torch.empty_like(y_pristine)
     Fd = None if F is None else torch.tensor(F, device=dev)
@@ -369,49 +417,63 @@ def main():
     step_ms = [a.elapsed_time(z) for a, z in ev]
     total_ms = PL.max_over_ranks(sum(step_ms), dist, dev)
     ms_per_step = total_ms / args.steps
-    value = PL.job_throughput(N, world, ms_per_step * 1e-3)
+    n_total = int(PL.sum_over_ranks(N, dist, dev))
+    value = n_total / (ms_per_step * 1e-3)
 
-    # roofline: algorithmic FP64 flops of the integrator kernel / its event-timed duration
-    flops = [flop_model(cfg, s) for s in stats]
-    achieved = statistics.mean(f / (k * 1e-3) for f, k in zip(flops, kern_ms)) / 1e12
+    # roofline: the binding roof of the per-cell path is the FP64 pipe; achieved = ALGORITHMIC
+    # FP64 flops (unit_flops x per-cell statistics) / the kernel's event-timed duration on the launch stream.
     peak = SMS * FP64_FMA_PER_SM_CLK * 2 * SM_MAX_MHZ * 1e6 / 1e12
     probe = None
     try:
         import ctypes as C
         tf, sm = C.c_double(), C.c_int32()
-        if P._lib.lib().bdfb_probe_fp64(local, 200.0, C.byref(tf), C.byref(sm)) == 0:
-            probe = tf.value
+        with ClockSampler(local) as pclk:
+            ok = P._lib.lib().bdfb_probe_fp64(local, 500.0, C.byref(tf), C.byref(sm)) == 0
+        if ok:
+            probe = {"tflops": tf.value, "sms": sm.value, "clocks": pclk.summary(),
+                     "kernel": "fp64_probe_kernel (8 independent DFMA chains per thread, all SMs)"}
     except Exception:
         pass
-    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic_per_launch(cfg, N),
-            "kernel": (("integrate_tpc_kernel<Tpc_%s>" if b.wrms_group == 1 else "integrate_group_kernel<ModelMech<%s>>")
-                       % mech) if mech else "integrate_kernel<%s>" % model,
-            "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
-            "fp64_probe_tflops": probe, "kernel_ms": statistics.mean(kern_ms),
-            "flops_per_launch": statistics.mean(flops)}
+    tw = transc_weights()
+    pf = [phase_flops(cfg, s) for s in stats]
+    flops = [sum(p.values()) for p in pf]
+    whole = statistics.mean(f / (k * 1e-3) for f, k in zip(flops, kern_ms)) / 1e12
+    roof_common = {"bound": "alu", "pipe": "fp64", "peak": peak, "unit": "TFLOP/s",
+                   "peak_source": "derived from B200_PROFILING.md unit counts: 148 SM x 64 FP64 FMA/clk x 2 x 1965 "
+                                  "MHz (MEASURED_PEAKS.json has no FP64 entry); fp64_probe is the measured DFMA "
+                                  "throughput with its clocks",
+                   "fp64_probe": probe, "transcendental_flops": tw,
+                   "whole_step": {"achieved": whole, "frac": whole / peak, "flops_per_integrate": statistics.mean(flops),
+                                  "ms": statistics.mean(kern_ms)}}
+    kname = (("integrate_tpc_kernel<Tpc_%s>" if b.wrms_group == 1 else "integrate_group_kernel<ModelMech<%s>>")
+             % mech) if mech else "integrate_kernel<%s>" % model
+    roof = dict(roof_common, achieved=whole, frac=whole / peak, traffic=traffic_per_launch(cfg, N), kernel=kname,
+                kernel_ms=statistics.mean(kern_ms), flops_per_launch=statistics.mean(flops))
     phases = None
     if phase_ms and phase_ms[0]:
-        # SPLIT: four kernels per trip; the roofline is that of the dominant one, K_ctl (HBM-bound: the slot
-        # pool's state round trip + the LU record of every Newton solve), with the whole-step FP64 fraction beside
+        # SPLIT: four kernels per trip, timed per phase with CUDA events on the launch stream.  The roofline is
+        # the dominant kernel's algorithmic FP64 fraction; the whole-step fraction sits beside it; K_ctl's HBM
+        # traffic (its slot-state round trips, an implementation cost, not algorithmic bytes) is a diagnostic.
         hpk, src = hbm_peak()
         pm = {k: statistics.mean(p[k] for p in phase_ms) for k in phase_ms[0]}
         tot = sum(pm.values())
+        phases = {}
+        for k, v in pm.items():
+            fl = statistics.mean(p[k] for p in pf)
+            phases[k] = {"ms": v, "share": v / tot, "flops": fl, "tflops": fl / (v * 1e-3) / 1e12,
+                         "frac": fl / (v * 1e-3) / 1e12 / peak}
         cb = statistics.mean(ctl_bytes(cfg, s) for s in stats)
-        rf = statistics.mean(rhs_flops(cfg, s) for s in stats)
-        ctl_gbs = cb / (pm["ctl"] * 1e-3) / 1e9
-        rhs_tf = rf / (pm["rhs"] * 1e-3) / 1e12
-        phases = {k: {"ms": v, "share": v / tot} for k, v in pm.items()}
-        phases["ctl"].update({"bound": "hbm", "gbs": ctl_gbs, "frac": ctl_gbs / hpk, "bytes": cb})
-        phases["rhs"].update({"bound": "alu", "tflops": rhs_tf, "frac": rhs_tf / peak, "flops": rf})
-        roof = {"bound": "hbm", "achieved": ctl_gbs, "peak": hpk, "unit": "GB/s", "frac": ctl_gbs / hpk,
-                "traffic": traffic_split(cfg, stats[-1]), "kernel": f"split_ctl_kernel<Tpc_{mech}> (K_ctl, "
-                f"{100 * pm['ctl'] / tot:.0f}% of the step)", "peak_source": src,
-                "kernel_ms": pm["ctl"], "bytes_per_integrate": cb,
-                "bytes_model": "DESIGN.md §6: per visit 2 TS records, per RHS value 32n+4, per Newton solve "
-                               "8n^2+60n, per attempt zn[0..q] r/w (q=3) + 32n, per step 32n/(q+1)",
-                "fp64_whole_step": {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                                    "flops_per_launch": statistics.mean(flops)}}
+        phases["ctl"]["hbm_model"] = {"bytes": cb, "gbs": cb / (pm["ctl"] * 1e-3) / 1e9,
+                                      "frac": cb / (pm["ctl"] * 1e-3) / 1e9 / hpk, "peak_source": src,
+                                      "traffic_ncu": traffic_split(cfg, stats[-1]),
+                                      "model": "DESIGN.md §6 (slot-state round trips: implementation bytes)"}
+        dom = max(pm, key=pm.get)
+        knames = {"ctl": "split_ctl_kernel", "jac": "split_jac_kernel", "lu": "split_lu_kernel",
+                  "rhs": "split_rhs_kernel"}
+        roof = dict(roof_common, achieved=phases[dom]["tflops"], frac=phases[dom]["frac"],
+                    traffic=traffic_split(cfg, stats[-1]) if dom == "ctl" else None,
+                    kernel=f"{knames[dom]}<Tpc_{mech}> (K_{dom}, {100 * pm[dom] / tot:.0f}% of the step)",
+                    kernel_ms=pm[dom], flops_per_launch=phases[dom]["flops"])
     if glob_mode:
         # lockstep batch: the state, J and LU stream through HBM every stage -> HBM roofline
         hb = [hbm_bytes_global(cfg, s) for s in stats]
@@ -420,7 +482,7 @@ def main():
         roof = {"bound": "hbm", "achieved": gbs, "peak": hpk, "unit": "GB/s", "frac": gbs / hpk,
                 "traffic": traffic_per_launch(cfg, N), "kernel": "global-norm kernel sequence (gk_*)",
                 "peak_source": src, "kernel_ms": statistics.mean(kern_ms),
-                "bytes_per_integrate": statistics.mean(hb), "fp64_tflops": achieved, "alu_frac": achieved / peak}
+                "bytes_per_integrate": statistics.mean(hb), "fp64": roof_common}
 
     # e2e through the host-buffer C-ABI call (pinned host memory; H2D + integrate + D2H timed)
     yh0 = torch.tensor(y0).pin_memory()
@@ -454,18 +516,21 @@ def main():
     s = PL.reduce_stats(stats[-1], dist, dev)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": desc, "cells_per_gpu": N, "n": n, "rtol": rtol,
+                "config": {"workload": desc, "cells_total": n_total, "cells_per_gpu": N, "n": n, "rtol": rtol,
                            "atol": atol if np.isscalar(atol) else list(atol), "dt_CFD": dt,
                            "mode": "global-norm" if glob_mode else "per-cell",
                            "parallelism": (f"dp{world} (cells sharded; NCCL allgather of the batch norms)"
                                            if glob_mode else f"dp{world} (cells sharded, no collective)"),
+                           "partition": ("single GPU" if world == 1 else
+                                         "contiguous slabs" if (cfg == "C1" or glob_mode or scaling == "weak") else
+                                         "block-cyclic 16^3 tiles"),
                            "l2": "inputs larger than L2 (state %.2f GB per GPU); pristine field restored "
                                  "untimed before each step" % (y0.nbytes / 1e9),
                            "mechanism": mech, "jacobian": args.jac},
                 "roofline": roof, "cpu_baseline": cpu,
-                "e2e": {"value": N * world / (e2e_total / args.steps * 1e-3), "unit": UNIT,
+                "e2e": {"value": n_total / (e2e_total / args.steps * 1e-3), "unit": UNIT,
                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(y0.nbytes)},
                 "gpu_launches": args.steps * b.last_launch_count(),
                 "clocks": clk.summary(),

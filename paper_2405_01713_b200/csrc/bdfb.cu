@@ -538,7 +538,7 @@ extern "C" int bdfb_set_comm(bdfb_batch* b, const void* nccl_unique_id, int32_t 
     return fail(b, BDFB_EINVAL, "bad communicator arguments");
   cudaSetDevice(b->device);
   if (b->gb.comm) { ncclCommDestroy(b->gb.comm); b->gb.comm = nullptr; }
-  if (nranks > 1) {
+  {   // a communicator also for nranks = 1: the exchange path then runs (and is tested) on one GPU
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&b->gb.comm, nranks, id, rank);

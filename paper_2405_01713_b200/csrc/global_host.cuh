@@ -71,7 +71,7 @@ struct GlobalRunner {
 
   // ---- collective helpers (rank-ordered, deterministic) -------------------
   double allsum(double local) {
-    if (!B.comm || B.nranks == 1) return local;
+    if (!B.comm) return local;   // with a communicator the exchange always runs (nranks = 1 included)
     cudaMemcpyAsync(B.sum, &local, sizeof(double), cudaMemcpyHostToDevice, st);
     ncclAllGather(B.sum, B.gath, 1, ncclDouble, B.comm, st);
     std::vector<double> h(B.nranks);
@@ -82,7 +82,7 @@ struct GlobalRunner {
     return acc;
   }
   int allor(int local) {
-    if (!B.comm || B.nranks == 1) return local;
+    if (!B.comm) return local;   // with a communicator the exchange always runs (nranks = 1 included)
     cudaMemcpyAsync(B.flag, &local, sizeof(int), cudaMemcpyHostToDevice, st);
     ncclAllGather(B.flag, B.igath, 1, ncclInt, B.comm, st);
     std::vector<int> h(B.nranks);
@@ -93,7 +93,7 @@ struct GlobalRunner {
     return r;
   }
   double allmax(double local) {
-    if (!B.comm || B.nranks == 1) return local;
+    if (!B.comm) return local;   // with a communicator the exchange always runs (nranks = 1 included)
     cudaMemcpyAsync(B.sum, &local, sizeof(double), cudaMemcpyHostToDevice, st);
     ncclAllGather(B.sum, B.gath, 1, ncclDouble, B.comm, st);
     std::vector<double> h(B.nranks);

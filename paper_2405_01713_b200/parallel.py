@@ -1,7 +1,9 @@
 """Multi-GPU plumbing for the per-cell path (one process per GPU).
 
-Cells are independent, so ranks integrate disjoint slabs with
-no collective on the data path (weak scaling).  The only communication is
+Cells are independent, so ranks integrate disjoint sets of cells
+with no collective on the data path: one fixed grid dealt in block-cyclic tiles
+(strong scaling, the BASELINE configuration "256^3 cells sharded over 2/4/8
+B200") or one slab of a fixed size per rank (weak scaling).  The only communication is
 host-side plumbing over torch.distributed: a barrier around the timed region,
 the max over ranks of the timed duration, and the sum of the aggregate
 integrator statistics.  (The global-norm mode's WRMS allreduce is the one
@@ -29,6 +31,37 @@ def shard(rank: int, world: int, cells_per_rank: int):
     return rank * cells_per_rank, (rank + 1) * cells_per_rank
 
 
+def block_cyclic_cells(rank: int, world: int, L: int, tile: int = 16):
+    """Strong scaling of one L^3 grid: the grid is cut into (L/tile)^3 tiles of tile^3 cells,
+    numbered x-fastest, and tile t is dealt to rank t mod world, so every rank gets a spatially spread share of
+    any stiffness gradient (an ignition front, a temperature ramp).  Returns the sorted global cell indices
+    (x-fastest: c = (k L + j) L + i, the synth.fields grid order) of `rank`'s tiles.  Requires tile | L; when
+    world does not divide the tile count the first (count mod world) ranks get one tile more."""
+    import numpy as np
+    if not (0 <= rank < world) or L < 1 or tile < 1 or L % tile:
+        raise ValueError("bad block-cyclic request")
+    T = L // tile
+    tiles = np.arange(rank, T ** 3, world, dtype=np.int64)
+    ti, tj, tk = tiles % T, (tiles // T) % T, tiles // (T * T)
+    o = np.arange(tile, dtype=np.int64)
+    ii = (ti[:, None] * tile + o[None, :])                     # [tiles, tile]
+    jj = (tj[:, None] * tile + o[None, :])
+    kk = (tk[:, None] * tile + o[None, :])
+    c = (kk[:, :, None, None] * L + jj[:, None, :, None]) * L + ii[:, None, None, :]
+    return np.sort(c.reshape(-1))
+
+
+def contiguous_cells(rank: int, world: int, total: int, align: int = 1):
+    """[start, stop) of rank's contiguous part of `total` cells, part sizes multiples of `align` except the last
+    (the global-norm mode keeps whole 256-cell reduction blocks per rank, reading R15)."""
+    if not (0 <= rank < world) or total < 1:
+        raise ValueError("bad contiguous request")
+    per = -(-total // world)
+    per = -(-per // align) * align
+    a = min(total, rank * per)
+    return a, min(total, a + per)
+
+
 def max_over_ranks(value: float, dist=None, device=None) -> float:
     """Max of a per-rank scalar (timed durations are reported as the slowest rank)."""
     if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
@@ -36,6 +69,16 @@ def max_over_ranks(value: float, dist=None, device=None) -> float:
     import torch
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, dist=None, device=None) -> float:
+    """Sum of a per-rank scalar (e.g. the cells each rank integrated)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
 

@@ -365,6 +365,26 @@ def test_global_norm_mode_parity(oracle, name, L, dt):
     assert np.all(cs["nst"].cpu().numpy() == so["nst"])
 
 
+def test_global_norm_nccl_exchange_single_rank(oracle):
+    """bdfb_set_comm with nranks = 1: the library's NCCL communicator is created and every batch norm goes
+    through the rank-ordered ncclAllGather exchange; with one rank the rank-ordered sum
+    is 0 + S, so the run is bit-identical to the run without a communicator."""
+    mech, n = MECH["drm19"]
+    y0, rho, F, prog = flame_field(mech, 4, dt=1e-6)
+    N = y0.shape[1]
+    out = []
+    for comm in (False, True):
+        b = P.Batch(N, n, 1e-6, 1e-10, mode=P.MODE_GLOBAL_NORM)
+        b.set_model("drm19")
+        if comm:
+            b.set_comm(torch.cuda.nccl.unique_id(), 1, 0, N)
+        y = cu(y0)
+        b.integrate(0.0, 1e-6, y, f_ext=cu(F), aux=cu(rho))
+        out.append((y.cpu().numpy(), b.stats()))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1]["nst"] == out[1][1]["nst"] and out[0][1]["nfe"] == out[1][1]["nfe"]
+
+
 def test_full_size_c4_sampled(oracle):
     """C4 at its BASELINE size (256^3 = 16.7M DRM19-class cells) in exactly the launch configuration bench.py
     times (the default per-cell kernel); end-state parity on the SURVEY §8(d).3 stratified 65,536-cell sample

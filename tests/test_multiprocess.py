@@ -113,3 +113,61 @@ def test_two_rank_typical_values_gloo():
     for r in range(world):
         lo, hi = out[r]
         assert np.array_equal(0.5 * (lo + hi), tv)
+
+
+# ---------------------------------------------------------------- strong scaling: block-cyclic tiles
+def test_block_cyclic_partition_covers_grid_once():
+    """Tiles of 16^3 dealt round-robin: every cell of the grid exactly once, balanced to one tile, and each
+    rank's cells spread over the whole grid (every z-slab of tiles is represented when world <= tiles/slab)."""
+    sys.path.insert(0, REPO)
+    from paper_2405_01713_b200 import parallel as PL
+    L, tile = 64, 16
+    for world in (1, 2, 3, 4, 8):
+        parts = [PL.block_cyclic_cells(r, world, L, tile) for r in range(world)]
+        allc = np.concatenate(parts)
+        assert len(allc) == L ** 3 and len(np.unique(allc)) == L ** 3
+        sizes = [len(p) for p in parts]
+        assert max(sizes) - min(sizes) <= tile ** 3
+        for p in parts:
+            assert len(np.unique(p // (L * L * tile))) == L // tile      # every z-slab of tiles
+    with pytest.raises(ValueError):
+        PL.block_cyclic_cells(0, 2, 60, 16)
+
+
+def _strong_worker(rank, world, port, L, tile, out):
+    sys.path.insert(0, REPO)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    from paper_2405_01713_b200 import parallel as PL
+    from synth import robertson_field
+    cells = PL.block_cyclic_cells(rank, world, L, tile)
+    y0 = robertson_field(L ** 3, cells=cells)
+    y, st = O.integrate_batch(O.Model.robertson(), y0, 0.0, 4.0, 1e-6, 1e-10)
+    total = PL.sum_over_ranks(len(cells), dist)
+    out[rank] = (cells, y, total)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_strong_scaling_block_cyclic_gloo():
+    """bench.py's default multi-GPU mode on the CPU: two ranks integrate their block-cyclic tiles of one fixed
+    grid; the union is the whole grid, the cell count sums to L^3 over the ranks, and every cell equals the
+    single-process result bit for bit (the seeded inputs do not depend on the partition)."""
+    world, L, tile = 2, 8, 4
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_strong_worker, args=(world, _free_port(), L, tile, out), nprocs=world, join=True)
+    sys.path.insert(0, REPO)
+    from oracle import oracle as O
+    from synth import robertson_field
+    y0 = robertson_field(L ** 3)
+    yref, _ = O.integrate_batch(O.Model.robertson(), y0, 0.0, 4.0, 1e-6, 1e-10)
+    seen = np.zeros(L ** 3, int)
+    for r in range(world):
+        cells, y, total = out[r]
+        assert total == L ** 3
+        seen[cells] += 1
+        assert np.array_equal(y, yref[:, cells])
+    assert np.all(seen == 1)
