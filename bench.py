@@ -45,14 +45,19 @@ CONFIGS = {
            "C3 H2/air (9 species + T, n=10) flame field on 64^3 cells, dt_CFD 1e-5 s"),
     "C4": ("drm19", "drm19_class", 22, 256, 1e-5, 1e-6, 1e-10,
            "C4 DRM19-class CH4/air (21 species + T, n=22) flame field on 256^3 cells, dt_CFD 1e-5 s"),
-    # the paper's lockstep batch (row a12).  C5's 53-species mechanism is not available (R22) and the
-    # group kernel holds n <= 32, so the global-norm path is measured on the DRM19-class mechanism, at C5's
-    # per-GPU cell count (256^3 / 8 GPUs = 128^3).
+    # the paper's lockstep batch (row a12) on the DRM19-class mechanism at C5's per-GPU cell count
+    # (256^3 / 8 GPUs = 128^3): the global-norm path of the generated thread-per-cell kernels.
+    # BASELINE configs[4]: the ~53-species mechanism on 256^3 cells over 8 B200 in the global-norm mode; one GPU
+    # runs its 1/8 share (a 256 x 256 x 32 slab = 128^3 cells); rank r of k <= 8 ranks its slab r (weak scaling)
+    "C5": ("gri53", "gri53_class", 54, 256, 1e-6, 1e-6, 1e-10,
+           "C5 GRI-3.0-class CH4/air (53 species + T, n=54, 325 reactions) flame field, global-norm mode (one "
+           "lockstep batch, batch-wide WRMS), 256^3 grid in 8 z-slabs of 128^3 cells (one per GPU), dt_CFD 1e-6 s"),
     "G4": ("drm19", "drm19_class", 22, 128, 1e-5, 1e-6, 1e-10,
            "G4 global-norm mode (lockstep batch, batch-wide WRMS) on the DRM19-class flame field, 128^3 cells "
            "(C5's per-GPU share at 8 GPUs), dt_CFD 1e-5 s"),
 }
-GLOBAL_CFGS = {"G4"}
+GLOBAL_CFGS = {"G4", "C5"}
+C5_SLAB = 256 ** 3 // 8            # cells per GPU in C5
 METRIC = "cell ODE integrations/sec per outer step"
 UNIT = "cells/s"
 FP64_FMA_PER_SM_CLK = 64        # B200 FP64 units per SM (sm_100a): 148 x 64 x 2 x 1.965 GHz = 37.2 TF
@@ -90,6 +95,10 @@ def rank_cells(cfg, rank=0, world=1, scaling="strong", cells_per_rank=None):
     from paper_2405_01713_b200 import parallel as PL
     L = CONFIGS[cfg][3]
     total = 1024 if cfg == "C1" else L ** 3
+    if cfg == "C5" and not cells_per_rank:     # the 256^3 grid's z-slab r (of 8): fixed share per GPU
+        if world > 8:
+            raise SystemExit("C5 is defined on 8 GPUs (256^3 / 8 cells each)")
+        return np.arange(rank * C5_SLAB, (rank + 1) * C5_SLAB), C5_SLAB * world
     if scaling == "weak" or cells_per_rank:
         N = cells_per_rank or total
         return np.arange(*PL.shard(rank, world, N)), N * world
@@ -368,7 +377,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    scaling = "weak" if args.cells else args.scaling
+    scaling = "weak" if (args.cells or cfg == "C5") else args.scaling
     y0, rho, F, prog = make_inputs(cfg, rank, args.cells or None, world, scaling)
     N = y0.shape[1]
     glob_mode = cfg in GLOBAL_CFGS

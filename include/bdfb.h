@@ -69,6 +69,9 @@ extern "C" {
 #define BDFB_MODEL_MECH_H2 3       /* n=10: H2/air mechanism (mechanisms/h2_lidryer.json),
                                       constant-volume reactor; aux[c] = rho; params: NULL     */
 #define BDFB_MODEL_MECH_DRM19 4    /* n=22: DRM19-class CH4/air (mechanisms/drm19_class.json) */
+#define BDFB_MODEL_MECH_GRI53 5    /* n=54: GRI-3.0-class CH4/air, 53 species, 325 reactions
+                                      (mechanisms/gri53_class.json; config C5); table-driven model,
+                                      global-norm mode only (per-cell integrate: BDFB_EUNSUPPORTED) */
 
 #define BDFB_LAYOUT_YC 0
 #define BDFB_LAYOUT_CY 1
@@ -129,7 +132,7 @@ typedef struct {
 /* Fill *opt with the defaults above. */
 void bdfb_default_options(bdfb_options *opt);
 
-/* Create a batch of n_cells systems of size n on CUDA device `device`.
+/* Create a batch of n_cells systems of size n (1..64) on CUDA device `device`.
  * rtol > 0; atol_host: host array of n values > 0 (Eq. 3; shared by
  * all cells, reading R13).  Allocates ALL workspace once (no allocation ever
  * happens in bdfb_integrate; the lesson of P:527-535).  opt may be NULL.

@@ -24,7 +24,7 @@ MODE_PER_CELL, MODE_GLOBAL_NORM = L.MODE_PER_CELL, L.MODE_GLOBAL_NORM
 __all__ = ["Batch", "MODE_PER_CELL", "MODE_GLOBAL_NORM", "MODELS", "eval_rhs", "eval_jac", "lu_factor_solve", "version", "library_path"]
 
 MODELS = {"linear": (L.MODEL_LINEAR, 1), "robertson": (L.MODEL_ROBERTSON, 3), "nyx_kwh": (L.MODEL_NYX_KWH, 1),
-          "h2": (L.MODEL_MECH_H2, 10), "drm19": (L.MODEL_MECH_DRM19, 22)}
+          "h2": (L.MODEL_MECH_H2, 10), "drm19": (L.MODEL_MECH_DRM19, 22), "gri53": (L.MODEL_MECH_GRI53, 54)}
 STATUS = {0: "OK", 1: "TOO_MUCH_WORK", 2: "ERR_FAILURE", 3: "CONV_FAILURE", 4: "RHS_FAIL", 5: "NONFINITE_INPUT"}
 CELL_STAT_FIELDS = ["status", "nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn", "q_last", "h_last", "t_reached"]
 

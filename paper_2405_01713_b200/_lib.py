@@ -11,7 +11,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BDFB_LIB") or os.path.join(PKG, "libbdfb.so")   # BDFB_LIB: experiments only
 
-MODEL_LINEAR, MODEL_ROBERTSON, MODEL_NYX_KWH, MODEL_MECH_H2, MODEL_MECH_DRM19 = 0, 1, 2, 3, 4
+MODEL_LINEAR, MODEL_ROBERTSON, MODEL_NYX_KWH, MODEL_MECH_H2, MODEL_MECH_DRM19, MODEL_MECH_GRI53 = 0, 1, 2, 3, 4, 5
 LAYOUT_YC, LAYOUT_CY = 0, 1
 MODE_PER_CELL, MODE_GLOBAL_NORM = 0, 1
 KERNEL_AUTO, KERNEL_THREAD, KERNEL_GROUP, KERNEL_SPLIT = 0, 1, 2, 3

@@ -23,6 +23,8 @@
 #include "global_host.cuh"
 #include "gen/mech_drm19_class.cuh"
 #include "gen/mech_h2_lidryer.cuh"
+#include "gen/mech_gri53_class.cuh"
+#include "mech_lanes.cuh"
 #include "gen/tpc_drm19_class.cuh"
 #include "gen/tpc_h2_lidryer.cuh"
 #include "mech_model.cuh"
@@ -72,6 +74,9 @@ struct bdfb_batch {
   std::string err;
 };
 
+// C5 (53 species + T, n = 54): the table-driven lanes model, one cell per warp (global-norm mode)
+using ModelGRI53 = ModelMechR<mech_gri53_class::Traits, 32>;
+
 static bool is_mech(int model) { return model == BDFB_MODEL_MECH_H2 || model == BDFB_MODEL_MECH_DRM19; }
 // mechanism models: AUTO = SPLIT (the fastest organisation measured on B200, profiles/r1)
 static bool use_split(const bdfb_batch* b) {
@@ -97,6 +102,7 @@ static int model_n(int model) {
     case BDFB_MODEL_NYX_KWH: return ModelNyxKwh::N;
     case BDFB_MODEL_MECH_H2: return ModelH2::N;
     case BDFB_MODEL_MECH_DRM19: return ModelDRM19::N;
+    case BDFB_MODEL_MECH_GRI53: return ModelGRI53::N;
   }
   return -1;
 }
@@ -250,7 +256,7 @@ int bdfb_create(bdfb_batch** out, int64_t n_cells, int32_t n, double rtol, const
   if (!out) return fail(nullptr, BDFB_EINVAL, "out is NULL");
   *out = nullptr;
   if (n_cells < 1) return fail(nullptr, BDFB_EINVAL, "n_cells must be >= 1");
-  if (n < 1 || n > 32) return fail(nullptr, BDFB_EINVAL, "n must be in 1..32");
+  if (n < 1 || n > 64) return fail(nullptr, BDFB_EINVAL, "n must be in 1..64");
   if (!(rtol > 0.0) || !isfinite(rtol)) return fail(nullptr, BDFB_EINVAL, "rtol must be > 0");
   if (!atol_host) return fail(nullptr, BDFB_EINVAL, "atol is NULL");
   for (int i = 0; i < n; ++i)
@@ -398,7 +404,7 @@ int bdfb_set_jacobian(bdfb_batch* b, int32_t mode) {
 
 int32_t bdfb_wrms_group(const bdfb_batch* b) {
   if (!b || b->model < 0) return 0;
-  if (b->opt.mode == BDFB_MODE_GLOBAL_NORM) return b->model == BDFB_MODEL_MECH_H2 ? ModelH2::G : ModelDRM19::G;
+  if (b->opt.mode == BDFB_MODE_GLOBAL_NORM) return 1;   // per-cell sums in component order (gk_cellsum)
   if (use_tpc(b) || use_split(b)) return 1;
   switch (b->model) {
     case BDFB_MODEL_MECH_H2: return ModelH2::G;
@@ -497,14 +503,21 @@ static int run_global(bdfb_batch* b, const Opts& o, double* y, const double* fex
   if constexpr (Model::G > 1) {
     typename Model::Params prm;
     memcpy(&prm, b->params, sizeof(prm));
-    auto* kr = gk_rhs<Model>;
-    auto* ks = gk_setup<Model>;
-    auto* kv = gk_solve<Model>;
-    const int smem = (int)(sizeof(double) * GMK<Model>::PG * GMK<Model>::GPB);
-    if (smem > 48 * 1024) {
-      cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if constexpr (IsLanes<Model>::value) {
+      const int s1 = (int)(sizeof(double) * GLK<Model>::PG_RHS * GLK<Model>::GPB);
+      const int s2 = (int)(sizeof(double) * GLK<Model>::PG_SET * GLK<Model>::GPB);
+      if (s1 > 48 * 1024) cudaFuncSetAttribute(gl_rhs<Model>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
+      if (s2 > 48 * 1024) cudaFuncSetAttribute(gl_setup<Model>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2);
+    } else {
+      auto* kr = gk_rhs<Model>;
+      auto* ks = gk_setup<Model>;
+      auto* kv = gk_solve<Model>;
+      const int smem = (int)(sizeof(double) * GMK<Model>::PG * GMK<Model>::GPB);
+      if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      }
     }
     cudaEventRecord(b->ev0, st);
     GlobalRunner<Model, Tpc> R(b->gb, o, prm, st, b->n, b->ncells, b->d_atol, fext, aux);
@@ -552,7 +565,8 @@ extern "C" int bdfb_set_comm(bdfb_batch* b, const void* nccl_unique_id, int32_t 
 
 // models whose RHS reads the per-cell aux input (density)
 static bool model_needs_aux(int model) {
-  return model == BDFB_MODEL_NYX_KWH || model == BDFB_MODEL_MECH_H2 || model == BDFB_MODEL_MECH_DRM19;
+  return model == BDFB_MODEL_NYX_KWH || model == BDFB_MODEL_MECH_H2 || model == BDFB_MODEL_MECH_DRM19 ||
+         model == BDFB_MODEL_MECH_GRI53;
 }
 
 extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, const double* f_ext,
@@ -584,6 +598,7 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
     switch (b->model) {
       case BDFB_MODEL_MECH_H2: return run_global<ModelH2, Tpc_h2_lidryer>(b, o, y, f_ext, aux, st);
       case BDFB_MODEL_MECH_DRM19: return run_global<ModelDRM19, Tpc_drm19_class>(b, o, y, f_ext, aux, st);
+      case BDFB_MODEL_MECH_GRI53: return run_global<ModelGRI53>(b, o, y, f_ext, aux, st);
       default: return fail(b, BDFB_EUNSUPPORTED, "global-norm mode: group models only (MECH_H2, MECH_DRM19)");
     }
   }
@@ -599,6 +614,8 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
       if (use_split(b)) return launch_split(b, o, y, f_ext, aux, st);
       return use_tpc(b) ? launch_tpc(b, o, y, f_ext, aux, st)
                         : launch_integrate<ModelDRM19>(b, o, y, f_ext, aux, st);
+    case BDFB_MODEL_MECH_GRI53:
+      return fail(b, BDFB_EUNSUPPORTED, "MECH_GRI53 (n = 54, config C5) runs in the global-norm mode");
   }
   return fail(b, BDFB_ENOMODEL, "unknown model");
 }
@@ -768,6 +785,59 @@ static int launch_eval(bdfb_batch* b, double t, const double* y, const double* f
   return BDFB_OK;
 }
 
+// RHS / Jacobian of a lanes model (mech_lanes.cuh), one cell per group; J[(i n + j) N + c]
+template <class MR>
+__global__ void __launch_bounds__(128) eval_lanes_kernel(long long N, const double* y, const double* fext,
+                                                         const double* aux, double* f, int* status, double* J) {
+  constexpr int G = MR::G, NN = MR::N, R = MR::R, PG = MR::SG + MR::JG + NN * (NN | 1);
+  extern __shared__ double smem[];
+  Grp<G> g;
+  double* sc = smem + (threadIdx.x / G) * PG;
+  double* js = sc + MR::SG;
+  double* A = js + MR::JG;
+  const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const bool live = grp < N;
+  const long long c = live ? grp : 0;
+  double yy[R], ff[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = g.lane + G * r;
+    yy[r] = i < NN ? y[(long long)i * N + c] : 0.0;
+  }
+  const double a = aux ? aux[c] : 0.0;
+  if (J == nullptr) {
+    const int rv = MR::rhs(g, yy, a, ff, sc);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = g.lane + G * r;
+      if (live && i < NN) f[(long long)i * N + c] = ff[r] + (fext ? fext[(long long)i * N + c] : 0.0);
+    }
+    if (live && g.lane == 0 && status) status[c] = rv;
+  } else {
+    constexpr int MS = NN | 1;
+    MR::jac(g, yy, a, A, 1, MS, sc, js);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = g.lane + G * r;
+      if (live && i < NN)
+        for (int j = 0; j < NN; ++j) J[((long long)i * NN + j) * N + c] = A[j * MS + i];
+    }
+  }
+}
+
+template <class MR>
+static int launch_eval_lanes(bdfb_batch* b, const double* y, const double* fext, const double* aux, double* f,
+                             int* status, double* J, cudaStream_t st) {
+  constexpr int PG = MR::SG + MR::JG + MR::N * (MR::N | 1);
+  const size_t smem = sizeof(double) * (size_t)PG * (128 / MR::G);
+  auto kern = eval_lanes_kernel<MR>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned grid = (unsigned)((b->ncells * MR::G + 127) / 128);
+  kern<<<grid, 128, smem, st>>>(b->ncells, y, fext, aux, f, status, J);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BDFB_OK : cuda_fail(b, e, "eval launch");
+}
+
 static int launch_eval_tpc(bdfb_batch* b, const double* y, const double* fext, const double* aux, double* f,
                            int* status, double* J, cudaStream_t st) {
   const cudaError_t e = tpc_eval(b->model, b->ncells, y, fext, aux, f, status, J, st);
@@ -792,6 +862,7 @@ extern "C" int bdfb_eval_rhs(bdfb_batch* b, double t, const double* y, const dou
     case BDFB_MODEL_MECH_DRM19:
       return (use_tpc(b) || use_split(b)) ? launch_eval_tpc(b, y, f_ext, aux, f, status, nullptr, st)
                                           : launch_eval<ModelDRM19>(b, t, y, f_ext, aux, f, status, nullptr, st);
+    case BDFB_MODEL_MECH_GRI53: return launch_eval_lanes<ModelGRI53>(b, y, f_ext, aux, f, status, nullptr, st);
   }
   return fail(b, BDFB_ENOMODEL, "unknown model");
 }
@@ -813,6 +884,7 @@ extern "C" int bdfb_eval_jac(bdfb_batch* b, double t, const double* y, const dou
     case BDFB_MODEL_MECH_DRM19:
       return use_tpc(b) ? launch_eval_tpc(b, y, nullptr, aux, nullptr, nullptr, J, st)
                         : launch_eval<ModelDRM19>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
+    case BDFB_MODEL_MECH_GRI53: return launch_eval_lanes<ModelGRI53>(b, y, nullptr, aux, nullptr, nullptr, J, st);
   }
   return fail(b, BDFB_ENOMODEL, "unknown model");
 }

@@ -10,6 +10,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "global_lanes.cuh"
 #include "global_mode.cuh"
 #include "global_tpc.cuh"
 
@@ -35,9 +36,16 @@ struct GlobalResult {
 
 // Tpc: the thread-per-cell mechanism type (gen/tpc_<mech>.cuh) whose kernels (global_tpc.cuh) do the RHS,
 // setup and solve; void: the group kernels of global_mode.cuh
+// lanes models (mech_lanes.cuh, any n): the kernels of global_lanes.cuh
+template <class M, class = void>
+struct IsLanes : std::false_type {};
+template <class M>
+struct IsLanes<M, std::void_t<decltype(M::LANES)>> : std::bool_constant<M::LANES> {};
+
 template <class Model, class Tpc = void>
 struct GlobalRunner {
   static constexpr bool TPC = !std::is_void<Tpc>::value;
+  static constexpr bool LANES = IsLanes<Model>::value;
   using TM = typename std::conditional<TPC, Tpc, Model>::type;
   using P = typename Model::Params;
   static constexpr int QM = QMAX;
@@ -121,6 +129,9 @@ struct GlobalRunner {
     cudaMemsetAsync(B.flag, 0, sizeof(int), st);
     if constexpr (TPC) {
       ++launches; gt_rhs<TM><<<gridc(), 128, 0, st>>>(N, yin, fext, aux, fout, B.flag);
+    } else if constexpr (LANES) {
+      ++launches; gl_rhs<Model><<<gridg(), 128, sizeof(double) * GLK<Model>::PG_RHS * GLK<Model>::GPB, st>>>(
+          N, yin, fext, aux, fout, B.flag);
     } else {
       ++launches; gk_rhs<Model><<<gridg(), 128, smemg(), st>>>(prm, N, t, yin, fext, aux, fout, B.flag);
     }
@@ -255,6 +266,9 @@ struct GlobalRunner {
     if constexpr (TPC) {
       ++launches; gt_setup<TM><<<gridc(), 128, 0, st>>>(N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.perm,
                                                          B.invd, B.flag);
+    } else if constexpr (LANES) {
+      ++launches; gl_setup<Model><<<gridg(), 128, sizeof(double) * GLK<Model>::PG_SET * GLK<Model>::GPB, st>>>(
+          N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.perm, B.invd, B.flag);
     } else {
       ++launches; gk_setup<Model><<<gridg(), 128, smemg(), st>>>(prm, N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU,
                                                                   B.pos, B.perm, B.invd, B.flag);
@@ -293,6 +307,9 @@ struct GlobalRunner {
           if constexpr (TPC) {
             ++launches; gt_solve<TM><<<gridc(), 128, 0, st>>>(N, sc2, B.LU, B.perm, B.invd, B.v.del, B.v.acor,
                                                                B.v.tmp);
+          } else if constexpr (LANES) {
+            ++launches; gl_solve<Model::N><<<gridc(), 128, 0, st>>>(N, sc2, B.LU, B.perm, B.invd, B.v.del, B.v.acor,
+                                                                    B.v.tmp);
           } else {
             ++launches; gk_solve<Model><<<gridg(), 128, smemg(), st>>>(N, sc2, B.LU, B.pos, B.perm, B.invd, B.v.del,
                                                                         B.v.acor, B.v.tmp);

@@ -116,7 +116,9 @@ def nyx_field(L, seed=None, cells=None, dt=NYX_DT):
 MIXTURES = {
     "h2_lidryer": ({"H2": 0.02852, "O2": 0.22635, "N2": 0.74513}, 700.0, 1100.0),
     "drm19_class": ({"CH4": 0.05519, "O2": 0.22015, "N2": 0.72466}, 700.0, 1400.0),
+    "gri53_class": ({"CH4": 0.05519, "O2": 0.22015, "N2": 0.72466}, 700.0, 1400.0),   # C5: CH4/air as C4
 }
+MECH_CONFIG = {"h2_lidryer": 3, "drm19_class": 4, "gri53_class": 5}   # seed S = 2405017130 + config
 DELTA_FLAME = 0.0971            # tanh width: ~15% of cells with 0.02 < c < 0.98 (unit-variance phi)
 
 
@@ -170,7 +172,7 @@ def flame_field(mech, L, seed=None, cells=None, dt=1e-5, forcing=True, threads=N
 
 
 def _flame_chunk(mech, L, seed, c_idx, dt, forcing):
-    seed = config_seed(4 if mech.startswith("drm19") else 3) if seed is None else seed
+    seed = config_seed(MECH_CONFIG[mech]) if seed is None else seed
     M = len(c_idx)
     Yf, W, T_cold, T_u, rho_u = fresh_state(mech)
     K = len(Yf)
@@ -212,7 +214,7 @@ def stratified_sample(prog, per_class, seed=0):
 
 
 # ---------------------------------------------------------------- auto-ignition box
-AUTOIGNITION_T = {"h2_lidryer": (900.0, 1300.0), "drm19_class": (1200.0, 1700.0)}
+AUTOIGNITION_T = {"h2_lidryer": (900.0, 1300.0), "drm19_class": (1200.0, 1700.0), "gri53_class": (1200.0, 1700.0)}
 
 
 def autoignition_box(mech, L, cells=None):

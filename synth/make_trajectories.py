@@ -54,9 +54,10 @@ def trajectory(mech, points=400):
     return cg[keep], states[keep], rho_u, Tb
 
 
-def main():
+def main(argv=None):
     os.makedirs(os.path.join(HERE, "data"), exist_ok=True)
-    for mech in MIXTURES:
+    argv = sys.argv[1:] if argv is None else argv
+    for mech in (argv or MIXTURES):
         c, s, rho, Tb = trajectory(mech)
         np.savez_compressed(os.path.join(HERE, "data", f"{mech}_trajectory.npz"), c=c, states=s, rho=rho, Tb=Tb)
         print(mech, "points", len(c), "T_b", Tb, "rho", rho)

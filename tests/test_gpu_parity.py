@@ -21,7 +21,7 @@ from synth.fields import stratified_sample  # noqa: E402
 
 DEV = torch.device("cuda", 0)
 STAT_KEYS = ("nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn")
-MECH = {"h2": ("h2_lidryer", 10), "drm19": ("drm19_class", 22)}
+MECH = {"h2": ("h2_lidryer", 10), "drm19": ("drm19_class", 22), "gri53": ("gri53_class", 54)}
 KERNELS = ("split", "thread", "group")   # per-cell kernel organisations of the mechanism models (bdfb_set_kernel)
 
 
@@ -130,7 +130,7 @@ def oracle_model(oracle, name):
 
 @pytest.mark.parametrize("name,kernel", [("robertson", "thread"), ("nyx_kwh", "thread"), ("h2", "thread"),
                                          ("h2", "group"), ("h2", "split"), ("drm19", "thread"), ("drm19", "group"),
-                                         ("drm19", "split")])
+                                         ("drm19", "split"), ("gri53", "auto")])
 def test_rhs_parity(oracle, name, kernel):
     y, rho, F = model_states(name, 131072 if name in ("h2", "drm19") and kernel == "split" else 32768)
     n, N = y.shape
@@ -141,7 +141,7 @@ def test_rhs_parity(oracle, name, kernel):
     f, st = f.cpu().numpy(), st.cpu().numpy()
     m = oracle_model(oracle, name)
     # every state for the default kernel of the mechanisms (>= 1e5 states), else a sample
-    full = kernel == "split" or N <= 4096
+    full = (kernel == "split" and name != "gri53") or N <= 4096
     idx = np.arange(N) if full else np.sort(np.random.default_rng(1).choice(N, 4096, replace=False))
     worst = 0.0
     for c in idx:
@@ -159,7 +159,7 @@ def test_rhs_parity(oracle, name, kernel):
 
 @pytest.mark.parametrize("name,kernel", [("robertson", "thread"), ("h2", "thread"), ("h2", "group"),
                                          ("h2", "split"), ("drm19", "thread"), ("drm19", "group"),
-                                         ("drm19", "split")])
+                                         ("drm19", "split"), ("gri53", "auto")])
 def test_jacobian_parity(oracle, name, kernel):
     y, rho, F = model_states(name, 4096)
     n, N = y.shape
@@ -343,7 +343,7 @@ def test_full_size_c3_sampled(oracle):
 
 
 # ------------------------------------------------------------------ global-norm mode (row a12)
-@pytest.mark.parametrize("name,L,dt", [("h2", 4, 1e-5), ("drm19", 4, 1e-6), ("drm19", 8, 1e-5)])
+@pytest.mark.parametrize("name,L,dt", [("h2", 4, 1e-5), ("drm19", 4, 1e-6), ("drm19", 8, 1e-5), ("gri53", 8, 1e-6)])
 def test_global_norm_mode_parity(oracle, name, L, dt):
     """The paper's lockstep batch: one h, q for all cells, batch-wide WRMS (R14, R15 order:
     per-cell sums, 256-cell block partials in order).  GPU (host control loop + device kernels)

@@ -14,7 +14,8 @@ import pytest
 RU = 8.31446261815324e7
 PATM = 1013250.0
 MECHS = {"h2_lidryer": ({"H2": 0.02852, "O2": 0.22635, "N2": 0.74513}, 1100.0),
-         "drm19_class": ({"CH4": 0.05519, "O2": 0.22015, "N2": 0.72466}, 1400.0)}
+         "drm19_class": ({"CH4": 0.05519, "O2": 0.22015, "N2": 0.72466}, 1400.0),
+         "gri53_class": ({"CH4": 0.05519, "O2": 0.22015, "N2": 0.72466}, 1400.0)}   # C5 (n = 54)
 
 
 def nasa(table, T):
