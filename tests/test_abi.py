@@ -48,7 +48,7 @@ def test_argument_validation_without_device(lib):
     assert (opt.qmax, opt.mode, opt.mxstep) == (5, 0, 10000)
     assert lib.bdfb_create(C.byref(h), 0, 3, 1e-6, ap, C.byref(opt), 0) == -1      # n_cells
     assert lib.bdfb_create(C.byref(h), 10, 0, 1e-6, ap, C.byref(opt), 0) == -1     # n
-    assert lib.bdfb_create(C.byref(h), 10, 33, 1e-6, ap, C.byref(opt), 0) == -1    # n > 32
+    assert lib.bdfb_create(C.byref(h), 10, 65, 1e-6, ap, C.byref(opt), 0) == -1    # n > 64
     assert lib.bdfb_create(C.byref(h), 10, 3, 0.0, ap, C.byref(opt), 0) == -1      # rtol
     bad = np.array([1e-10, -1.0, 1e-10])
     assert lib.bdfb_create(C.byref(h), 10, 3, 1e-6, bad.ctypes.data_as(C.POINTER(C.c_double)), C.byref(opt), 0) == -1
