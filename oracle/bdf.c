@@ -416,10 +416,69 @@ static int lsetup(cell *c, int convfail, int *jcur)
   return rv;
 }
 
-/* linear solve b <- M^{-1} b  (cvLsSolve dense with 2/(1+gamrat) / CVDiagSolve) */
-static int lsolve(cell *c, double *b)
+/* Inexact Newton-Krylov (approaches 1A/1B; reading R29): A v = v - gamma Jv with the
+ * difference-quotient Jv at the current Newton iterate y = zn0 + ycor (c->y) and fy = f(y) (c->ftemp):
+ * sigma = 1/||v||_WRMS, Jv = (f(y + sigma v) - fy) (1/sigma), at most 3 tries with sigma *= 1/4 after a
+ * recoverable RHS failure (CVODE cvLsDQJtimes); these RHS calls are not counted in nfe. */
+#define EPLIFAC 0.05     /* c_l of Eq. 6 */
+#define MAX_DQITERS 3
+static int atimes_dq(void *ctx, const double *v, double *z)
+{
+  cell *c = (cell *)ctx;
+  const int n = c->n;
+  double w[ORC_NMAX], fw[ORC_NMAX];
+  double sig = 1.0 / orc_wrms(n, v, c->ewt, c->o->group);
+  int r = 0;
+  for (int it = 0; it < MAX_DQITERS; ++it) {
+    for (int i = 0; i < n; ++i) w[i] = sig * v[i] + c->y[i];
+    r = orc_rhs(c->p, c->tn, w, fw);
+    if (r == 0) break;
+    if (r < 0) return -1;
+    sig = sig * 0.25;
+  }
+  if (r > 0) return 1;
+  const double siginv = 1.0 / sig;
+  for (int i = 0; i < n; ++i) {
+    const double jv = (fw[i] - c->ftemp[i]) * siginv;
+    z[i] = v[i] - c->gamma * jv;
+  }
+  return 0;
+}
+
+/* cvLsSolve, iterative branch: if ||b||_WRMS <= deltar = c_l tq[4] return x = b (first Newton iteration)
+ * or 0; else GMRES on the Eq. 5 system with S1 = S2 = diag(ewt) to the 2-norm tolerance deltar sqrt(n)
+ * (Eq. 6); RES_REDUCED is accepted on the first Newton iteration only; every other failure is recoverable. */
+static int lsolve_gmres(cell *c, double *b, int m)
+{
+  const int n = c->n;
+  const double deltar = EPLIFAC * c->tq[4];
+  const double bnorm = orc_wrms(n, b, c->ewt, c->o->group);
+  if (bnorm <= deltar) {
+    if (m > 0)
+      for (int i = 0; i < n; ++i) b[i] = 0.0;
+    return 0;
+  }
+  double ones = 0.0;
+  for (int i = 0; i < n; ++i) ones = ones + 1.0 * 1.0;
+  const double delta = deltar * sqrt(ones);
+  double x[ORC_NMAX], rn;
+  int nli = 0;
+  const int maxl = c->o->maxl > 0 ? c->o->maxl : 5;
+  const int r = orc_gmres(n, maxl, atimes_dq, c, b, c->ewt, c->ewt, delta, x, &nli, &rn);
+  c->st.nli += nli;
+  if (r == ORC_GMRES_ATIMES_FAIL_UNREC) return -1;
+  if (r == ORC_GMRES_SUCCESS || (r == ORC_GMRES_RES_REDUCED && m == 0)) {
+    for (int i = 0; i < n; ++i) b[i] = x[i];
+    return 0;
+  }
+  return 1;
+}
+
+/* linear solve b <- M^{-1} b  (cvLsSolve dense with 2/(1+gamrat) / CVDiagSolve / GMRES); m = Newton iteration */
+static int lsolve(cell *c, double *b, int m)
 {
   int n = c->n;
+  if (c->o->ls == ORC_LS_GMRES) return lsolve_gmres(c, b, m);
   if (c->o->ls != ORC_LS_DIAG) {
     for (long k = 0; k < c->ncell; ++k) {
       if (c->o->plain) orc_lu_solve_div(n, c->M + k * n * n, c->piv + k * n, b + k * n);
@@ -451,6 +510,13 @@ static int newton(cell *c, int nflag)
   int convfail = (nflag == FIRST_CALL || nflag == PREV_ERR_FAIL) ? CF_NONE : CF_OTHER;
   int setup = (nflag == PREV_CONV_FAIL) || (nflag == PREV_ERR_FAIL) || (c->st.nst == 0) ||
               (c->st.nst >= c->nstlp + MSBP) || (fabs(c->gamrat - 1.0) > DGMAX);
+  /* matrix-free GMRES without a preconditioner has no setup (CVODE sets lsetup = NULL): R = 1 at every
+   * solve, no matrix refresh and no retry after a failure (reading R29) */
+  const int msetup = c->o->ls != ORC_LS_GMRES;
+  if (!msetup) {
+    setup = 0;
+    c->crate = 1.0;
+  }
   double *ycor = c->ycor, *G = c->G;
   double tol = c->tq[4];
   int jcur = 0;
@@ -469,7 +535,8 @@ static int newton(cell *c, int nflag)
       for (;;) {                                                  /* N6 */
         c->st.nni++;
         for (long i = 0; i < n; ++i) G[i] = -G[i];
-        rv = lsolve(c, G);
+        rv = lsolve(c, G, m);
+        if (rv < 0) return NLS_RHS_UNREC;
         if (rv) break;
         for (long i = 0; i < n; ++i) ycor[i] = ycor[i] + G[i];
         double del = wrms(c, G);
@@ -490,7 +557,7 @@ static int newton(cell *c, int nflag)
       }
     }
     /* FAIL: retry once with a fresh Jacobian if it was not current */
-    if (rv > 0 && !jcur) {
+    if (rv > 0 && !jcur && msetup) {
       setup = 1;
       convfail = CF_BAD_J;
       for (long i = 0; i < n; ++i) ycor[i] = 0.0;
@@ -798,6 +865,7 @@ out:
 int orc_integrate(const orc_problem *p, const orc_opts *o, double t0, double tf,
                   double *y, orc_stats *st, orc_trace *tr)
 {
+  if (o->method == ORC_METHOD_ERK4) return orc_integrate_erk(p, o, t0, tf, y, st);
   cellbuf B;
   cell C;
   cell *c = &C;

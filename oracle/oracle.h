@@ -34,6 +34,7 @@ extern "C" {
 
 #define ORC_QMAX 5          /* listing §8c.1: QMAX */
 #define ORC_NMAX 64         /* largest system the oracle handles (n <= 64) */
+#define ORC_MAXL 64         /* largest GMRES Krylov dimension (the integrator uses maxl = 5) */
 
 /* ---- models -------------------------------------------- */
 enum {
@@ -46,7 +47,13 @@ enum {
 /* linear-solver choice inside Newton (P:399 dense direct, P:480 CVDiag) */
 /* ORC_LS_DENSE_DQ: dense direct solver with the difference-quotient Jacobian (the paper's approaches 3A/3B,
  * P:177-178) instead of the analytic one (2A/2B) */
-enum { ORC_LS_DENSE = 0, ORC_LS_DIAG = 1, ORC_LS_DENSE_DQ = 2 };
+/* ORC_LS_GMRES: inexact Newton-Krylov, scaled GMRES with the difference-quotient Jv product (approaches 1A/1B,
+ * Table 1, Eq. 5-6; krylov.c and lsolve_gmres in bdf.c) */
+enum { ORC_LS_DENSE = 0, ORC_LS_DIAG = 1, ORC_LS_DENSE_DQ = 2, ORC_LS_GMRES = 3 };
+
+/* time-integration method (orc_opts.method): CVODE BDF (default) or the explicit adaptive ERK of P:415-426
+ * (erk.c) */
+enum { ORC_METHOD_BDF = 0, ORC_METHOD_ERK4 = 1 };
 
 /* Jacobian source for the dense solver */
 enum { ORC_JAC_ANALYTIC = 0 /* model's exact J: closed form or complex step */ };
@@ -109,6 +116,8 @@ typedef struct {
   double hmin, hmax;     /* hmax <= 0 means infinity */
   int ls;                /* ORC_LS_DENSE | ORC_LS_DIAG | ORC_LS_DENSE_DQ */
   int group;             /* G: WRMS summation order emulation (R15); 1 = sequential */
+  int method;            /* ORC_METHOD_BDF | ORC_METHOD_ERK4 (orc_integrate dispatches on it) */
+  int maxl;              /* ORC_LS_GMRES: Krylov dimension cap (0 = 5, CVODE's default; reading R29) */
   int plain;             /* 1: the listing's plain arithmetic -- libm pow(x, 1.0/L) for the step-size
                             factors and true division in LU_SOLVE -- instead of readings R25/R16 (the
                             GPU's division-free root and reciprocal-multiply solve).  The GPU must match
@@ -121,6 +130,7 @@ typedef struct {
   int32_t q_last;
   double h_last;
   double t_reached;
+  int32_t nli;           /* ORC_LS_GMRES: linear (Krylov) iterations; their Jv RHS calls are not in nfe */
 } orc_stats;
 
 /* optional trace of accepted steps, for the Nordsieck invariant pin */
@@ -165,6 +175,26 @@ int orc_newton_once(const orc_problem *p, const orc_opts *o, double tn, double h
                     const double *zn0, const double *zn1, const double *ewt, double *acor, double *acnrm,
                     int *nni, int *nfe);
 
+/* Scaled GMRES (krylov.c; Eq. 5-6).  Solves A x = b through A~ = S1 A S2^-1 with S1 = diag(s1),
+ * S2 = diag(s2) (NULL = identity), zero initial guess, at most maxl (<= ORC_MAXL) iterations, no restarts;
+ * converged when the rotation residual ||S1 (b - A x)||_2 <= delta.  atimes(ctx, v, z) sets z = A v and
+ * returns 0, > 0 (recoverable failure) or < 0.  Outputs x, the iteration count and the final rotation
+ * residual.  Returns ORC_GMRES_*: SUCCESS; RES_REDUCED (cap reached, residual below ||S1 b||: x is the best
+ * iterate); CONV_FAIL; ATIMES_FAIL_REC / _UNREC; QRFACT_FAIL / QRSOL_FAIL (zero diagonal in the rotated
+ * Hessenberg matrix).                                                                                    */
+typedef int (*orc_atimes_fn)(void *ctx, const double *v, double *z);
+enum { ORC_GMRES_SUCCESS = 0, ORC_GMRES_RES_REDUCED = 1, ORC_GMRES_CONV_FAIL = 2, ORC_GMRES_ATIMES_FAIL_REC = 3,
+       ORC_GMRES_QRFACT_FAIL = 4, ORC_GMRES_QRSOL_FAIL = 5, ORC_GMRES_ATIMES_FAIL_UNREC = -1 };
+int orc_gmres(int n, int maxl, orc_atimes_fn atimes, void *ctx, const double *b, const double *s1,
+              const double *s2, double delta, double *x, int *nli, double *res_norm);
+
+/* Explicit adaptive ERK (erk.c): one step of the embedded 4(3) pair from (t, y)
+ * with step h: ynew (order 4) and err = h sum_i e_i k_i (the order-4 minus order-3 difference, the LTE
+ * estimate).  Returns 0 or the RHS status of the first failing stage.  nfe: RHS calls made (5, or 4 when
+ * k1 != NULL supplies f(t, y)).                                                                           */
+int orc_erk_step(const orc_problem *p, double t, double h, const double *y, const double *k1, double *ynew,
+                 double *err, int *nfe);
+
 /* f = R(t,y) + f_ext.  Returns 0, or >0 for a recoverable RHS failure. */
 int orc_rhs(const orc_problem *p, double t, const double *y, double *f);
 /* S_i: the RHS with |.| on every term (reading R19 parity scale). */
@@ -190,9 +220,14 @@ double orc_root(double x, int L);
 void orc_set_bdf(int q, double h, const double *tau /* [7], tau[1..6] */,
                  int qwait, double *l, double *tq);
 
-/* Integrate one cell from t0 to tf in place (y: [n]).  Returns status.   */
+/* Integrate one cell from t0 to tf in place (y: [n]).  Returns status.
+ * o->method == ORC_METHOD_ERK4 integrates with the explicit ERK (orc_integrate_erk).                     */
 int orc_integrate(const orc_problem *p, const orc_opts *o, double t0,
                   double tf, double *y, orc_stats *st, orc_trace *tr);
+
+/* The explicit adaptive ERK integration of one cell (erk.c; WRMS error control of Eq. 3 with the
+ * embedded estimate, reading R30).  Uses o->rtol, atol, mxstep, h0, hmin, hmax.  Returns status.         */
+int orc_integrate_erk(const orc_problem *p, const orc_opts *o, double t0, double tf, double *y, orc_stats *st);
 
 /* Global-norm mode: the N cells of a YC field integrated as one system with
  * batch-wide norms (see bdf.c).  fext YC or NULL, rho [N] or NULL.          */

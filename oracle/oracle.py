@@ -21,14 +21,16 @@ REPO = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 
 MODEL_LINEAR, MODEL_ROBERTSON, MODEL_KWH, MODEL_MECH = 0, 1, 2, 3
-LS_DENSE, LS_DIAG, LS_DENSE_DQ = 0, 1, 2
+LS_DENSE, LS_DIAG, LS_DENSE_DQ, LS_GMRES = 0, 1, 2, 3
+METHOD_BDF, METHOD_ERK4 = 0, 1
 STATUS = {0: "OK", 1: "TOO_MUCH_WORK", 2: "ERR_FAILURE", 3: "CONV_FAILURE", 4: "RHS_FAIL",
           5: "NONFINITE_INPUT"}
 QMAX = 5
 
 
 def build(force: bool = False) -> str:
-    srcs = [os.path.join(HERE, f) for f in ("bdf.c", "linalg.c", "models.c", "oracle.h", "mech_body.h")]
+    srcs = [os.path.join(HERE, f) for f in ("bdf.c", "linalg.c", "models.c", "krylov.c", "erk.c",
+                                              "oracle.h", "mech_body.h")]
     if force or not os.path.exists(LIB_PATH) or any(
             os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in srcs):
         subprocess.check_call(["make", "-s", "-C", HERE, "liboracle.so"])
@@ -58,13 +60,14 @@ class Problem(C.Structure):
 class Opts(C.Structure):
     _fields_ = [("rtol", C.c_double), ("atol", C.POINTER(C.c_double)), ("qmax", C.c_int),
                 ("mxstep", C.c_int64), ("h0", C.c_double), ("hmin", C.c_double), ("hmax", C.c_double),
-                ("ls", C.c_int), ("group", C.c_int), ("plain", C.c_int)]
+                ("ls", C.c_int), ("group", C.c_int), ("method", C.c_int), ("maxl", C.c_int),
+                ("plain", C.c_int)]
 
 
 class Stats(C.Structure):
     _fields_ = [("status", C.c_int32), ("nst", C.c_int32), ("nfe", C.c_int32), ("nje", C.c_int32),
                 ("nsetups", C.c_int32), ("nni", C.c_int32), ("netf", C.c_int32), ("ncfn", C.c_int32),
-                ("q_last", C.c_int32), ("h_last", C.c_double), ("t_reached", C.c_double)]
+                ("q_last", C.c_int32), ("h_last", C.c_double), ("t_reached", C.c_double), ("nli", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -74,6 +77,10 @@ class Trace(C.Structure):
     _fields_ = [("cap", C.c_int), ("count", C.c_int), ("tn", C.POINTER(C.c_double)),
                 ("h", C.POINTER(C.c_double)), ("q", C.POINTER(C.c_int)), ("zn", C.POINTER(C.c_double))]
 
+
+ATIMES = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double))
+GMRES_STATUS = {0: "SUCCESS", 1: "RES_REDUCED", 2: "CONV_FAIL", 3: "ATIMES_FAIL_REC", 4: "QRFACT_FAIL",
+                5: "QRSOL_FAIL", -1: "ATIMES_FAIL_UNREC"}
 
 _lib = None
 _lock = threading.Lock()
@@ -108,6 +115,15 @@ def lib():
             L.orc_newton_once.argtypes = [C.POINTER(Problem), C.POINTER(Opts), C.c_double, C.c_double,
                                           C.c_double, C.c_double, dp, dp, dp, dp, dp, C.POINTER(C.c_int),
                                           C.POINTER(C.c_int)]
+            L.orc_gmres.restype = C.c_int
+            L.orc_gmres.argtypes = [C.c_int, C.c_int, ATIMES, C.c_void_p, dp, dp, dp, C.c_double, dp,
+                                    C.POINTER(C.c_int), dp]
+            L.orc_erk_step.restype = C.c_int
+            L.orc_erk_step.argtypes = [C.POINTER(Problem), C.c_double, C.c_double, dp, dp, dp, dp,
+                                       C.POINTER(C.c_int)]
+            L.orc_integrate_erk.restype = C.c_int
+            L.orc_integrate_erk.argtypes = [C.POINTER(Problem), C.POINTER(Opts), C.c_double, C.c_double, dp,
+                                            C.POINTER(Stats)]
             L.orc_rhs.restype = C.c_int
             L.orc_rhs.argtypes = [C.POINTER(Problem), C.c_double, dp, dp]
             L.orc_rhs_scale.restype = C.c_int
@@ -207,6 +223,42 @@ def newton_once(model, zn0, zn1, ewt, h, rl1, tol, rho=1.0, fext=None, tn=0.0, a
     r = lib().orc_newton_once(C.byref(p), C.byref(o), float(tn), float(h), float(rl1), float(tol), _dp(zn0),
                               _dp(zn1), _dp(ewt), _dp(acor), C.byref(acn), C.byref(nni), C.byref(nfe))
     return r, acor, acn.value, nni.value, nfe.value
+
+
+def gmres(A, b, s1=None, s2=None, delta=0.0, maxl=None):
+    """Scaled GMRES of the oracle (orc_gmres, Eq. 5-6) on a dense matrix A or a callable v -> A v.
+    Returns (x, status, iterations, rotation residual)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    n = len(b)
+    Am = None if callable(A) else np.asarray(A, dtype=np.float64)
+
+    def _at(ctx, v, z):
+        vv = np.ctypeslib.as_array(v, shape=(n,)).copy()
+        zz = A(vv) if Am is None else Am @ vv
+        for i in range(n):
+            z[i] = float(zz[i])
+        return 0
+
+    cb = ATIMES(_at)
+    x = np.zeros(n)
+    it = C.c_int(0)
+    rn = C.c_double(0.0)
+    s1a = None if s1 is None else np.ascontiguousarray(s1, dtype=np.float64)
+    s2a = None if s2 is None else np.ascontiguousarray(s2, dtype=np.float64)
+    r = lib().orc_gmres(n, int(maxl or n), cb, None, _dp(b), _dp(s1a) if s1a is not None else None,
+                        _dp(s2a) if s2a is not None else None, float(delta), _dp(x), C.byref(it), C.byref(rn))
+    return x, r, it.value, rn.value
+
+
+def erk_step(model, y, h, rho=1.0, fext=None, t=0.0):
+    """One step of the embedded 4(3) pair (orc_erk_step): returns (ynew, err, status, nfe)."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    yn = np.zeros(model.n)
+    er = np.zeros(model.n)
+    nfe = C.c_int(0)
+    p = model.problem(rho, fext)
+    r = lib().orc_erk_step(C.byref(p), float(t), float(h), _dp(y), None, _dp(yn), _dp(er), C.byref(nfe))
+    return yn, er, r, nfe.value
 
 
 def root(x, L):
@@ -395,11 +447,12 @@ def kwh_state(model, e, rho):
     return dict(zip(["T", "nH0", "nHp", "nHe0", "nHep", "nHepp", "ne", "g"], out)), r
 
 
-def make_opts(n, rtol, atol, qmax=5, mxstep=10000, h0=0.0, hmin=0.0, hmax=0.0, ls=LS_DENSE, group=1, plain=False):
+def make_opts(n, rtol, atol, qmax=5, mxstep=10000, h0=0.0, hmin=0.0, hmax=0.0, ls=LS_DENSE, group=1, plain=False,
+              method=METHOD_BDF, maxl=0):
     """plain=True: the listing's plain arithmetic (libm pow roots, true division in LU_SOLVE) instead of
     readings R25/R16 -- the CUDA path must match both within the end-state band."""
     at = np.ascontiguousarray(np.broadcast_to(np.asarray(atol, dtype=np.float64), (n,)))
-    o = Opts(rtol, _dp(at), qmax, mxstep, h0, hmin, hmax, ls, group, 1 if plain else 0)
+    o = Opts(rtol, _dp(at), qmax, mxstep, h0, hmin, hmax, ls, group, method, maxl, 1 if plain else 0)
     o._keep = at
     return o
 
@@ -439,7 +492,8 @@ def integrate_global(model, y_yc, t0, tf, rtol, atol, rho=None, fext_yc=None, gr
     return y, st.as_dict()
 
 
-STAT_FIELDS = ["status", "nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn", "q_last", "h_last", "t_reached"]
+STAT_FIELDS = ["status", "nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn", "q_last", "h_last", "t_reached",
+               "nli"]
 
 
 def integrate_batch(model, y_yc, t0, tf, rtol, atol, rho=None, fext_yc=None, ls=None, group=1, threads=1,
