@@ -524,6 +524,9 @@ static int newton(cell *c, int nflag)
   for (;;) {
     int rv = residual(c, ycor, G);                               /* N4 */
     if (rv < 0) return NLS_RHS_UNREC;
+    /* a failed first residual (of the solve or of its retry) is not retried: SUNNonlinSol_Newton leaves its
+     * loop before the retry logic (reading R5; retrying would re-evaluate the same failing state forever) */
+    if (rv > 0) return NLS_RECOVERABLE;
     if (rv == 0 && setup) {
       rv = lsetup(c, convfail, &jcur);
       if (rv < 0) return NLS_RHS_UNREC;

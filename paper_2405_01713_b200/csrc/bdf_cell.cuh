@@ -629,7 +629,11 @@ struct Integrator {
           break;
         }
         case -3: {  // Newton residual f(tn, zn0 + ycor) ready
-          if (rv) { act = A_NFAIL; break; }
+          if (rv) {
+            if (s.m == 0) s.jcur = 1;   // a failed first residual is not retried (reading R5)
+            act = A_NFAIL;
+            break;
+          }
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             s.fy[r] = fr[r];

@@ -574,7 +574,11 @@ struct GroupIntegrator {
           break;
         }
         case -3: {  // Newton residual f(tn, zn0 + ycor) ready
-          if (rv) { act = X_NFAIL; break; }
+          if (rv) {   // a failed first residual is not retried (reading R5)
+            if (g.lane == 0 && s->m == 0) s->jcur = 1;
+            act = X_NFAIL;
+            break;
+          }
           V(c, g, V_FY) = fr;
           const double t = s->rl1 * V(c, g, V_ZN + 1) + V(c, g, V_ACOR);
           V(c, g, V_DEL) = -s->gamma * fr + t;

@@ -545,7 +545,10 @@ struct TpcIntegrator {
   __device__ static int consume(const Opts& o, TS& s, const W& w, int rv, const double (&fr)[N]) {
     switch (s.phase) {
       case PH_NRES: {  // Newton residual: G = (rl1 zn[1] + ycor) - gamma f(tn, zn0 + ycor)
-        if (rv) return A_NFAIL;
+        if (rv) {
+          if (s.m == 0) s.jcur = 1;   // a failed first residual is not retried (reading R5)
+          return A_NFAIL;
+        }
         const double rl1 = s.rl1, gm = s.gamma;
 #pragma unroll
         for (int i = 0; i < N; ++i) {

@@ -294,6 +294,7 @@ struct GlobalRunner {
     cudaMemsetAsync(B.v.acor, 0, sizeof(double) * M, st);
     for (;;) {
       int rv = residual();
+      if (rv > 0) return 1;   // a failed first residual is not retried (reading R5)
       if (rv == 0 && setup) {
         rv = lsetup(convfail, jcur);
         setup = 0;
