@@ -118,6 +118,8 @@ typedef struct {
   int64_t nst, nfe, nje, nsetups, nni, netf, ncfn;   /* sums over cells       */
   int64_t nst_max;           /* max over cells of nst                          */
   int64_t nfe_max;
+  int64_t nli;               /* GMRES linear (Krylov) iterations summed over cells; each made one
+                                RHS call for its Jv quotient, not counted in nfe (CVODE's nfeDQ) */
 } bdfb_stats;
 
 /* Optional per-cell outputs: device arrays of length N (any may be NULL). */
@@ -177,6 +179,39 @@ int bdfb_set_kernel(bdfb_batch *b, int32_t kernel);
 #define BDFB_JAC_ANALYTIC 0
 #define BDFB_JAC_DQ 1
 int bdfb_set_jacobian(bdfb_batch *b, int32_t mode);
+
+/* Linear solver of the Newton iteration (Table 1):
+ *  BDFB_LS_DENSE (default): modified Newton with the dense LU with partial pivoting of M = I - gamma J
+ *    (approaches 2A/2B with the analytic J, 3A/3B with BDFB_JAC_DQ).
+ *  BDFB_LS_DIAG: CVDiag, the diagonal difference-quotient approximation of J from one extra RHS call per
+ *    setup, M^-1 applied elementwise and updated exactly when gamma moves (the Nyx solver, here for
+ *    any n).  The setup's RHS call is counted in nfe and as one nje.
+ *  BDFB_LS_GMRES: inexact Newton-Krylov (approaches 1A/1B): no matrix setup, every Newton
+ *    iteration solves (I - gamma J) delta = -G by GMRES on the scaled system of Eq. 5 (S1 = S2 = diag of the
+ *    Eq. 3 weights, no preconditioner), stopping test Eq. 6 with c_l = 0.05 on the rotation residual,
+ *    J v by the difference quotient (f(y + sigma v) - f(y)) / sigma, sigma = 1 / ||v||_WRMS, at the current
+ *    Newton iterate; at most maxl Krylov iterations (1..5; 0 = 5, CVODE's default), no restarts.  Each
+ *    Krylov iteration is one RHS call (bdfb_stats.nli), not counted in nfe.
+ * DIAG and GMRES run in the SPLIT kernel of the mechanism models in per-cell mode (else BDFB_EUNSUPPORTED;
+ * BDFB_EINVAL for an unknown id, maxl out of range or a DQ Jacobian mode).  The slot pool is re-sized here
+ * (never in bdfb_integrate).  Readings R29 fix the details the paper leaves open.             */
+#define BDFB_LS_DENSE 0
+#define BDFB_LS_DIAG 1
+#define BDFB_LS_GMRES 2
+int bdfb_set_linear_solver(bdfb_batch *b, int32_t ls, int32_t maxl);
+
+/* Time-integration method:
+ *  BDFB_METHOD_BDF (default): the variable-order BDF of this header.
+ *  BDFB_METHOD_ERK4: explicit adaptive Runge-Kutta, "a fourth-order explicit method" from ARKODE
+ *    (P:415-426): the Zonneveld 5-stage 4(3) pair with the Eq. 3 WRMS error test on its embedded
+ *    estimate, no algebraic solver (nje = nsetups = nni = 0, q_last = 4); one cell per thread of a
+ *    persistent kernel (csrc/erk.cu), mxstep / h0 / hmin / hmax of bdfb_options apply.  Reading R30
+ *     fixes the tableau and the controller constants the paper leaves open.
+ * ERK4 runs the mechanism models in per-cell mode (else BDFB_EUNSUPPORTED); its workspace (8 n doubles per
+ * resident thread) is allocated here.  Call after bdfb_set_model.                                        */
+#define BDFB_METHOD_BDF 0
+#define BDFB_METHOD_ERK4 1
+int bdfb_set_method(bdfb_batch *b, int32_t method);
 
 /* The lane-group size G whose WRMS summation order (reading R15: lane l sums
  * components i = l (mod G) in increasing i, then an xor butterfly G/2..1)

@@ -159,6 +159,15 @@ class Batch:
         """"analytic" (default) or "dq": CVODE's difference-quotient dense Jacobian (bdfb_set_jacobian)."""
         _check(self._L.bdfb_set_jacobian(self.h, {"analytic": 0, "dq": 1}[mode]), self.h)
 
+    def set_method(self, method):
+        """"bdf" (default) or "erk4": the explicit adaptive ERK of P:415-426 (bdfb_set_method)."""
+        _check(self._L.bdfb_set_method(self.h, {"bdf": 0, "erk4": 1}[method]), self.h)
+
+    def set_linear_solver(self, ls, maxl=0):
+        """"dense" (default), "diag" (CVDiag) or "gmres" (inexact Newton-Krylov; maxl
+        Krylov iterations, 0 = 5) for the Newton iteration (bdfb_set_linear_solver)."""
+        _check(self._L.bdfb_set_linear_solver(self.h, {"dense": 0, "diag": 1, "gmres": 2}[ls], int(maxl)), self.h)
+
     @property
     def wrms_group(self):
         """Lane-group size of the WRMS summation order (reading R15) the selected kernel uses."""

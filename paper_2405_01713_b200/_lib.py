@@ -22,7 +22,7 @@ SYMBOLS = ["bdfb_default_options", "bdfb_create", "bdfb_set_model", "bdfb_set_ce
            "bdfb_destroy", "bdfb_last_error", "bdfb_version", "bdfb_eval_rhs", "bdfb_eval_jac",
            "bdfb_lu_factor_solve", "bdfb_probe_fp64", "bdfb_set_comm", "bdfb_set_kernel", "bdfb_wrms_group",
            "bdfb_phase_ms", "bdfb_minmax", "bdfb_set_atol_typical", "bdfb_set_jacobian",
-           "bdfb_split_lu_factor_solve"]
+           "bdfb_split_lu_factor_solve", "bdfb_set_linear_solver", "bdfb_set_method"]
 
 
 class Options(C.Structure):
@@ -33,7 +33,7 @@ class Options(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("n_cells", C.c_int64), ("n_failed", C.c_int64), ("nst", C.c_int64), ("nfe", C.c_int64),
                 ("nje", C.c_int64), ("nsetups", C.c_int64), ("nni", C.c_int64), ("netf", C.c_int64),
-                ("ncfn", C.c_int64), ("nst_max", C.c_int64), ("nfe_max", C.c_int64)]
+                ("ncfn", C.c_int64), ("nst_max", C.c_int64), ("nfe_max", C.c_int64), ("nli", C.c_int64)]
 
 
 class CellStats(C.Structure):
@@ -81,6 +81,10 @@ def lib():
     L.bdfb_last_launch_count.argtypes = [vp]
     L.bdfb_set_jacobian.restype = C.c_int
     L.bdfb_set_jacobian.argtypes = [vp, i32]
+    L.bdfb_set_method.restype = C.c_int
+    L.bdfb_set_method.argtypes = [vp, i32]
+    L.bdfb_set_linear_solver.restype = C.c_int
+    L.bdfb_set_linear_solver.argtypes = [vp, i32, i32]
     L.bdfb_minmax.restype = C.c_int
     L.bdfb_minmax.argtypes = [vp, vp, i32, vp, vp, vp]
     L.bdfb_set_atol_typical.restype = C.c_int

@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
-UNITS = ["bdfb.cu", "tpc.cu", "split.cu"]          # translation units, compiled in parallel
+UNITS = ["bdfb.cu", "tpc.cu", "split.cu", "split_mf.cu", "erk.cu"]          # translation units, compiled in parallel
 
 
 def sources():

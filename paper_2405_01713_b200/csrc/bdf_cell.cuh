@@ -66,6 +66,7 @@ struct CellStatsPtrs {
 
 struct Agg {  // device aggregate counters (unsigned long long for atomics)
   unsigned long long n_failed, nst, nfe, nje, nsetups, nni, netf, ncfn, nst_max, nfe_max, cells_done;
+  unsigned long long nli;   // GMRES linear iterations (SPLIT LS_GMRES only)
 };
 
 template <int N, int R>

@@ -73,8 +73,14 @@ namespace bdfb {
 #define BDFB_SPLIT_INIT_KERNEL 0   // measured slower on C4 (K_ctl+K_init 3.80 s vs K_ctl 3.34 s): kept as an option
 #endif
 
-// split-local phases: waiting for the setup kernels; finished, to be stored by K_init
-constexpr int PH_SETUP = 6, PH_STORE = 7;
+// split-local phases: waiting for the setup kernels; finished, to be stored by K_init; a Jv request of GMRES
+constexpr int PH_SETUP = 6, PH_STORE = 7, PH_KRY = 8;
+
+// linear solver inside the Newton iteration (bdfb_set_linear_solver; Table 1)
+enum : int { LS_DENSE = 0, LS_DIAG = 1, LS_GMRES = 2 };
+constexpr int KMAXL = 5;            // Krylov dimension of the VEC record (CVODE's default maxl; reading R29)
+constexpr double EPLIFAC = 0.05;    // c_l of Eq. 6
+constexpr int MAX_DQITERS = 3;      // Jv difference quotient: tries with sigma /= 4 after an RHS failure
 
 struct SplitBufs {
   double* vec;                 // S/32 * D * 32
@@ -89,6 +95,7 @@ struct SplitBufs {
   unsigned long long* live;    // [2]: live slots after the K_ctl of iteration it (it & 1)
   long long slots;             // S (multiple of 32)
   int jac_dq;                  // 1: difference-quotient Jacobian (K_dqjac) instead of the analytic one
+  int maxl;                    // LS_GMRES: Krylov iterations per linear solve, 1..KMAXL
 };
 
 // Substitutions of LU_SOLVE (listing; reading R16) on a column-major LU
@@ -136,12 +143,21 @@ __device__ __forceinline__ void lurec_substitute(const double* __restrict__ lu, 
   b[0] = b[0] * inv[0];
 }
 
-template <class Mech, class GM>
+template <class Mech, class GM, int LS = LS_DENSE>
 struct Split {
   static constexpr int N = Mech::N;
   using I = TpcIntegrator<Mech, GM, 32, false>;
   using W = typename I::W;
-  static constexpr int D = W::DOUBLES;
+  static constexpr int D0 = W::DOUBLES;
+  // extra VEC elements of the matrix-free linear solvers.  CVDiag: f at the setup point, gamma of the
+  // diagonal (M^-1 itself lives in W::invd).  GMRES: Krylov basis V[0..KMAXL] (scaled), fy = f(ycur), the
+  // rotated Hessenberg matrix H[KMAXL+1][KMAXL], Givens pairs, sigma, beta, rotation product, l, Jv retries,
+  // linear iterations of the cell.
+  static constexpr int X_FT = D0, X_GSV = D0 + N;
+  static constexpr int X_V = D0, X_FY = X_V + (KMAXL + 1) * N, X_H = X_FY + N, X_GIV = X_H + (KMAXL + 1) * KMAXL,
+                       X_SIG = X_GIV + 2 * KMAXL, X_BETA = X_SIG + 1, X_ROT = X_BETA + 1, X_L = X_ROT + 1,
+                       X_DQ = X_L + 1, X_NLI = X_DQ + 1, X_END = X_NLI + 1;
+  static constexpr int D = LS == LS_DENSE ? D0 : (LS == LS_DIAG ? ((D0 + N + 1 + 1) & ~1) : ((X_END + 1) & ~1));
   static constexpr int JREC = (N * N + 3) / 4 * 4;
   static constexpr int LU_INVD = N * N, LU_PERM = N * N + N;     // perm: ints at double offset LU_PERM
   static constexpr int LUREC = (N * N + N + (N + 1) / 2 + 3) / 4 * 4;
@@ -170,6 +186,11 @@ struct Split {
 #pragma unroll
       for (int i = 0; i < N; ++i) b[i] = sc * b[i];
     }
+    return newton_update(s, w, b);
+  }
+
+  // ycor += delta, ||delta|| and the Newton test of Eq. 4 (TpcIntegrator::solve's tail), for every linear solver
+  __device__ static int newton_update(TS& s, const W& w, double (&b)[N]) {
     double acc = 0.0, acc2 = 0.0;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -200,6 +221,277 @@ struct Split {
     return I::A_RET;
   }
 
+  // ---- CVDiag (LS_DIAG, listing "Variant for n=1 / C2" for any n; oracle lsetup/lsolve) ----------
+  // setup part 1 (at the matrix-setup decision; fr = f(y) of the residual just consumed): the perturbed
+  // state y + r (h f - zn[1]), r = FRACT rl1, is requested from K_rhs
+  __device__ static int diag_request(TS& s, const W& w) {
+    const double r = FRACT * s.rl1;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double ft0 = w.fr(i);
+      w.at(X_FT + i) = ft0;
+      const double ft = s.h * ft0 - w.zn(1, i);
+      w.yq(i) = r * ft + w.yq(i);
+    }
+    s.nje++;
+    s.jcur = 1;
+    s.tq_req = s.tn;
+    s.phase = PH_DIAG;
+    return I::A_RET;
+  }
+  // setup part 2: M_ii = (FRACT ft + (-h)(f(yp) - f(y))) / (FRACT ft) (1 when |ft w| < u), M^-1 into invd
+  __device__ static int diag_consume(TS& s, const W& w, int rv, const double (&fr)[N]) {
+    bool bad = rv != 0;
+    if (!bad) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        if (bad) continue;
+        const double ft0 = w.at(X_FT + i);
+        const double ft = s.h * ft0 - w.zn(1, i);
+        double Mi = 1.0;
+        if (fabs(ft * w.ewt(i)) >= UROUND) Mi = (FRACT * ft + (-s.h) * (fr[i] - ft0)) / (FRACT * ft);
+        if (Mi == 0.0) {
+          bad = true;
+        } else {
+          w.invd(i) = 1.0 / Mi;
+        }
+      }
+      w.at(X_GSV) = s.gamma;
+    }
+    I::setup_done(s);
+    return bad ? I::A_NFAIL : I::A_SOLVE;
+  }
+  // CVDiagSolve: M^-1 updated exactly when gamma moved since the setup; delta = M^-1 (-G) (no 2/(1+gamrat))
+  __device__ static int diag_solve(TS& s, const W& w) {
+    s.nni++;
+    const double gsv = w.at(X_GSV);
+    if (gsv != s.gamma) {
+      const double r = s.gamma / gsv;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double Mi = (1.0 / w.invd(i) + (-1.0)) * r + 1.0;
+        if (Mi == 0.0) return I::A_NFAIL;
+        w.invd(i) = 1.0 / Mi;
+      }
+      w.at(X_GSV) = s.gamma;
+    }
+    double b[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[i] = (-w.del(i)) * w.invd(i);
+    return newton_update(s, w, b);
+  }
+
+  // ---- inexact Newton-Krylov (LS_GMRES; oracle lsolve_gmres + orc_gmres, reading R29) ----------
+  // Scaled GMRES on A = I - gamma J with S1 = S2 = diag(ewt), J v by a difference quotient of the RHS at the
+  // Newton iterate ycur = zn0 + ycor: one K_rhs request per Krylov iteration (phase PH_KRY).
+  __device__ static double vdot(const W& w, int a, int b) {
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) t = t + w.at(a + i) * w.at(b + i);
+    return t;
+  }
+  __device__ static double& Hm(const W& w, int i, int j) { return w.at(X_H + i * KMAXL + j); }
+  // request f(ycur + sigma v), v = V_l / ewt (a fresh sigma = 1 / ||v||_WRMS when `fresh`)
+  __device__ static int kry_request(TS& s, const W& w, int l, bool fresh) {
+    double sig = w.at(X_SIG);
+    if (fresh) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double v = w.at(X_V + l * N + i) / w.ewt(i);
+        const double p = v * w.ewt(i);
+        acc = acc + p * p;
+      }
+      sig = 1.0 / sqrt(acc / (double)N);
+      w.at(X_SIG) = sig;
+      w.at(X_DQ) = 0.0;
+      w.at(X_L) = (double)l;
+      w.at(X_NLI) = w.at(X_NLI) + 1.0;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double v = w.at(X_V + l * N + i) / w.ewt(i);
+      w.yq(i) = sig * v + (w.zn(0, i) + w.acor(i));
+    }
+    s.tq_req = s.tn;
+    s.phase = PH_KRY;
+    return I::A_RET;
+  }
+  // x = S2^-1 sum_k y_k V_k from the rotated least-squares system (SUNQRsol), then the Newton update
+  __device__ static int kry_finish(TS& s, const W& w, int kdim) {
+    double g[KMAXL + 1];
+    g[0] = w.at(X_BETA);
+#pragma unroll
+    for (int i = 1; i <= KMAXL; ++i) g[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < KMAXL; ++j) {
+      if (j < kdim) {
+        const double c = w.at(X_GIV + 2 * j), sn = w.at(X_GIV + 2 * j + 1);
+        const double t1 = g[j], t2 = g[j + 1];
+        g[j] = c * t1 - sn * t2;
+        g[j + 1] = sn * t1 + c * t2;
+      }
+    }
+#pragma unroll
+    for (int j = KMAXL - 1; j >= 0; --j) {
+      if (j < kdim) {
+        const double hjj = Hm(w, j, j);
+        if (hjj == 0.0) return I::A_NFAIL;         // QRSOL_FAIL: recoverable
+        g[j] = g[j] / hjj;
+#pragma unroll
+        for (int i = 0; i < KMAXL; ++i)
+          if (i < j) g[i] = g[i] - g[j] * Hm(w, i, j);
+      }
+    }
+    double b[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double xc = 0.0;
+#pragma unroll
+      for (int k = 0; k < KMAXL; ++k)
+        if (k < kdim) xc = xc + g[k] * w.at(X_V + k * N + i);
+      b[i] = xc / w.ewt(i);
+    }
+    return newton_update(s, w, b);
+  }
+  // cvLsSolve (iterative): the small-residual exit, else GMRES from x0 = 0 with V0 = S1 b / beta
+  __device__ static int kry_start(TS& s, const W& w) {
+    s.nni++;
+    const double deltar = EPLIFAC * s.tol;
+    double b[N];
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      b[i] = -w.del(i);
+      const double p = b[i] * w.ewt(i);
+      acc = acc + p * p;
+    }
+    if (sqrt(acc / (double)N) <= deltar) {
+      if (s.m > 0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) b[i] = 0.0;
+      }
+      return newton_update(s, w, b);
+    }
+    const double delta = deltar * sqrt((double)N);
+    double bt = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double v = w.ewt(i) * b[i];
+      w.at(X_V + i) = v;
+      w.at(X_FY + i) = w.fr(i);
+      bt = bt + v * v;
+    }
+    const double beta = sqrt(bt);
+    if (beta <= delta) {       // SUCCESS with x = 0
+#pragma unroll
+      for (int i = 0; i < N; ++i) b[i] = 0.0;
+      return newton_update(s, w, b);
+    }
+#pragma unroll
+    for (int i = 0; i < (KMAXL + 1) * KMAXL; ++i) w.at(X_H + i) = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) w.at(X_V + i) = (1.0 / beta) * w.at(X_V + i);
+    w.at(X_BETA) = beta;
+    w.at(X_ROT) = 1.0;
+    return kry_request(s, w, 0, true);
+  }
+  // one Krylov iteration with the Jv RHS value fr: V_{l+1} = S1 (v - gamma Jv), MGS (SUNModifiedGS),
+  // Givens update (SUNQRfact), rotation residual test (Eq. 6); next request, or the solution
+  __device__ static int kry_consume(TS& s, const W& w, int rv, const double (&fr)[N], int maxl) {
+    const int l = (int)w.at(X_L);
+    if (rv) {                                        // cvLsDQJtimes: shrink sigma and retry
+      const double dq = w.at(X_DQ) + 1.0;
+      if (dq >= (double)MAX_DQITERS) return I::A_NFAIL;
+      w.at(X_DQ) = dq;
+      w.at(X_SIG) = w.at(X_SIG) * 0.25;
+      return kry_request(s, w, l, false);
+    }
+    const int k = l + 1;
+    {
+      const double siginv = 1.0 / w.at(X_SIG);
+      const double gm = s.gamma;
+      double vk = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double jv = (fr[i] - w.at(X_FY + i)) * siginv;
+        const double v = w.at(X_V + l * N + i) / w.ewt(i);
+        const double z = v - gm * jv;
+        const double t = w.ewt(i) * z;
+        w.at(X_V + k * N + i) = t;
+        vk = vk + t * t;
+      }
+      // modified Gram-Schmidt against V_0..V_l, with the re-orthogonalisation test (FACTOR 1000)
+      const double vk_norm = sqrt(vk);
+      for (int i0 = 0; i0 < k; ++i0) {
+        const double h = vdot(w, X_V + i0 * N, X_V + k * N);
+        Hm(w, i0, l) = h;
+#pragma unroll
+        for (int j = 0; j < N; ++j) w.at(X_V + k * N + j) = w.at(X_V + k * N + j) + (-h) * w.at(X_V + i0 * N + j);
+      }
+      double nv = sqrt(vdot(w, X_V + k * N, X_V + k * N));
+      double temp = 1000.0 * vk_norm;
+      if ((temp + nv) == temp) {
+        double nn2 = 0.0;
+        for (int i0 = 0; i0 < k; ++i0) {
+          const double np = vdot(w, X_V + i0 * N, X_V + k * N);
+          temp = 1000.0 * Hm(w, i0, l);
+          if ((temp + np) == temp) continue;
+          Hm(w, i0, l) = Hm(w, i0, l) + np;
+#pragma unroll
+          for (int j = 0; j < N; ++j)
+            w.at(X_V + k * N + j) = w.at(X_V + k * N + j) + (-np) * w.at(X_V + i0 * N + j);
+          nn2 = nn2 + np * np;
+        }
+        if (nn2 != 0.0) {
+          const double np = nv * nv - nn2;
+          nv = (np > 0.0) ? sqrt(np) : 0.0;
+        }
+      }
+      Hm(w, k, l) = nv;
+    }
+    // Givens: the previous rotations on column l, then a new one zeroing H[l+1][l]
+    for (int j = 0; j < l; ++j) {
+      const double c = w.at(X_GIV + 2 * j), sn = w.at(X_GIV + 2 * j + 1);
+      const double t1 = Hm(w, j, l), t2 = Hm(w, j + 1, l);
+      Hm(w, j, l) = c * t1 - sn * t2;
+      Hm(w, j + 1, l) = sn * t1 + c * t2;
+    }
+    const double t1 = Hm(w, l, l), t2 = Hm(w, l + 1, l);
+    double c, sn;
+    if (t2 == 0.0) {
+      c = 1.0;
+      sn = 0.0;
+    } else if (fabs(t2) >= fabs(t1)) {
+      const double t3 = t1 / t2;
+      sn = -1.0 / sqrt(1.0 + t3 * t3);
+      c = -sn * t3;
+    } else {
+      const double t3 = t2 / t1;
+      c = 1.0 / sqrt(1.0 + t3 * t3);
+      sn = -c * t3;
+    }
+    w.at(X_GIV + 2 * l) = c;
+    w.at(X_GIV + 2 * l + 1) = sn;
+    const double hll = c * t1 - sn * t2;
+    Hm(w, l, l) = hll;
+    if (hll == 0.0) return I::A_NFAIL;                 // QRFACT_FAIL: recoverable
+    const double rot = w.at(X_ROT) * sn;
+    w.at(X_ROT) = rot;
+    const double beta = w.at(X_BETA);
+    const double rho = fabs(rot * beta);
+    const double delta = EPLIFAC * s.tol * sqrt((double)N);
+    if (rho <= delta) return kry_finish(s, w, k);
+    if (k >= maxl) {   // cap: RES_REDUCED accepted on the first Newton iteration only (cvLsSolve)
+      if (rho < beta && s.m == 0) return kry_finish(s, w, k);
+      return I::A_NFAIL;
+    }
+    const double inv = 1.0 / Hm(w, k, l);
+#pragma unroll
+    for (int j = 0; j < N; ++j) w.at(X_V + k * N + j) = inv * w.at(X_V + k * N + j);
+    return kry_request(s, w, k, true);
+  }
+
   // the trip after the setup decision (both passes): SOLVE .. ATTEMPT, in the
   // stage order of TpcIntegrator::trip.  Returns A_RET (RHS requested) or A_DONE.
   // DEFER_STORE: a finished cell is not stored here; it is marked PH_STORE and returns A_STORE (K_init
@@ -208,7 +500,11 @@ struct Split {
   __device__ static int finish(const Opts& o, TS& s, const W& w, int act, const double* lu, double* y,
                                const double* fext, const double* aux, const double* atol,
                                unsigned long long* counter, Agg& acc, const CellStatsPtrs& cs) {
-    if (act == I::A_SOLVE) act = solve(s, w, lu);
+    if (act == I::A_SOLVE) {
+      if constexpr (LS == LS_DENSE) act = solve(s, w, lu);
+      else if constexpr (LS == LS_DIAG) act = diag_solve(s, w);
+      else act = kry_start(s, w);
+    }
     if (act == I::A_NFAIL) act = I::nfail(o, s, w);
     if (act == I::A_ERRTEST) act = I::errtest(o, s, w);
     if (act == I::A_STEP_TOP) act = I::step_top(o, s, w);
@@ -217,6 +513,10 @@ struct Split {
       return act;
     }
     if (act == I::A_STORE) {
+      if constexpr (LS == LS_GMRES) {   // the cell's linear iterations (aggregate only), reset for the next cell
+        if (s.status != ST_NONFINITE) atomicAdd(&acc.nli, (unsigned long long)w.at(X_NLI));
+        w.at(X_NLI) = 0.0;
+      }
       I::store(o, s, w, y, acc, cs);
       act = I::A_LOAD;
     }
@@ -227,7 +527,7 @@ struct Split {
 };
 
 // initialise the pool: every slot empty (phase DONE)
-template <class Mech, class GM>
+template <class Mech, class GM, int LS = LS_DENSE>
 __global__ void split_init_kernel(SplitBufs b) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s == 0) {
@@ -235,7 +535,8 @@ __global__ void split_init_kernel(SplitBufs b) {
     for (int i = 0; i < 6; ++i) b.cnt[i] = 0;
   }
   if (s >= b.slots) return;
-  TS* t = Split<Mech, GM>::ts(b, s);
+  TS* t = Split<Mech, GM, LS>::ts(b, s);
+  if constexpr (LS == LS_GMRES) Split<Mech, GM, LS>::ws(b, s).at(Split<Mech, GM, LS>::X_NLI) = 0.0;
   t->phase = PH_DONE;
   t->flag = 0;
   t->pend = 0;
@@ -248,11 +549,11 @@ __global__ void split_init_kernel(SplitBufs b) {
 // trip stopped at a matrix setup (phase PH_SETUP) resumes after it: the setup
 // kernels ran in between, so the trip costs the cell one extra iteration
 // (its RHS slot idles once) instead of a latency-bound second pass.
-template <class Mech, class GM>
+template <class Mech, class GM, int LS = LS_DENSE>
 __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     split_ctl_kernel(Opts o, SplitBufs b, int it, double* y, const double* fext, const double* aux,
                      const double* atol, unsigned long long* counter, Agg* agg, CellStatsPtrs cs) {
-  using SP = Split<Mech, GM>;
+  using SP = Split<Mech, GM, LS>;
   using I = typename SP::I;
   constexpr int N = Mech::N;
   extern __shared__ double smem[];           // TS records of the block's threads (TS_STRIDE each)
@@ -346,17 +647,30 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     } else if (run) {
       double fr[N];
       int rv = 0;
-      if (s.phase == PH_INIT || s.phase == PH_HIN || s.phase == PH_NRES || s.phase == PH_ETF3) {
+      const int ph = s.phase;
+      if (ph == PH_INIT || ph == PH_HIN || ph == PH_NRES || ph == PH_ETF3 || (LS == LS_DIAG && ph == PH_DIAG) ||
+          (LS == LS_GMRES && ph == PH_KRY)) {
         rv = b.rv[slot];
-        s.nfe++;
+        if (ph != PH_KRY) s.nfe++;   // the Jv quotients' RHS calls are not counted in nfe (CVODE's nfeDQ)
 #pragma unroll
         for (int i = 0; i < N; ++i) fr[i] = w.fr(i);
       }
-      act = I::consume(o, s, w, rv, fr);
+      if (LS == LS_DIAG && ph == PH_DIAG) {
+        act = SP::diag_consume(s, w, rv, fr);
+      } else if (LS == LS_GMRES && ph == PH_KRY) {
+        act = SP::kry_consume(s, w, rv, fr, b.maxl);
+      } else {
+        if (LS == LS_GMRES && ph == PH_NRES && s.m == 0) {   // no setup for matrix-free GMRES: R = 1 per solve,
+          s.crate = 1.0;                                     // no matrix refresh, no retry (reading R29)
+          s.setup = 0;
+          s.jcur = 1;
+        }
+        act = I::consume(o, s, w, rv, fr);
+      }
       if (act == I::A_HIN_FINISH) act = I::hin_finish(o, s);
       if (act == I::A_START) act = I::start(o, s, w);
-      if (act == I::A_SETUP) act = I::setup_decide(s);
-      if (act == I::A_SETUP_J || act == I::A_SETUP_LU) {
+      if (act == I::A_SETUP) act = (LS == LS_DIAG) ? SP::diag_request(s, w) : I::setup_decide(s);
+      if (LS == LS_DENSE && (act == I::A_SETUP_J || act == I::A_SETUP_LU)) {
         s.pend = act;
         s.coop = 0;
         s.phase = PH_SETUP;
@@ -414,6 +728,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     atomicMax(&agg->nst_max, a.nst_max);
     atomicMax(&agg->nfe_max, a.nfe_max);
     atomicAdd(&agg->cells_done, a.cells_done);
+    if (LS == LS_GMRES) atomicAdd(&agg->nli, a.nli);
   }
 }
 
@@ -422,13 +737,13 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
 // load the next one from the work counter (f(t0, y0) requested), or consume a cvHin RHS value (h0 by cvHin;
 // once h0 is set, start, step_top and the first ATTEMPT: the first Newton residual requested).  The state
 // is accessed in place (TS record L1-cached; the SoA rows of scattered slots: rare work).
-template <class Mech, class GM>
+template <class Mech, class GM, int LS = LS_DENSE>
 __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_init_cells_kernel(Opts o, SplitBufs b, int it, double* y,
                                                                            const double* fext, const double* aux,
                                                                            const double* atol,
                                                                            unsigned long long* counter, Agg* agg,
                                                                            CellStatsPtrs cs) {
-  using SP = Split<Mech, GM>;
+  using SP = Split<Mech, GM, LS>;
   using I = typename SP::I;
   constexpr int N = Mech::N;
   __shared__ double satol[N];
@@ -496,9 +811,9 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_init_cells_kernel(Opts
 // i into the cell's column-major J record; status -> TS.coop (nonzero:
 // recoverable failure).  Shared scratch per group: RHS scratch SG + the
 // Jacobian's per-reaction partials JG.
-template <class Mech, class GM>
+template <class Mech, class GM, int LS = LS_DENSE>
 __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_kernel(SplitBufs b, int it) {
-  using SP = Split<Mech, GM>;
+  using SP = Split<Mech, GM, LS>;
   constexpr int N = Mech::N, G = GM::G;
   constexpr int MS = N | 1;                      // odd row stride of the shared J (conflict-free)
   extern __shared__ double smem[];
@@ -531,9 +846,9 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_kernel(SplitBufs b
 // minInc = 1000 |h| u n fnorm (1 if fnorm = 0), inc = max(srur |y_j|, minInc / ewt_j),
 // J(:, j) = (1/inc) f(y + inc e_j) + (-(1/inc)) fy, f = the generated RHS + F -- the oracle's orc_jac_dq
 // operation for operation.  An RHS failure marks the cell (TS.coop = 1: a recoverable setup failure).
-template <class Mech, class GM>
+template <class Mech, class GM, int LS = LS_DENSE>
 __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, 3) split_dqjac_kernel(SplitBufs b, int it) {
-  using SP = Split<Mech, GM>;
+  using SP = Split<Mech, GM, LS>;
   constexpr int N = Mech::N;
   const long long cnt = (long long)b.cnt[3 * (it & 1) + 1] * N, stride = (long long)gridDim.x * BDFB_SPLIT_BLOCK;
   for (long long t = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; t < cnt; t += stride) {
@@ -680,9 +995,9 @@ __device__ __forceinline__ int oct_factor(unsigned gmask, int gl, double (&a)[(N
 // K_lu: one setup-list entry per group of 8 lanes (grid-stride); M = I - gamma J
 // from the cell's column-major J, oct_factor, factors stored column-major in
 // pivoted row order + 1/U_kk + perm, as the Newton solve of K_ctl reads them.
-template <class Mech, class GM>
+template <class Mech, class GM, int LS = LS_DENSE>
 __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b, int it) {
-  using SP = Split<Mech, GM>;
+  using SP = Split<Mech, GM, LS>;
   constexpr int N = Mech::N, R = (N + OCT - 1) / OCT;
   const int lane = threadIdx.x & 31, gl = lane & (OCT - 1);
   const unsigned gmask = 0xffu << (lane & ~(OCT - 1));
@@ -726,15 +1041,17 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b,
 #ifndef BDFB_SPLIT_RHS_MINB
 #define BDFB_SPLIT_RHS_MINB 3   // 168 registers, 12 warps/SM: 7% faster than 255 registers / 8 warps (measured)
 #endif
-template <class Mech, class GM>
+template <class Mech, class GM, int LS = LS_DENSE>
 __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_RHS_MINB) split_rhs_kernel(SplitBufs b, int it) {
-  using SP = Split<Mech, GM>;
+  using SP = Split<Mech, GM, LS>;
   constexpr int N = Mech::N;
   const long long stride = (long long)gridDim.x * BDFB_SPLIT_BLOCK;
   for (long long slot = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; slot < b.slots; slot += stride) {
     const TS* t = SP::ts(b, slot);
     const int ph = t->phase;
-    if (!(ph == PH_INIT || ph == PH_HIN || ph == PH_NRES || ph == PH_ETF3)) continue;
+    if (!(ph == PH_INIT || ph == PH_HIN || ph == PH_NRES || ph == PH_ETF3 || (LS == LS_DIAG && ph == PH_DIAG) ||
+          (LS == LS_GMRES && ph == PH_KRY)))
+      continue;
     const typename SP::W w = SP::ws(b, slot);
     double yv[N], fv[N];
 #pragma unroll

@@ -32,6 +32,7 @@
 #include "tpc_api.h"
 #include "bdf_split.cuh"
 #include "split_api.h"
+#include "erk_api.h"
 
 using namespace bdfb;
 
@@ -68,6 +69,11 @@ struct bdfb_batch {
   std::vector<cudaEvent_t> sev;           // split: per-phase timing events of one launch batch
   std::vector<cudaEvent_t> xev;           // split overlap: ordering events between the two streams
   int jac_mode = BDFB_JAC_ANALYTIC;       // bdfb_set_jacobian
+  int ls = BDFB_LS_DENSE;                 // bdfb_set_linear_solver (SPLIT)
+  int maxl = 5;                           // GMRES Krylov cap
+  int method = BDFB_METHOD_BDF;           // bdfb_set_method
+  double* d_erk = nullptr;                // ERK per-thread workspace (resident grid)
+  long long erk_threads = 0;
   cudaStream_t st2 = nullptr;             // split overlap: stream of K_jac + K_lu (BDFB_SPLIT_OVERLAP=1)
   double phase_ms[8] = {};                // split: device ms per phase of the last integrate
   int nphases = 0;
@@ -127,7 +133,7 @@ static void free_split(bdfb_batch* b) {
 static int prepare_split(bdfb_batch* b) {
   cudaError_t e = cudaSetDevice(b->device);
   SplitGeom gm{};
-  if (e == cudaSuccess) e = split_geometry(b->model, b->device, &gm);
+  if (e == cudaSuccess) e = split_geometry(b->model, b->ls, b->device, &gm);
   if (e != cudaSuccess) return cuda_fail(b, e, "split geometry");
   long long cap = 393216;   // measured on C4: 196608 2.51M, 262144 2.65M, 393216 2.78M, 524288 2.76M, 786432 2.79M cells/s
   if (const char* env = getenv("BDFB_SPLIT_SLOTS")) cap = atoll(env) > 0 ? atoll(env) : cap;
@@ -136,7 +142,7 @@ static int prepare_split(bdfb_batch* b) {
   if (S != b->sb.slots || gm.vec_doubles != b->sgeom.vec_doubles || gm.lurec != b->sgeom.lurec) {
     free_split(b);
     bool ok = true;
-    auto A = [&](void** p, size_t bytes) { if (ok && cudaMalloc(p, bytes) != cudaSuccess) ok = false; };
+    auto A = [&](void** p, size_t bytes) { if (ok && bytes && cudaMalloc(p, bytes) != cudaSuccess) ok = false; };
     A((void**)&b->sb.vec, sizeof(double) * (size_t)gm.vec_doubles * S);
     A((void**)&b->sb.ts, sizeof(double) * (size_t)gm.ts_doubles * S);
     A((void**)&b->sb.J, sizeof(double) * (size_t)gm.jrec * S);
@@ -154,6 +160,7 @@ static int prepare_split(bdfb_batch* b) {
     b->sb.slots = S;
   }
   b->sb.jac_dq = b->jac_mode == BDFB_JAC_DQ ? 1 : 0;
+  b->sb.maxl = b->maxl;
   if (!b->h_live && cudaHostAlloc((void**)&b->h_live, sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess)
     return fail(b, BDFB_ENOMEM, "pinned live counter");
   b->sgeom = gm;
@@ -188,7 +195,7 @@ static int launch_split(bdfb_batch* b, const Opts& o, double* y, const double* f
           return fail(b, BDFB_ECUDA, "ordering events");
     }
   }
-  cudaError_t e = split_integrate(b->model, o, y, fext, aux, b->d_atol, b->sb, b->sgeom, b->d_counter, b->d_agg,
+  cudaError_t e = split_integrate(b->model, b->ls, o, y, fext, aux, b->d_atol, b->sb, b->sgeom, b->d_counter, b->d_agg,
                                   b->cs, b->h_live, batch, st, &launches, b->sev.data(), b->phase_ms,
                                   overlap ? b->st2 : nullptr, overlap ? b->xev.data() : nullptr);
   b->nphases = SPLIT_PHASES;
@@ -199,7 +206,40 @@ static int launch_split(bdfb_batch* b, const Opts& o, double* y, const double* f
   return BDFB_OK;
 }
 
+static int prepare_erk(bdfb_batch* b) {
+  long long threads = 0, dpt = 0;
+  cudaError_t e = cudaSetDevice(b->device);
+  if (e == cudaSuccess) e = erk_geometry(b->model, b->device, b->ncells, &threads, &dpt);
+  if (e != cudaSuccess) return cuda_fail(b, e, "ERK geometry");
+  if (threads != b->erk_threads) {
+    if (b->d_erk) cudaFree(b->d_erk);
+    b->d_erk = nullptr;
+    b->erk_threads = 0;
+    if (cudaMalloc(&b->d_erk, sizeof(double) * (size_t)dpt * threads) != cudaSuccess)
+      return fail(b, BDFB_ENOMEM, "ERK workspace");
+    b->erk_threads = threads;
+  }
+  return BDFB_OK;
+}
+
+static int launch_erk(bdfb_batch* b, const Opts& o, double* y, const double* fext, const double* aux,
+                      cudaStream_t st) {
+  if (b->erk_threads < 1) return fail(b, BDFB_ENOMODEL, "ERK workspace not prepared");
+  cudaMemsetAsync(b->d_counter, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(b->d_agg, 0, sizeof(Agg), st);
+  cudaEventRecord(b->ev0, st);
+  cudaError_t e = erk_integrate(b->model, o, y, fext, aux, b->d_atol, b->d_erk, b->erk_threads, b->d_counter,
+                                b->d_agg, b->cs, st);
+  cudaEventRecord(b->ev1, st);
+  if (e != cudaSuccess) return cuda_fail(b, e, "ERK launch");
+  b->launches = 1;
+  b->nphases = 0;
+  b->timed = true;
+  return BDFB_OK;
+}
+
 static int prepare_kernel(bdfb_batch* b) {
+  if (b->method == BDFB_METHOD_ERK4) return prepare_erk(b);
   if (b->opt.mode == BDFB_MODE_PER_CELL && use_split(b)) return prepare_split(b);
   if (b->opt.mode != BDFB_MODE_PER_CELL || !use_tpc(b)) return BDFB_OK;
   long long slots = 0, dps = 0, ips = 0;
@@ -326,6 +366,7 @@ void bdfb_destroy(bdfb_batch* b) {
   if (b->d_aux) cudaFree(b->d_aux);
   if (b->d_ws) cudaFree(b->d_ws);
   if (b->d_iws) cudaFree(b->d_iws);
+  if (b->d_erk) cudaFree(b->d_erk);
   free_split(b);
   if (b->h_live) cudaFreeHost(b->h_live);
   for (auto ev : b->sev) cudaEventDestroy(ev);
@@ -397,9 +438,34 @@ int bdfb_set_jacobian(bdfb_batch* b, int32_t mode) {
   if (mode != BDFB_JAC_ANALYTIC && mode != BDFB_JAC_DQ) return fail(b, BDFB_EINVAL, "bad Jacobian mode");
   if (mode == BDFB_JAC_DQ && !(use_split(b) && b->opt.mode == BDFB_MODE_PER_CELL))
     return fail(b, BDFB_EUNSUPPORTED, "the difference-quotient Jacobian needs the SPLIT mechanism kernel");
+  if (mode == BDFB_JAC_DQ && b->ls != BDFB_LS_DENSE)
+    return fail(b, BDFB_EINVAL, "the difference-quotient Jacobian belongs to the dense linear solver");
   b->jac_mode = mode;
   b->sb.jac_dq = mode == BDFB_JAC_DQ ? 1 : 0;
   return BDFB_OK;
+}
+
+int bdfb_set_method(bdfb_batch* b, int32_t method) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (method != BDFB_METHOD_BDF && method != BDFB_METHOD_ERK4) return fail(b, BDFB_EINVAL, "bad method");
+  if (method == BDFB_METHOD_ERK4 && !(is_mech(b->model) && b->opt.mode == BDFB_MODE_PER_CELL))
+    return fail(b, BDFB_EUNSUPPORTED, "the explicit ERK runs the mechanism models (MECH_H2, MECH_DRM19) per cell");
+  b->method = method;
+  return prepare_kernel(b);
+}
+
+int bdfb_set_linear_solver(bdfb_batch* b, int32_t ls, int32_t maxl) {
+  if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
+  if (ls != BDFB_LS_DENSE && ls != BDFB_LS_DIAG && ls != BDFB_LS_GMRES) return fail(b, BDFB_EINVAL, "bad linear solver");
+  if (ls == BDFB_LS_GMRES && (maxl < 0 || maxl > KMAXL)) return fail(b, BDFB_EINVAL, "maxl must be in 0..5");
+  if (ls != BDFB_LS_DENSE) {
+    if (!(use_split(b) && b->opt.mode == BDFB_MODE_PER_CELL))
+      return fail(b, BDFB_EUNSUPPORTED, "CVDiag / GMRES run in the SPLIT mechanism kernel in per-cell mode");
+    if (b->jac_mode != BDFB_JAC_ANALYTIC) return fail(b, BDFB_EINVAL, "CVDiag / GMRES take no dense Jacobian mode");
+  }
+  b->ls = ls;
+  b->maxl = (ls == BDFB_LS_GMRES && maxl > 0) ? maxl : KMAXL;
+  return prepare_kernel(b);
 }
 
 int32_t bdfb_wrms_group(const bdfb_batch* b) {
@@ -579,6 +645,8 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
   if (model_needs_aux(b->model) && !aux) return fail(b, BDFB_EINVAL, "this model needs aux (density)");
   if (b->jac_mode == BDFB_JAC_DQ && !(use_split(b) && b->opt.mode == BDFB_MODE_PER_CELL))
     return fail(b, BDFB_EUNSUPPORTED, "the difference-quotient Jacobian needs the SPLIT mechanism kernel");
+  if (b->ls != BDFB_LS_DENSE && !(use_split(b) && b->opt.mode == BDFB_MODE_PER_CELL))
+    return fail(b, BDFB_EUNSUPPORTED, "CVDiag / GMRES run in the SPLIT mechanism kernel in per-cell mode");
   cudaSetDevice(b->device);
   Opts o;
   o.rtol = b->rtol;
@@ -602,6 +670,7 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
       default: return fail(b, BDFB_EUNSUPPORTED, "global-norm mode: group models only (MECH_H2, MECH_DRM19)");
     }
   }
+  if (b->method == BDFB_METHOD_ERK4) return launch_erk(b, o, y, f_ext, aux, st);
   switch (b->model) {
     case BDFB_MODEL_LINEAR: return launch_integrate<ModelLinear>(b, o, y, f_ext, aux, st);
     case BDFB_MODEL_ROBERTSON: return launch_integrate<ModelRobertson>(b, o, y, f_ext, aux, st);
@@ -676,6 +745,7 @@ extern "C" int64_t bdfb_get_stats(bdfb_batch* b, bdfb_stats* agg) {
     agg->ncfn = (int64_t)h.ncfn;
     agg->nst_max = (int64_t)h.nst_max;
     agg->nfe_max = (int64_t)h.nfe_max;
+    agg->nli = (int64_t)h.nli;
   }
   return (int64_t)h.n_failed;
 }

@@ -17,7 +17,9 @@ struct SplitGeom {
   int vec_doubles, ts_doubles, jrec, lurec;   // doubles per slot of the VEC, TS, J and LU records
 };
 
-cudaError_t split_geometry(int mech, int device, SplitGeom* gm);
+// ls: LS_DENSE | LS_DIAG | LS_GMRES (bdf_split.cuh); the matrix-free solvers are built in split_mf.cu
+cudaError_t split_geometry(int mech, int ls, int device, SplitGeom* gm);
+cudaError_t split_mf_geometry(int mech, int ls, int device, SplitGeom* gm);
 
 // Integrate all o.ncells cells through the slot pool sb (host loop over
 // K_ctl/K_rhs launch batches of `batch` iterations on st, one live-count read
@@ -27,11 +29,17 @@ cudaError_t split_geometry(int mech, int device, SplitGeom* gm);
 // st2 (or NULL): a second stream on which K_jac and K_lu run, overlapping K_rhs
 // (they touch disjoint slots); xev: 2 * batch ordering events for it.
 constexpr int SPLIT_PHASES = 4;
-cudaError_t split_integrate(int mech, const Opts& o, double* y, const double* fext, const double* aux,
+cudaError_t split_integrate(int mech, int ls, const Opts& o, double* y, const double* fext, const double* aux,
                             const double* atol, const SplitBufs& sb, const SplitGeom& gm, unsigned long long* counter,
                             Agg* agg, const CellStatsPtrs& cs, unsigned long long* h_live, int batch,
                             cudaStream_t st, int* launches, cudaEvent_t* events, double* phase_ms,
                             cudaStream_t st2, cudaEvent_t* xev);
+
+cudaError_t split_mf_integrate(int mech, int ls, const Opts& o, double* y, const double* fext, const double* aux,
+                               const double* atol, const SplitBufs& sb, const SplitGeom& gm,
+                               unsigned long long* counter, Agg* agg, const CellStatsPtrs& cs,
+                               unsigned long long* h_live, int batch, cudaStream_t st, int* launches,
+                               cudaEvent_t* events, double* phase_ms);
 
 // LU diagnostic with the SPLIT path's routines (oct_factor + the Newton
 // solve's substitutions); n in {2,4,6,8,10,12,16,22,32}; rec: N *
