@@ -137,26 +137,38 @@ def unit_flops(cfg):
         f_rhs, f_jac = 12, 10
     else:  # nyx_kwh: ~12 regula-falsi evaluations x (~16 transcendental + 40 arith) + cooling sum
         f_rhs, f_jac = 12 * (16 * w["exp"] + 40) + 20 * w["exp"] + 60, 0
+    # krylov: one GMRES iteration besides its RHS call (Jv quotient and scaling 6n, modified Gram-Schmidt against
+    # ~2 basis vectors 8n, norm 2n, Givens ~20); erk_attempt: the stage combinations 14n, the solution 8n, the
+    # error estimate 10n and its norm 3n of one ERK attempt
     return {"rhs": f_rhs, "jac": f_jac, "setup": (2 * (n - 1) * n * (2 * n - 1)) // 6 + n * (n - 1) // 2 + n + 2 * n * n,
-            "solve": 2 * n * n - n + 9 * n, "attempt": 26 * n + 60, "step": 11 * n + 80}
+            "solve": 2 * n * n - n + 9 * n, "attempt": 26 * n + 60, "step": 11 * n + 80, "krylov": 16 * n + 20,
+            "erk_attempt": 35 * n + 20}
 
 
-def phase_flops(cfg, st):
+def phase_flops(cfg, st, method="bdf", ls="dense"):
     """Algorithmic FP64 flops of one integrate per SPLIT kernel phase (the whole step is their sum):
     K_rhs = nfe F_rhs, K_jac = nje F_jac, K_lu = nsetups F_setup, K_ctl = Newton solves + vector passes +
     control.  Global-norm mode: batch counters, every batch step does the work for every cell."""
     u = unit_flops(cfg)
     att = st["nst"] + st["netf"] + st["ncfn"]
-    ph = {"rhs": st["nfe"] * u["rhs"], "jac": st["nje"] * u["jac"], "lu": st["nsetups"] * u["setup"],
-          "ctl": st["nni"] * u["solve"] + att * u["attempt"] + st["nst"] * u["step"]}
+    if method == "erk4":   # one kernel: RHS calls and the stage algebra; no algebraic solver
+        return {"rhs": st["nfe"] * u["rhs"], "ctl": (st["nst"] + st["netf"]) * u["erk_attempt"]}
+    nli = st.get("nli", 0)   # GMRES: one RHS call per Krylov iteration (Jv quotient)
+    ph = {"rhs": (st["nfe"] + nli) * u["rhs"], "jac": st["nje"] * u["jac"], "lu": st["nsetups"] * u["setup"],
+          "ctl": st["nni"] * u["solve"] + att * u["attempt"] + st["nst"] * u["step"] + nli * u["krylov"]}
+    if ls != "dense":      # matrix-free: no J, no LU; CVDiag's setup is one RHS call (in nfe) + 6n, its solve 2n
+        n = CONFIGS[cfg][2]
+        ph["jac"], ph["lu"] = 0, 0
+        ph["ctl"] = st["nni"] * (2 * n + 9 * n) + st["nsetups"] * 6 * n + att * u["attempt"] + st["nst"] * u["step"] + \
+            nli * u["krylov"]
     if cfg in GLOBAL_CFGS:
         ph = {k: v * st["n_cells"] for k, v in ph.items()}
     return ph
 
 
-def flop_model(cfg, st):
+def flop_model(cfg, st, method="bdf"):
     """Algorithmic FP64 flops of one integrate (whole step) from the aggregate per-cell statistics."""
-    return sum(phase_flops(cfg, st).values())
+    return sum(phase_flops(cfg, st, method).values())
 
 
 def hbm_bytes_global(cfg, st):
@@ -266,11 +278,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle
-def oracle_cells_per_s(cfg, budget_s=15.0, threads=None, rank_cells=None, steps=1):
-    """Time the CPU oracle (as it stands) on a bounded stratified sample of the workload."""
+def oracle_cells_per_s(cfg, budget_s=15.0, threads=None, rank_cells=None, steps=1, dt=None, solver=None):
+    """Time the CPU oracle (as it stands) on a bounded uniform random sample of the workload's cells
+    (an unbiased estimate of the per-cell cost).  solver: oracle options (ls, maxl, method)."""
     from oracle import oracle as O
-    from synth.fields import stratified_sample
-    model, mech, n, L, dt, rtol, atol, _ = CONFIGS[cfg]
+    model, mech, n, L, dt0, rtol, atol, _ = CONFIGS[cfg]
+    dt = dt or dt0
+    solver = solver or {}
     threads = threads or os.cpu_count() or 1
     if cfg in GLOBAL_CFGS:
         # the lockstep batch is one system: the oracle's global variant on a contiguous sub-batch, 1 thread
@@ -297,24 +311,22 @@ def oracle_cells_per_s(cfg, budget_s=15.0, threads=None, rank_cells=None, steps=
         idx = np.arange(len(idx))
     else:
         from synth import flame_field
-        # stratified by flame progress over a 2M-cell window of the grid
-        cand = np.arange(min(L ** 3, 1 << 21))
-        _, _, _, prog = flame_field(mech, L, cells=cand, dt=dt, forcing=False)
-        pick = stratified_sample(prog, 40000)
-        y, rho, F, _ = flame_field(mech, L, cells=cand[pick], dt=dt)
+        # a uniform random sample of the grid's cells (seeded): the workload's own mix of fresh, reacting and
+        # burnt cells
+        pick = np.sort(np.random.default_rng(2405017130).choice(L ** 3, min(L ** 3, 40000), replace=False))
+        y, rho, F, _ = flame_field(mech, L, cells=pick, dt=dt)
         om, G = O.Model.mechanism(mech), CONFIGS_G[cfg]
         idx = np.arange(len(pick))
 
     def run(sel):
         t = time.perf_counter()
         O.integrate_batch(om, y[:, sel], 0.0, dt, rtol, atol, rho=None if rho is None else rho[sel],
-                          fext_yc=None if F is None else F[:, sel], group=G, threads=threads)
+                          fext_yc=None if F is None else F[:, sel], group=G, threads=threads, **solver)
         return time.perf_counter() - t
 
     probe = idx[: min(len(idx), 512)]
     tp = run(probe)
     m = int(min(len(idx), max(len(probe), len(probe) * budget_s / max(tp, 1e-6))))
-    # interleave strata: take every k-th cell so the sample keeps the class mix
     sel = idx[np.linspace(0, len(idx) - 1, m).astype(int)]
     times = [run(sel) for _ in range(steps)]
     return m, times, threads
@@ -340,18 +352,35 @@ def main():
                     help="per-cell kernel organisation of the mechanism models (default: the library's)")
     ap.add_argument("--jac", default="analytic", choices=["analytic", "dq"],
                     help="Jacobian: analytic (2A/2B) or CVODE's difference quotient (3A/3B; SPLIT kernel)")
+    ap.add_argument("--ls", default="dense", choices=["dense", "diag", "gmres"],
+                    help="Newton linear solver: dense LU (2A/3A), CVDiag (P:480) or GMRES (1A; SPLIT kernel)")
+    ap.add_argument("--maxl", type=int, default=0, help="GMRES Krylov cap (0 = 5)")
+    ap.add_argument("--method", default="bdf", choices=["bdf", "erk4"],
+                    help="bdf (default) or the explicit adaptive ERK of P:415-426")
+    ap.add_argument("--dt", type=float, default=0.0, help="override the config's dt_CFD")
     args = ap.parse_args()
 
     from paper_2405_01713_b200 import parallel as PL
     rank, world, local = PL.env_rank()
     cfg = args.config
     model, mech, n, L, dt, rtol, atol, desc = CONFIGS[cfg]
+    if args.dt:
+        desc = desc.replace("dt_CFD %g s" % dt, "dt_CFD %g s" % args.dt)
+        dt = args.dt
+    from oracle import oracle as _O   # constants only (solver ids); the product path never calls it
+    solver = {}
+    if args.ls != "dense":
+        solver.update(ls={"diag": _O.LS_DIAG, "gmres": _O.LS_GMRES}[args.ls], maxl=args.maxl)
+        desc += ", %s linear solver" % {"diag": "CVDiag", "gmres": "GMRES (inexact Newton-Krylov, 1A)"}[args.ls]
+    if args.method == "erk4":
+        solver.update(method=_O.METHOD_ERK4, mxstep=1000000)
+        desc += ", explicit ERK 4(3) (P:415-426)"
 
     if args.impl == "reference":
         if rank != 0:
             return
         m, times, thr = oracle_cells_per_s(cfg, budget_s=max(5.0, 60.0 / max(args.steps, 1)), steps=args.warmup +
-                                           args.steps)
+                                           args.steps, dt=dt, solver=solver)
         times = times[args.warmup:] or times
         tt = sum(times)
         val = m * len(times) / tt
@@ -362,7 +391,7 @@ def main():
                 "cpu_baseline": {"value": val, "unit": UNIT, "cores": thr, "kind": "oracle",
                                  "sample": (f"first {m} cells of the {cfg} field as one lockstep batch per step"
                                             if cfg in GLOBAL_CFGS else
-                                            f"{m} stratified cells of the {cfg} workload per step")},
+                                            f"{m} uniformly sampled cells of the {cfg} workload per step")},
                 "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -381,12 +410,17 @@ def main():
     y0, rho, F, prog = make_inputs(cfg, rank, args.cells or None, world, scaling)
     N = y0.shape[1]
     glob_mode = cfg in GLOBAL_CFGS
-    b = P.Batch(N, n, rtol, atol, device=local, mode=P.MODE_GLOBAL_NORM if glob_mode else P.MODE_PER_CELL)
+    b = P.Batch(N, n, rtol, atol, device=local, mode=P.MODE_GLOBAL_NORM if glob_mode else P.MODE_PER_CELL,
+                mxstep=1000000 if args.method == "erk4" else 10000)
     if args.kernel and mech:
         b.set_kernel(args.kernel)
     b.set_model(model)
     if args.jac != "analytic":
         b.set_jacobian(args.jac)
+    if args.ls != "dense":
+        b.set_linear_solver(args.ls, args.maxl)
+    if args.method != "bdf":
+        b.set_method(args.method)
     if glob_mode and world > 1:
         # one lockstep system across ranks: the library's own NCCL communicator carries the norms
         uid = torch.cuda.nccl.unique_id() if rank == 0 else None
@@ -444,7 +478,7 @@ def main():
     except Exception:
         pass
     tw = transc_weights()
-    pf = [phase_flops(cfg, s) for s in stats]
+    pf = [phase_flops(cfg, s, args.method, args.ls) for s in stats]
     flops = [sum(p.values()) for p in pf]
     whole = statistics.mean(f / (k * 1e-3) for f, k in zip(flops, kern_ms)) / 1e12
     roof_common = {"bound": "alu", "pipe": "fp64", "peak": peak, "unit": "TFLOP/s",
@@ -456,10 +490,12 @@ def main():
                                   "ms": statistics.mean(kern_ms)}}
     kname = (("integrate_tpc_kernel<Tpc_%s>" if b.wrms_group == 1 else "integrate_group_kernel<ModelMech<%s>>")
              % mech) if mech else "integrate_kernel<%s>" % model
+    if args.method == "erk4":
+        kname = "erk_kernel<Tpc_%s>" % mech
     roof = dict(roof_common, achieved=whole, frac=whole / peak, traffic=traffic_per_launch(cfg, N), kernel=kname,
                 kernel_ms=statistics.mean(kern_ms), flops_per_launch=statistics.mean(flops))
     phases = None
-    if phase_ms and phase_ms[0]:
+    if phase_ms and phase_ms[0] and args.method == "bdf":
         # SPLIT: four kernels per trip, timed per phase with CUDA events on the launch stream.  The roofline is
         # the dominant kernel's algorithmic FP64 fraction; the whole-step fraction sits beside it; K_ctl's HBM
         # traffic (its slot-state round trips, an implementation cost, not algorithmic bytes) is a diagnostic.
@@ -469,8 +505,8 @@ def main():
         phases = {}
         for k, v in pm.items():
             fl = statistics.mean(p[k] for p in pf)
-            phases[k] = {"ms": v, "share": v / tot, "flops": fl, "tflops": fl / (v * 1e-3) / 1e12,
-                         "frac": fl / (v * 1e-3) / 1e12 / peak}
+            tfl = fl / (v * 1e-3) / 1e12 if v > 0 else 0.0
+            phases[k] = {"ms": v, "share": v / tot, "flops": fl, "tflops": tfl, "frac": tfl / peak}
         cb = statistics.mean(ctl_bytes(cfg, s) for s in stats)
         phases["ctl"]["hbm_model"] = {"bytes": cb, "gbs": cb / (pm["ctl"] * 1e-3) / 1e9,
                                       "frac": cb / (pm["ctl"] * 1e-3) / 1e9 / hpk, "peak_source": src,
@@ -517,9 +553,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        m, times, thr = oracle_cells_per_s(cfg, budget_s=15.0)
+        m, times, thr = oracle_cells_per_s(cfg, budget_s=15.0, dt=dt, solver=solver)
         smp = (f"first {m} cells of the {cfg} field integrated as one lockstep batch (orc_integrate_global), one pass"
-               if glob_mode else f"{m} stratified cells of the {cfg} workload (same recipe and seed), one pass")
+               if glob_mode else f"{m} uniformly sampled cells of the {cfg} workload (same recipe and seed), one pass")
         cpu = {"value": m / times[0], "unit": UNIT, "cores": thr, "kind": "oracle", "sample": smp}
 
     s = PL.reduce_stats(stats[-1], dist, dev)
@@ -537,14 +573,15 @@ def main():
                                          "block-cyclic 16^3 tiles"),
                            "l2": "inputs larger than L2 (state %.2f GB per GPU); pristine field restored "
                                  "untimed before each step" % (y0.nbytes / 1e9),
-                           "mechanism": mech, "jacobian": args.jac},
+                           "mechanism": mech, "jacobian": args.jac, "linear_solver": args.ls,
+                           "method": args.method},
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": n_total / (e2e_total / args.steps * 1e-3), "unit": UNIT,
                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(y0.nbytes)},
                 "gpu_launches": args.steps * b.last_launch_count(),
                 "clocks": clk.summary(),
                 "stats": {k: s[k] for k in ("n_cells", "n_failed", "nst", "nfe", "nje", "nsetups", "nni", "netf",
-                                            "ncfn", "nst_max")},
+                                            "ncfn", "nst_max", "nli") if k in s},
                 "kernel_ms_per_step": kern_ms, "phases": phases}
         print(json.dumps(line), flush=True)
     if dist:

@@ -20,7 +20,9 @@ CSRC = os.path.join(PKG, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
-UNITS = ["bdfb.cu", "tpc.cu", "split.cu", "split_mf.cu", "erk.cu"]          # translation units, compiled in parallel
+UNITS = ["bdfb.cu", "tpc.cu", "split.cu", "split_mf.cu", "erk.cu", "rhs.cu"]
+# contraction (a*b + c -> DFMA) only where the parity bar allows it: the generated RHS kernels (R19)
+UNIT_FMAD = {}   # measured: -fmad=true for rhs.cu made K_rhs 3% slower (more spills; profiles/r2/history.md)
 
 
 def sources():
@@ -43,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(PKG, "build", u.replace(".cu", ".o"))
         os.makedirs(os.path.dirname(obj), exist_ok=True)
         objs.append(obj)
-        procs.append(subprocess.Popen([NVCC] + ARCH + FLAGS + ["-c", "-o", obj, os.path.join(CSRC, u)],
+        fl = [UNIT_FMAD.get(u, f) if f == "-fmad=false" else f for f in FLAGS]
+        procs.append(subprocess.Popen([NVCC] + ARCH + fl + ["-c", "-o", obj, os.path.join(CSRC, u)],
                                       stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
     info, err = [], None
     for u, p in zip(UNITS, procs):

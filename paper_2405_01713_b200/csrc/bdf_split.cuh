@@ -1041,12 +1041,25 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b,
 #ifndef BDFB_SPLIT_RHS_MINB
 #define BDFB_SPLIT_RHS_MINB 3   // 168 registers, 12 warps/SM: 7% faster than 255 registers / 8 warps (measured)
 #endif
-template <class Mech, class GM, int LS = LS_DENSE>
-__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, BDFB_SPLIT_RHS_MINB) split_rhs_kernel(SplitBufs b, int it) {
+// VAR 0: 128-thread blocks, 3 per SM, free-running warps; VAR 1: the same with a block barrier per
+// grid-stride trip; VAR 2: one 384-thread block per SM with a barrier per trip, so that all 12 warps of an SM
+// walk the ~10K-instruction generated RHS together (instruction-cache locality; see erk.cu)
+template <int VAR>
+struct RhsVar {
+  static constexpr int BLOCK = VAR == 2 ? 384 : BDFB_SPLIT_BLOCK;
+  static constexpr int MINB = VAR == 2 ? 1 : BDFB_SPLIT_RHS_MINB;
+  static constexpr bool SYNC = VAR != 0;
+};
+template <class Mech, class GM, int LS = LS_DENSE, int VAR = 0>
+__global__ void __launch_bounds__(RhsVar<VAR>::BLOCK, RhsVar<VAR>::MINB) split_rhs_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM, LS>;
+  using V = RhsVar<VAR>;
   constexpr int N = Mech::N;
-  const long long stride = (long long)gridDim.x * BDFB_SPLIT_BLOCK;
-  for (long long slot = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; slot < b.slots; slot += stride) {
+  const long long stride = (long long)gridDim.x * V::BLOCK;
+  for (long long s0 = (long long)blockIdx.x * V::BLOCK; s0 < b.slots; s0 += stride) {   // block-uniform trips
+    if (V::SYNC) __syncthreads();
+    const long long slot = s0 + threadIdx.x;
+    if (slot >= b.slots) continue;
     const TS* t = SP::ts(b, slot);
     const int ph = t->phase;
     if (!(ph == PH_INIT || ph == PH_HIN || ph == PH_NRES || ph == PH_ETF3 || (LS == LS_DIAG && ph == PH_DIAG) ||

@@ -12,7 +12,8 @@
 // counter.  Each thread is a flat state machine whose only RHS call site is shared by every phase
 // (f(t0, y0), the initial-step probe, k1 after an accepted step, stages 2..5), so a warp's lanes -- at
 // different steps of different cells -- always evaluate the generated straight-line RHS
-// (gen/tpc_<mech>.cuh) together: full warps on the FP64 pipe, no algebraic solver, no shared memory.
+// (gen/tpc_<mech>.cuh) together, and a block barrier per trip keeps the block's 12 warps in the same
+// stretch of that code (one block per SM): full warps on the FP64 pipe, no algebraic solver.
 // The cell's vectors (y, F, k1..k5, weights: 8n doubles) live in a per-thread workspace sized for the
 // resident grid, element-major across threads (one coalesced 256-byte line pair per warp access; 80 MB
 // for DRM19 on 148 SMs, L2-resident).
@@ -28,11 +29,14 @@
 namespace bdfb {
 namespace {
 
+// one block of 12 warps per SM, block-synchronous RHS calls: the generated RHS is ~10K instructions of
+// straight-line SASS; warps at different places in it thrash the instruction cache (ncu, 128-thread
+// blocks without the barrier: 38 of 49 stall cycles per issue "no instruction", IPC 0.23)
 #ifndef BDFB_ERK_BLOCK
-#define BDFB_ERK_BLOCK 128
+#define BDFB_ERK_BLOCK 384
 #endif
 #ifndef BDFB_ERK_MINB
-#define BDFB_ERK_MINB 3
+#define BDFB_ERK_MINB 1
 #endif
 
 constexpr double ERK_SAFETY = 0.9, ERK_ETAMX1 = 1e4, ERK_ETAMX = 10.0, ERK_ETAMIN = 0.1, ERK_ETACF = 0.25;
@@ -69,6 +73,46 @@ __device__ __forceinline__ double wnorm_k(const EW<N>& w, int s) {   // ||k_s||_
   return sqrt(acc / (double)N);
 }
 
+// the request of a phase, the generated RHS and f + F into its k slot (k1 for f(t0, y0) and f(tn, yn), k2 for
+// the initial-step probe, k_s for stage s), out of line: the register-hungry RHS gets its own allocation and
+// the state machine around it stays light
+template <class Mech>
+__device__ __noinline__ int erk_eval(const EW<Mech::N> w, int phase, double hs, double h0, double rho) {
+  constexpr int N = Mech::N;
+  double yv[N], fv[N];
+  int dst = 0;
+  if (phase == R_F0 || phase == R_K1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) yv[i] = w.y(i);
+  } else if (phase == R_H0) {
+    dst = 1;
+#pragma unroll
+    for (int i = 0; i < N; ++i) yv[i] = h0 * w.k(0, i) + w.y(i);
+  } else {                       // stage s = phase - R_K1 (1..4): y + h sum_{j<s, a_sj != 0} a_sj k_j
+    const int st = phase - R_K1;
+    dst = st;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double acc = 0.0;
+      bool first = true;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double a = kErkA[st][j];
+        if (j < st && a != 0.0) {
+          const double tj = a * w.k(j, i);
+          acc = first ? tj : acc + tj;
+          first = false;
+        }
+      }
+      yv[i] = hs * acc + w.y(i);
+    }
+  }
+  const int rv = Mech::rhs(yv, rho, fv);
+#pragma unroll
+  for (int i = 0; i < N; ++i) w.k(dst, i) = fv[i] + w.F(i);
+  return rv;
+}
+
 struct ES {   // scalar state of a thread's cell (15 doubles)
   double rho, t, h, hs, h0, d1, etamax, hlast;
   long long cell;
@@ -100,11 +144,18 @@ __global__ void __launch_bounds__(BDFB_ERK_BLOCK, BDFB_ERK_MINB)
   etamax = ERK_ETAMX1;
   nef = ncf = last = 0;
   phase = R_NONE;
+  bool alive = true;
   for (;;) {
-    if (phase == R_NONE) {   // load the next cell
+    if (alive && phase == R_NONE) {   // load the next cell
       const long long c = (long long)atomicAdd(counter, 1ull);
-      if (c >= o.ncells) break;
-      cell = c;
+      if (c >= o.ncells) alive = false;
+      else cell = c;
+    }
+    // the block's warps enter the RHS together (instruction-cache locality); the block retires with its last cell
+    if (!__syncthreads_or(alive)) break;
+    if (!alive) continue;
+    if (phase == R_NONE) {
+      const long long c = cell;
       rho = aux ? aux[c] : 0.0;
       bool bad = !isfinite(rho);
 #pragma unroll
@@ -124,32 +175,7 @@ __global__ void __launch_bounds__(BDFB_ERK_BLOCK, BDFB_ERK_MINB)
     }
     if (phase >= 0) {
       // ---- the single RHS call site: build the request vector of this phase
-      double yv[N], fv[N];
-      if (phase == R_F0 || phase == R_K1) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) yv[i] = w.y(i);
-      } else if (phase == R_H0) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) yv[i] = h0 * w.k(0, i) + w.y(i);
-      } else {                       // stage s = phase - R_K1 (1..4): y + h sum_{j<s, a_sj != 0} a_sj k_j
-        const int st = phase - R_K1;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          double acc = 0.0;
-          bool first = true;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const double a = kErkA[st][j];
-            if (j < st && a != 0.0) {
-              const double tj = a * w.k(j, i);
-              acc = first ? tj : acc + tj;
-              first = false;
-            }
-          }
-          yv[i] = hs * acc + w.y(i);
-        }
-      }
-      const int rv = Mech::rhs(yv, rho, fv);
+      const int rv = erk_eval<Mech>(w, phase, hs, h0, rho);
       nfe++;
       // ---- consume
       if (phase == R_F0 || phase == R_K1) {
@@ -158,7 +184,6 @@ __global__ void __launch_bounds__(BDFB_ERK_BLOCK, BDFB_ERK_MINB)
           phase = -1;
         } else {
 #pragma unroll
-          for (int i = 0; i < N; ++i) w.k(0, i) = fv[i] + w.F(i);
           if (phase == R_F0) {
             if (o.h0 != 0.0) {
               h = o.h0;
@@ -187,7 +212,7 @@ __global__ void __launch_bounds__(BDFB_ERK_BLOCK, BDFB_ERK_MINB)
           double acc = 0.0;
 #pragma unroll
           for (int i = 0; i < N; ++i) {
-            const double d = (fv[i] + w.F(i)) - w.k(0, i);
+            const double d = w.k(1, i) - w.k(0, i);
             const double p = d * w.ewt(i);
             acc = acc + p * p;
           }
@@ -210,8 +235,6 @@ __global__ void __launch_bounds__(BDFB_ERK_BLOCK, BDFB_ERK_MINB)
             phase = -4;
           }
         } else {
-#pragma unroll
-          for (int i = 0; i < N; ++i) w.k(st, i) = fv[i] + w.F(i);
           if (phase < R_S5) {
             phase++;
           } else {             // all five stages: solution, estimate, error test

@@ -41,6 +41,16 @@ cudaError_t split_mf_integrate(int mech, int ls, const Opts& o, double* y, const
                                unsigned long long* h_live, int batch, cudaStream_t st, int* launches,
                                cudaEvent_t* events, double* phase_ms);
 
+// K_rhs launch and occupancy (rhs.cu, the -fmad=true translation unit; explicit instantiations for both
+// mechanisms and the three linear solvers)
+template <class Mech, class GM, int LS>
+cudaError_t split_rhs_run(unsigned grid, cudaStream_t st, const SplitBufs& b, int it);
+template <class Mech, class GM, int LS>
+cudaError_t split_rhs_occupancy(int* blocks_per_sm);
+// f = R(y) + F with the K_rhs code (rhs.cu), YC layout
+cudaError_t tpc_eval_rhs(int mech, long long N, const double* y, const double* fext, const double* aux, double* f,
+                         int* status, cudaStream_t st);
+
 // LU diagnostic with the SPLIT path's routines (oct_factor + the Newton
 // solve's substitutions); n in {2,4,6,8,10,12,16,22,32}; rec: N *
 // split_lu_rec_doubles(n) doubles of device scratch.

@@ -30,9 +30,7 @@ struct SplitK {
       return e;
     int nsm = 0, pr = 0;
     if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pr, split_rhs_kernel<Mech, GM, LS>, BDFB_SPLIT_BLOCK, 0)) !=
-        cudaSuccess)
-      return e;
+    if ((e = split_rhs_occupancy<Mech, GM, LS>(&pr)) != cudaSuccess) return e;
     if (pr < 1) return cudaErrorInvalidConfiguration;
     if (LS == LS_DENSE && jac_smem() > 48 * 1024 &&
         (e = cudaFuncSetAttribute(split_jac_kernel<Mech, GM, LS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -112,7 +110,7 @@ struct SplitK {
           cudaEventRecord(xev[2 * k + 1], st2);
           last_l = xev[2 * k + 1];
         }
-        split_rhs_kernel<Mech, GM, LS><<<grhs, blk, 0, st>>>(b, it);
+        split_rhs_run<Mech, GM, LS>(grhs, st, b, it);
         if (events) cudaEventRecord(ev[4], st);
         n += (LS == LS_DENSE) ? 4 : 2;
       }

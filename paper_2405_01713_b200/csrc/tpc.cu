@@ -10,6 +10,7 @@
 #include "gen/tpc_h2_lidryer.cuh"
 #include "mech_model.cuh"
 #include "tpc_api.h"
+#include "split_api.h"
 
 namespace bdfb {
 
@@ -145,6 +146,7 @@ cudaError_t tpc_integrate(int mech, const Opts& o, double* y, const double* fext
 
 cudaError_t tpc_eval(int mech, long long N, const double* y, const double* fext, const double* aux, double* f,
                      int* status, double* J, cudaStream_t st) {
+  if (J == nullptr) return tpc_eval_rhs(mech, N, y, fext, aux, f, status, st);   // the K_rhs code (rhs.cu)
   switch (mech) {
     case BDFB_MODEL_MECH_H2: return eval<Tpc_h2_lidryer>(N, y, fext, aux, f, status, J, st);
     case BDFB_MODEL_MECH_DRM19: return eval<Tpc_drm19_class>(N, y, fext, aux, f, status, J, st);

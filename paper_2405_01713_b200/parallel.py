@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import os
 
-STAT_SUM = ("n_cells", "n_failed", "nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn")
+STAT_SUM = ("n_cells", "n_failed", "nst", "nfe", "nje", "nsetups", "nni", "netf", "ncfn", "nli")
 STAT_MAX = ("nst_max", "nfe_max")
 
 
