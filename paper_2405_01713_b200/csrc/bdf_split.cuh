@@ -98,14 +98,41 @@ struct SplitBufs {
   int maxl;                    // LS_GMRES: Krylov iterations per linear solve, 1..KMAXL
 };
 
+// LU record layout: 1 = each slot's record contiguous (a thread streams its own record with 16-byte loads;
+// every warp load touches 32 lines); 32 = warp-blocked SoA like VEC, element e of slot s at
+// LU[((s/32) LUREC + e) 32 + s%32] (a warp load of one element is one coalesced 256-byte access)
+#ifndef BDFB_SPLIT_LU_SOA
+#define BDFB_SPLIT_LU_SOA 0   // measured on C4: K_ctl -4% but K_lu 1.05 -> 2.22 s (scattered 8-byte writes): off
+#endif
+constexpr int LU_STRIDE = BDFB_SPLIT_LU_SOA ? 32 : 1;
+
 // Substitutions of LU_SOLVE (listing; reading R16) on a column-major LU
 // record (factors in pivoted row order | 1/U_kk | perm), b already permuted:
 // unit-L forward substitution column by column, then the back substitution
 // with the reciprocal diagonal -- the operations and order of the oracle's
 // orc_lu_solve.  Shared by the Newton solve of K_ctl and the LU diagnostic.
-template <int N>
+// S: element stride of the record (LU_STRIDE).
+template <int N, int S>
 __device__ __forceinline__ void lurec_substitute(const double* __restrict__ lu, double (&b)[N]) {
   constexpr int LU_INVD = N * N;
+  if constexpr (S != 1) {
+#pragma unroll
+    for (int k = 0; k < N - 1; ++k) {         // unit-L forward substitution, column k
+#pragma unroll
+      for (int i = k + 1; i < N; ++i) b[i] = fma(-lu[(k * N + i) * S], b[k], b[i]);
+    }
+    double inv[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) inv[i] = lu[(LU_INVD + i) * S];
+#pragma unroll
+    for (int k = N - 1; k > 0; --k) {         // back substitution, column k, reciprocal diagonal
+      b[k] = b[k] * inv[k];
+#pragma unroll
+      for (int i = 0; i < k; ++i) b[i] = fma(-lu[(k * N + i) * S], b[k], b[i]);
+    }
+    b[0] = b[0] * inv[0];
+    return;
+  }
   const double2* col = reinterpret_cast<const double2*>(lu);
 #pragma unroll
   for (int k = 0; k < N - 1; ++k) {           // unit-L forward substitution, column k
@@ -160,7 +187,15 @@ struct Split {
   static constexpr int D = LS == LS_DENSE ? D0 : (LS == LS_DIAG ? ((D0 + N + 1 + 1) & ~1) : ((X_END + 1) & ~1));
   static constexpr int JREC = (N * N + 3) / 4 * 4;
   static constexpr int LU_INVD = N * N, LU_PERM = N * N + N;     // perm: ints at double offset LU_PERM
-  static constexpr int LUREC = (N * N + N + (N + 1) / 2 + 3) / 4 * 4;
+  // perm: ints at double offset LU_PERM (contiguous records) or one double element per entry (SoA)
+  static constexpr int LUREC = LU_STRIDE == 1 ? (N * N + N + (N + 1) / 2 + 3) / 4 * 4 : N * N + 2 * N;
+  __device__ static double* lurec(const SplitBufs& b, long long slot) {
+    return LU_STRIDE == 1 ? b.LU + slot * LUREC : b.LU + ((slot >> 5) * LUREC) * 32 + (slot & 31);
+  }
+  __device__ static int lu_perm(const double* lu, int i) {
+    if constexpr (LU_STRIDE == 1) return reinterpret_cast<const int*>(lu + LU_PERM)[i];
+    else return (int)lu[(LU_PERM + i) * LU_STRIDE];
+  }
   static_assert(N % 2 == 0, "16-byte column loads need an even n");
   static_assert(sizeof(TS) <= sizeof(double) * TS_STRIDE, "TS record");
 
@@ -177,10 +212,9 @@ struct Split {
   __device__ static int solve(TS& s, const W& w, const double* __restrict__ lu) {
     s.nni++;
     double b[N];
-    const int* perm = reinterpret_cast<const int*>(lu + LU_PERM);
 #pragma unroll
-    for (int i = 0; i < N; ++i) b[i] = -w.del(perm[i]);
-    lurec_substitute<N>(lu, b);
+    for (int i = 0; i < N; ++i) b[i] = -w.del(lu_perm(lu, i));
+    lurec_substitute<N, LU_STRIDE>(lu, b);
     if (s.gamrat != 1.0) {
       const double sc = 2.0 / (1.0 + s.gamrat);
 #pragma unroll
@@ -599,7 +633,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
   // bulk L2 prefetch (one TMA instruction each) of the warp's 32 LU records and of its state rows: the
   // Newton solve's column loads and the Nordsieck passes then hit L2 instead of waiting on HBM
   if (lane == 0 && w0 + 32 <= b.slots) {
-    const double* lu0 = b.LU + w0 * SP::LUREC;
+    const double* lu0 = SP::lurec(b, w0);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lu0), "r"((unsigned)(32 * SP::LUREC * 8)) : "memory");
 #if BDFB_SPLIT_PREFETCH > 1
     const double* v0 = b.vec + ((w0 >> 5) * SP::D) * 32;
@@ -614,7 +648,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
   TS& s = *SP::ts(b, have ? slot : 0);
 #endif
   const typename SP::W w = SP::ws(b, have ? slot : 0);
-  const double* lu = b.LU + (have ? slot : 0) * SP::LUREC;
+  const double* lu = SP::lurec(b, have ? slot : 0);
   int act = I::A_DONE;
   bool setup = false, jreq = false, init = false;
   if (have) {
@@ -1008,7 +1042,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b,
     if (t->coop) continue;                       // the Jacobian failed: the resumed trip handles it (uniform)
     const double gm = t->gamma;
     const double* J = b.J + slot * SP::JREC;
-    double* lu = b.LU + slot * SP::LUREC;
+    double* lu = SP::lurec(b, slot);
     double a[R][N];
 #pragma unroll
     for (int s = 0; s < R; ++s) {
@@ -1025,9 +1059,10 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b,
         const int r = gl + OCT * s;
         if (r < N) {
 #pragma unroll
-          for (int j = 0; j < N; ++j) lu[j * N + pos[s]] = a[s][j];
-          lu[SP::LU_INVD + pos[s]] = dinv[s];
-          reinterpret_cast<int*>(lu + SP::LU_PERM)[pos[s]] = r;
+          for (int j = 0; j < N; ++j) lu[(j * N + pos[s]) * LU_STRIDE] = a[s][j];
+          lu[(SP::LU_INVD + pos[s]) * LU_STRIDE] = dinv[s];
+          if (LU_STRIDE == 1) reinterpret_cast<int*>(lu + SP::LU_PERM)[pos[s]] = r;
+          else lu[(SP::LU_PERM + pos[s]) * LU_STRIDE] = (double)r;
         }
       }
     }

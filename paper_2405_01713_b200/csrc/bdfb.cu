@@ -1066,7 +1066,7 @@ extern "C" int bdfb_split_lu_factor_solve(int32_t n, int64_t N, double* M, int32
     return fail(nullptr, BDFB_EUNSUPPORTED, "n not instantiated for the SPLIT LU (2,4,6,8,10,12,16,22,32)");
   cudaStream_t st = (cudaStream_t)stream;
   double* rec = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&rec, sizeof(double) * split_lu_rec_doubles(n) * (size_t)N, st);
+  cudaError_t e = cudaMallocAsync((void**)&rec, sizeof(double) * split_lu_rec_doubles(n) * (size_t)((N + 31) / 32 * 32), st);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMallocAsync (LU records)");
   e = split_lu_diag(n, N, M, piv, b, info, rec, st);
   cudaError_t e2 = cudaFreeAsync(rec, st);

@@ -267,8 +267,12 @@ struct GlobalRunner {
       ++launches; gt_setup<TM><<<gridc(), 128, 0, st>>>(N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.perm,
                                                          B.invd, B.flag);
     } else if constexpr (LANES) {
-      ++launches; gl_setup<Model><<<gridg(), 128, sizeof(double) * GLK<Model>::PG_SET * GLK<Model>::GPB, st>>>(
-          N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.perm, B.invd, B.flag);
+      if (jbad) {   // J into HBM (table-driven lanes model), then the register-row LU
+        ++launches; gl_setup<Model><<<gridg(), 128, sizeof(double) * GLK<Model>::PG_SET * GLK<Model>::GPB, st>>>(
+            N, 1, gamma, B.v.yq, aux, B.J, B.LU, B.perm, B.invd, B.flag, 1);
+      }
+      ++launches; gl_lu<Model::N><<<(unsigned)((N + GLU<Model::N>::CPB - 1) / GLU<Model::N>::CPB), GLU<Model::N>::T,
+                                    0, st>>>(N, gamma, B.J, B.LU, B.perm, B.invd, B.flag);
     } else {
       ++launches; gk_setup<Model><<<gridg(), 128, smemg(), st>>>(prm, N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU,
                                                                   B.pos, B.perm, B.invd, B.flag);

@@ -19,6 +19,7 @@
 // Every other kernel of the mode (vectors, deterministic norms, the NCCL rank
 // exchange) is shared with the other mechanisms (global_mode.cuh).
 #pragma once
+#include <utility>
 #include "bdf_tpc.cuh"
 #include "mech_lanes.cuh"
 
@@ -128,11 +129,12 @@ __global__ void __launch_bounds__(128) gl_rhs(long long N, const double* y, cons
   if (live && rv && g.lane == 0) atomicOr(flag, 1);
 }
 
-// setup of one cell per group: (jbad) J at y into HBM; M = I - gamma J; LU; factors + perm + 1/U to HBM
+// setup of one cell per group: (jbad) J at y into HBM; unless jac_only: M = I - gamma J; LU; factors + perm +
+// 1/U to HBM.  (The default path calls it with jac_only = 1 and factors with gl_lu.)
 template <class MR>
 __global__ void __launch_bounds__(128) gl_setup(long long N, int jbad, double gamma, const double* y,
                                                 const double* aux, double* J, double* LU, int* perm, double* invd,
-                                                int* flag) {
+                                                int* flag, int jac_only) {
   using K = GLK<MR>;
   constexpr int G = MR::G, NN = MR::N, R = MR::R, MS = K::MS;
   extern __shared__ double smem[];
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(128) gl_setup(long long N, int jbad, double ga
     }
   }
   g.sync();
-  if (!bad) {
+  if (!bad && !jac_only) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = g.lane + G * r;
@@ -194,6 +196,147 @@ __global__ void __launch_bounds__(128) gl_setup(long long N, int jbad, double ga
     }
   }
   if (live && bad && g.lane == 0) atomicOr(flag, 1);
+}
+
+// M = I - gamma J and its LU with partial pivoting, ONE CELL PER BLOCK of 32 ceil(n/32) threads, thread i
+// owning row i of M in registers for the whole factorisation (columns fully unrolled).  Per column k: the
+// pivot (max |m_ik| over rows at LAPACK positions >= k, ties to the smaller position) by a warp butterfly and
+// an ordered combination of the warps' candidates in shared memory; the pivot row's owner publishes its row
+// and 1/pivot; every row below forms its multiplier m = m_ik (1/pivot) and applies fma(-m, u_kj, m_ij) --
+// the listing's LU_FACTOR operation for operation (reading R16), as glu_factor_r, so factors and pivots are
+// bit-identical.  Versus the shared-memory warp LU of gl_setup (3 shared-memory accesses per FMA, 8 warps per
+// SM): the update is one broadcast shared load per FMA from registers, 16 warps per SM.  Factors written in
+// pivoted row order, cell-minor (element e of cell c at [e N + c]) with perm and 1/U_kk (tpc_solve layout).
+// CPB cells per block of CPB x 32 ceil(n/32) threads: all 12 warps of an SM walk the same column of the
+// unrolled factorisation together (one barrier pair per column for all six cells: instruction-cache locality)
+template <int NN>
+struct GLU {
+  static constexpr int W = (NN + 31) / 32, TC = 32 * W, CPB = 384 / TC > 0 ? 384 / TC : 1, T = CPB * TC;
+};
+// shared state of a gl_lu block: per cell the published pivot row and 1/pivot, the warps' pivot candidates
+// (double-buffered by column parity)
+template <int NN>
+struct GLUShared {
+  double2 prow[2][GLU<NN>::CPB][NN / 2 + 1];
+  double crv[2][GLU<NN>::CPB][GLU<NN>::W], srinv[2][GLU<NN>::CPB];
+  int crp[2][GLU<NN>::CPB][GLU<NN>::W], crr[2][GLU<NN>::CPB][GLU<NN>::W];
+};
+// column K of gl_lu (K a compile-time constant, so that the row stays in registers); returns false at an exact
+// zero pivot (uniform per cell; the block keeps meeting the barriers)
+template <int NN, int K>
+__device__ __forceinline__ bool glu_column(GLUShared<NN>& sh, double (&a)[NN], int& pos, double& dinv, int i,
+                                           int cb, bool alive) {
+  constexpr int W = GLU<NN>::W, par = K & 1, J0 = (K + 1) & ~1;
+  const int lane = i & 31, warp = i >> 5;
+  const bool own = i < NN && alive;
+  double bv = -1.0;
+  int bp = 0x7fffffff, br = -1;
+  if (own && pos >= K) {
+    bv = fabs(a[K]);
+    bp = pos;
+    br = i;
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+    const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+    const int orr = __shfl_xor_sync(0xffffffffu, br, off);
+    if (ov > bv || (ov == bv && op < bp)) {
+      bv = ov;
+      bp = op;
+      br = orr;
+    }
+  }
+  if (lane == 0) {
+    sh.crv[par][cb][warp] = bv;
+    sh.crp[par][cb][warp] = bp;
+    sh.crr[par][cb][warp] = br;
+  }
+  __syncthreads();
+  bv = sh.crv[par][cb][0];
+  bp = sh.crp[par][cb][0];
+  br = sh.crr[par][cb][0];
+#pragma unroll
+  for (int w = 1; w < W; ++w) {
+    const double ov = sh.crv[par][cb][w];
+    const int op = sh.crp[par][cb][w];
+    if (ov > bv || (ov == bv && op < bp)) {
+      bv = ov;
+      bp = op;
+      br = sh.crr[par][cb][w];
+    }
+  }
+  const bool ok = bv > 0.0;
+  if (ok && i == br) {
+    const double rinv = 1.0 / a[K];
+    sh.srinv[par][cb] = rinv;
+#pragma unroll
+    for (int j = J0; j < NN; j += 2) sh.prow[par][cb][j / 2] = make_double2(a[j], j + 1 < NN ? a[j + 1] : 0.0);
+    pos = K;
+    dinv = rinv;
+  } else if (ok && own && pos == K) {
+    pos = bp;
+  }
+  __syncthreads();
+  if (ok && own && pos > K) {
+    const double m = a[K] * sh.srinv[par][cb];
+    a[K] = m;
+#pragma unroll
+    for (int j = J0; j < NN; j += 2) {
+      const double2 u = sh.prow[par][cb][j / 2];
+      if (j > K) a[j] = fma(-m, u.x, a[j]);
+      if (j + 1 < NN) a[j + 1] = fma(-m, u.y, a[j + 1]);
+    }
+  }
+  return ok;
+}
+template <int NN, int... Ks>
+__device__ __forceinline__ int glu_columns(GLUShared<NN>& sh, double (&a)[NN], int& pos, double& dinv, int i, int cb,
+                                           bool alive, std::integer_sequence<int, Ks...>) {
+  int info = 0;
+  // every thread runs every column (block-wide barriers); a cell whose pivot was exactly zero stops updating
+  (void)((glu_column<NN, Ks>(sh, a, pos, dinv, i, cb, alive && !info) || !alive || info || (info = Ks + 1, true)) &&
+         ...);
+  return info;
+}
+
+// M = I - gamma J and its LU with partial pivoting, one cell per 32 ceil(n/32) threads (CPB cells per block),
+// thread i owning row i of M in registers for the whole factorisation (columns unrolled at compile time).  Per
+// column k: the pivot (max |m_ik| over rows at LAPACK positions >= k, ties to the smaller position) by a warp
+// butterfly and an ordered combination of the warps' candidates in shared memory; the pivot row's owner
+// publishes its row and 1/pivot; every row below forms its multiplier m = m_ik (1/pivot) and applies
+// fma(-m, u_kj, m_ij) -- the listing's LU_FACTOR operation for operation (reading R16), as glu_factor_r, so
+// factors and pivots are bit-identical.  Versus the shared-memory warp LU of gl_setup (three shared-memory
+// accesses per FMA, 8 warps per SM): one broadcast 16-byte shared load per two FMAs on register rows, 12 warps
+// per SM in lockstep.  Factors written in pivoted row order, cell-minor (element e of cell c at [e N + c]) with
+// perm and 1/U_kk (the tpc_solve layout).
+template <int NN>
+__global__ void __launch_bounds__(GLU<NN>::T, 1)
+    gl_lu(long long N, double gamma, const double* J, double* LU, int* perm, double* invd, int* flag) {
+  __shared__ GLUShared<NN> sh;
+  constexpr int TC = GLU<NN>::TC;
+  const int cb = threadIdx.x / TC, i = threadIdx.x % TC;
+  const long long c = (long long)blockIdx.x * GLU<NN>::CPB + cb;
+  const bool alive = c < N;
+  const bool own = i < NN && alive;
+  double a[NN];
+#pragma unroll
+  for (int j = 0; j < NN; ++j) a[j] = own ? (i == j ? 1.0 : 0.0) - gamma * J[((long long)i * NN + j) * N + c] : 0.0;
+  int pos = i;
+  double dinv = 0.0;
+  const int info = glu_columns<NN>(sh, a, pos, dinv, i, cb, alive, std::make_integer_sequence<int, NN>{});
+  if (!alive) return;
+  if (info) {
+    if (i == 0) atomicOr(flag, 1);
+    return;
+  }
+  if (own) {
+    const long long p = pos;
+#pragma unroll
+    for (int j = 0; j < NN; ++j) LU[(p * NN + j) * N + c] = a[j];
+    perm[p * N + c] = i;
+    invd[p * N + c] = dinv;
+  }
 }
 
 template <int NN>

@@ -25,13 +25,15 @@ namespace {
 template <int NN>
 __global__ void __launch_bounds__(128) split_lu_diag_kernel(long long N, double* M, int* piv, double* b, int* info,
                                                             double* rec) {
-  constexpr int R = (NN + OCT - 1) / OCT, LUREC = (NN * NN + NN + (NN + 1) / 2 + 3) / 4 * 4;
+  constexpr int R = (NN + OCT - 1) / OCT;
+  constexpr int S = LU_STRIDE;
+  constexpr int LUREC = S == 1 ? (NN * NN + NN + (NN + 1) / 2 + 3) / 4 * 4 : NN * NN + 2 * NN;
   constexpr int LU_INVD = NN * NN, LU_PERM = NN * NN + NN;
   const int lane = threadIdx.x & 31, gl = lane & (OCT - 1);
   const unsigned gmask = 0xffu << (lane & ~(OCT - 1));
   const long long c = ((long long)blockIdx.x * 128 + threadIdx.x) / OCT;
   if (c >= N) return;                         // whole groups exit together (N is per group)
-  double* lu = rec + c * LUREC;
+  double* lu = S == 1 ? rec + c * LUREC : rec + ((c >> 5) * LUREC) * 32 + (c & 31);   // K_lu's record layout
   double a[R][NN];
 #pragma unroll
   for (int s = 0; s < R; ++s) {
@@ -48,9 +50,10 @@ __global__ void __launch_bounds__(128) split_lu_diag_kernel(long long N, double*
       const int r = gl + OCT * s;
       if (r < NN) {
 #pragma unroll
-        for (int j = 0; j < NN; ++j) lu[j * NN + pos[s]] = a[s][j];
-        lu[LU_INVD + pos[s]] = dinv[s];
-        reinterpret_cast<int*>(lu + LU_PERM)[pos[s]] = r;
+        for (int j = 0; j < NN; ++j) lu[(j * NN + pos[s]) * S] = a[s][j];
+        lu[(LU_INVD + pos[s]) * S] = dinv[s];
+        if (S == 1) reinterpret_cast<int*>(lu + LU_PERM)[pos[s]] = r;
+        else lu[(LU_PERM + pos[s]) * S] = (double)r;
       }
     }
   }
@@ -58,14 +61,17 @@ __global__ void __launch_bounds__(128) split_lu_diag_kernel(long long N, double*
   if (gl != 0) return;
   info[c] = inf;
   if (inf) return;
-  const int* perm = reinterpret_cast<const int*>(lu + LU_PERM);
+  int perm[NN];
+#pragma unroll
+  for (int i = 0; i < NN; ++i)
+    perm[i] = S == 1 ? reinterpret_cast<const int*>(lu + LU_PERM)[i] : (int)lu[(LU_PERM + i) * S];
   double x[NN];
 #pragma unroll
   for (int i = 0; i < NN; ++i) x[i] = b[(long long)perm[i] * N + c];
-  lurec_substitute<NN>(lu, x);
+  lurec_substitute<NN, S>(lu, x);
   for (int i = 0; i < NN; ++i) {
     b[(long long)i * N + c] = x[i];
-    for (int j = 0; j < NN; ++j) M[((long long)i * NN + j) * N + c] = lu[j * NN + i];
+    for (int j = 0; j < NN; ++j) M[((long long)i * NN + j) * N + c] = lu[(j * NN + i) * S];
   }
   // getrf swap sequence of the permutation: at step k the row perm[k] sits at position where[perm[k]]
   int cur[NN], where[NN];
@@ -100,7 +106,10 @@ cudaError_t split_lu_diag(int n, long long N, double* M, int* piv, double* b, in
   return cudaGetLastError();
 }
 
-size_t split_lu_rec_doubles(int n) { return (size_t)((n * n + n + (n + 1) / 2 + 3) / 4 * 4); }
+// scratch doubles per cell of the diagnostic's record pool (the caller rounds N up to a multiple of 32)
+size_t split_lu_rec_doubles(int n) {
+  return LU_STRIDE == 1 ? (size_t)((n * n + n + (n + 1) / 2 + 3) / 4 * 4) : (size_t)(n * n + 2 * n);
+}
 
 cudaError_t split_geometry(int mech, int ls, int device, SplitGeom* gm) {
   if (ls != LS_DENSE) return split_mf_geometry(mech, ls, device, gm);
