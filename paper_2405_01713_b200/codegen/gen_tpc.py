@@ -450,7 +450,7 @@ def generate(name, out_dir):
     return p
 
 
-MECHANISMS = ["h2_lidryer", "drm19_class"]
+MECHANISMS = ["h2_lidryer", "drm19_class", "gri53_class"]   # gri53: its RHS only is used (C5)
 
 
 def main(argv=None):

@@ -27,6 +27,7 @@
 #include "mech_lanes.cuh"
 #include "gen/tpc_drm19_class.cuh"
 #include "gen/tpc_h2_lidryer.cuh"
+#include "gen/tpc_gri53_class.cuh"
 #include "mech_model.cuh"
 #include "models_simple.cuh"
 #include "tpc_api.h"
@@ -666,7 +667,7 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
     switch (b->model) {
       case BDFB_MODEL_MECH_H2: return run_global<ModelH2, Tpc_h2_lidryer>(b, o, y, f_ext, aux, st);
       case BDFB_MODEL_MECH_DRM19: return run_global<ModelDRM19, Tpc_drm19_class>(b, o, y, f_ext, aux, st);
-      case BDFB_MODEL_MECH_GRI53: return run_global<ModelGRI53>(b, o, y, f_ext, aux, st);
+      case BDFB_MODEL_MECH_GRI53: return run_global<ModelGRI53, Tpc_gri53_class>(b, o, y, f_ext, aux, st);
       default: return fail(b, BDFB_EUNSUPPORTED, "global-norm mode: group models only (MECH_H2, MECH_DRM19)");
     }
   }
@@ -932,7 +933,8 @@ extern "C" int bdfb_eval_rhs(bdfb_batch* b, double t, const double* y, const dou
     case BDFB_MODEL_MECH_DRM19:
       return (use_tpc(b) || use_split(b)) ? launch_eval_tpc(b, y, f_ext, aux, f, status, nullptr, st)
                                           : launch_eval<ModelDRM19>(b, t, y, f_ext, aux, f, status, nullptr, st);
-    case BDFB_MODEL_MECH_GRI53: return launch_eval_lanes<ModelGRI53>(b, y, f_ext, aux, f, status, nullptr, st);
+    case BDFB_MODEL_MECH_GRI53:   // the generated thread-per-cell RHS the C5 path runs (gt_rhs)
+      return launch_eval_tpc(b, y, f_ext, aux, f, status, nullptr, st);
   }
   return fail(b, BDFB_ENOMODEL, "unknown model");
 }

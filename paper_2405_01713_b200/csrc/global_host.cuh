@@ -42,6 +42,8 @@ struct IsLanes : std::false_type {};
 template <class M>
 struct IsLanes<M, std::void_t<decltype(M::LANES)>> : std::bool_constant<M::LANES> {};
 
+// Tpc: the generated thread-per-cell RHS (and, for group models, setup and solve).  For the lanes model of
+// C5 (n = 54) only its RHS is used (gt_rhs); J stays the table-driven lanes Jacobian, the LU is gl_lu.
 template <class Model, class Tpc = void>
 struct GlobalRunner {
   static constexpr bool TPC = !std::is_void<Tpc>::value;
@@ -263,7 +265,7 @@ struct GlobalRunner {
       jcur = 0;
     }
     cudaMemsetAsync(B.flag, 0, sizeof(int), st);
-    if constexpr (TPC) {
+    if constexpr (TPC && !LANES) {
       ++launches; gt_setup<TM><<<gridc(), 128, 0, st>>>(N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.perm,
                                                          B.invd, B.flag);
     } else if constexpr (LANES) {
@@ -309,7 +311,7 @@ struct GlobalRunner {
         for (;;) {
           nni++;
           const double sc2 = (gamrat != 1.0) ? 2.0 / (1.0 + gamrat) : 1.0;
-          if constexpr (TPC) {
+          if constexpr (TPC && !LANES) {
             ++launches; gt_solve<TM><<<gridc(), 128, 0, st>>>(N, sc2, B.LU, B.perm, B.invd, B.v.del, B.v.acor,
                                                                B.v.tmp);
           } else if constexpr (LANES) {

@@ -12,6 +12,7 @@
 #include "gen/mech_h2_lidryer.cuh"
 #include "gen/tpc_drm19_class.cuh"
 #include "gen/tpc_h2_lidryer.cuh"
+#include "gen/tpc_gri53_class.cuh"
 #include "mech_model.cuh"
 #include "split_api.h"
 
@@ -90,6 +91,9 @@ cudaError_t tpc_eval_rhs(int mech, long long N, const double* y, const double* f
     case BDFB_MODEL_MECH_H2: eval_rhs_kernel<Tpc_h2_lidryer><<<g, 128, 0, st>>>(N, y, fext, aux, f, status); break;
     case BDFB_MODEL_MECH_DRM19:
       eval_rhs_kernel<Tpc_drm19_class><<<g, 128, 0, st>>>(N, y, fext, aux, f, status);
+      break;
+    case BDFB_MODEL_MECH_GRI53:
+      eval_rhs_kernel<Tpc_gri53_class><<<g, 128, 0, st>>>(N, y, fext, aux, f, status);
       break;
     default: return cudaErrorInvalidValue;
   }
