@@ -52,6 +52,10 @@ CONFIGS = {
     "C5": ("gri53", "gri53_class", 54, 256, 1e-6, 1e-6, 1e-10,
            "C5 GRI-3.0-class CH4/air (53 species + T, n=54, 325 reactions) flame field, global-norm mode (one "
            "lockstep batch, batch-wide WRMS), 256^3 grid in 8 z-slabs of 128^3 cells (one per GPU), dt_CFD 1e-6 s"),
+    # C5's mechanism and grid share per cell (the north_star's per-cell mode) instead of the lockstep batch
+    "C5P": ("gri53", "gri53_class", 54, 256, 1e-6, 1e-6, 1e-10,
+            "C5P GRI-3.0-class CH4/air (53 species + T, n=54, 325 reactions) flame field, per-cell mode (SPLIT), "
+            "256^3 grid in 8 z-slabs of 128^3 cells (one per GPU), dt_CFD 1e-6 s"),
     "G4": ("drm19", "drm19_class", 22, 128, 1e-5, 1e-6, 1e-10,
            "G4 global-norm mode (lockstep batch, batch-wide WRMS) on the DRM19-class flame field, 128^3 cells "
            "(C5's per-GPU share at 8 GPUs), dt_CFD 1e-5 s"),
@@ -95,7 +99,7 @@ def rank_cells(cfg, rank=0, world=1, scaling="strong", cells_per_rank=None):
     from paper_2405_01713_b200 import parallel as PL
     L = CONFIGS[cfg][3]
     total = 1024 if cfg == "C1" else L ** 3
-    if cfg == "C5" and not cells_per_rank:     # the 256^3 grid's z-slab r (of 8): fixed share per GPU
+    if cfg in ("C5", "C5P") and not cells_per_rank:     # the 256^3 grid's z-slab r (of 8): fixed share per GPU
         if world > 8:
             raise SystemExit("C5 is defined on 8 GPUs (256^3 / 8 cells each)")
         return np.arange(rank * C5_SLAB, (rank + 1) * C5_SLAB), C5_SLAB * world
@@ -332,7 +336,7 @@ def oracle_cells_per_s(cfg, budget_s=15.0, threads=None, rank_cells=None, steps=
     return m, times, threads
 
 
-CONFIGS_G = {"C3": 1, "C4": 1}     # WRMS summation group of the default (thread-per-cell) kernel, R15
+CONFIGS_G = {"C3": 1, "C4": 1, "C5P": 1}     # WRMS summation group of the default (thread-per-cell) kernel, R15
 
 
 # ------------------------------------------------------------------ main
@@ -406,7 +410,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    scaling = "weak" if (args.cells or cfg == "C5") else args.scaling
+    scaling = "weak" if (args.cells or cfg in ("C5", "C5P")) else args.scaling
     y0, rho, F, prog = make_inputs(cfg, rank, args.cells or None, world, scaling)
     N = y0.shape[1]
     glob_mode = cfg in GLOBAL_CFGS
@@ -513,8 +517,9 @@ def main():
                                       "traffic_ncu": traffic_split(cfg, stats[-1]),
                                       "model": "DESIGN.md §6 (slot-state round trips: implementation bytes)"}
         dom = max(pm, key=pm.get)
-        knames = {"ctl": "split_ctl_kernel", "jac": "split_jac_kernel", "lu": "split_lu_kernel",
-                  "rhs": "split_rhs_kernel"}
+        big = n > 32   # split_big.cuh setup kernels
+        knames = {"ctl": "split_ctl_kernel", "jac": "split_jac_lanes_kernel" if big else "split_jac_kernel",
+                  "lu": "split_lu_rows_kernel" if big else "split_lu_kernel", "rhs": "split_rhs_kernel"}
         roof = dict(roof_common, achieved=phases[dom]["tflops"], frac=phases[dom]["frac"],
                     traffic=traffic_split(cfg, stats[-1]) if dom == "ctl" else None,
                     kernel=f"{knames[dom]}<Tpc_{mech}> (K_{dom}, {100 * pm[dom] / tot:.0f}% of the step)",

@@ -70,8 +70,10 @@ extern "C" {
                                       constant-volume reactor; aux[c] = rho; params: NULL     */
 #define BDFB_MODEL_MECH_DRM19 4    /* n=22: DRM19-class CH4/air (mechanisms/drm19_class.json) */
 #define BDFB_MODEL_MECH_GRI53 5    /* n=54: GRI-3.0-class CH4/air, 53 species, 325 reactions
-                                      (mechanisms/gri53_class.json; config C5); table-driven model,
-                                      global-norm mode only (per-cell integrate: BDFB_EUNSUPPORTED) */
+                                      (mechanisms/gri53_class.json; config C5): generated thread-per-cell
+                                      RHS, table-driven lanes Jacobian; per cell with the SPLIT kernel
+                                      (dense / CVDiag / GMRES, ERK4) or in the global-norm mode; the
+                                      THREAD / GROUP kernels and the DQ Jacobian: BDFB_EUNSUPPORTED */
 
 #define BDFB_LAYOUT_YC 0
 #define BDFB_LAYOUT_CY 1

@@ -85,9 +85,11 @@ struct bdfb_batch {
 using ModelGRI53 = ModelMechR<mech_gri53_class::Traits, 32>;
 
 static bool is_mech(int model) { return model == BDFB_MODEL_MECH_H2 || model == BDFB_MODEL_MECH_DRM19; }
+// mechanisms the SPLIT per-cell integrator and the ERK kernel run (n = 54 with the split_big.cuh setup kernels)
+static bool is_split_mech(int model) { return is_mech(model) || model == BDFB_MODEL_MECH_GRI53; }
 // mechanism models: AUTO = SPLIT (the fastest organisation measured on B200, profiles/r1)
 static bool use_split(const bdfb_batch* b) {
-  return is_mech(b->model) && (b->kernel == BDFB_KERNEL_SPLIT || b->kernel == BDFB_KERNEL_AUTO);
+  return is_split_mech(b->model) && (b->kernel == BDFB_KERNEL_SPLIT || b->kernel == BDFB_KERNEL_AUTO);
 }
 static bool use_tpc(const bdfb_batch* b) { return is_mech(b->model) && b->kernel == BDFB_KERNEL_THREAD; }
 
@@ -439,6 +441,8 @@ int bdfb_set_jacobian(bdfb_batch* b, int32_t mode) {
   if (mode != BDFB_JAC_ANALYTIC && mode != BDFB_JAC_DQ) return fail(b, BDFB_EINVAL, "bad Jacobian mode");
   if (mode == BDFB_JAC_DQ && !(use_split(b) && b->opt.mode == BDFB_MODE_PER_CELL))
     return fail(b, BDFB_EUNSUPPORTED, "the difference-quotient Jacobian needs the SPLIT mechanism kernel");
+  if (mode == BDFB_JAC_DQ && b->model == BDFB_MODEL_MECH_GRI53)
+    return fail(b, BDFB_EUNSUPPORTED, "the difference-quotient Jacobian is built for n <= 32");
   if (mode == BDFB_JAC_DQ && b->ls != BDFB_LS_DENSE)
     return fail(b, BDFB_EINVAL, "the difference-quotient Jacobian belongs to the dense linear solver");
   b->jac_mode = mode;
@@ -449,7 +453,7 @@ int bdfb_set_jacobian(bdfb_batch* b, int32_t mode) {
 int bdfb_set_method(bdfb_batch* b, int32_t method) {
   if (!b) return fail(nullptr, BDFB_EINVAL, "batch is NULL");
   if (method != BDFB_METHOD_BDF && method != BDFB_METHOD_ERK4) return fail(b, BDFB_EINVAL, "bad method");
-  if (method == BDFB_METHOD_ERK4 && !(is_mech(b->model) && b->opt.mode == BDFB_MODE_PER_CELL))
+  if (method == BDFB_METHOD_ERK4 && !(is_split_mech(b->model) && b->opt.mode == BDFB_MODE_PER_CELL))
     return fail(b, BDFB_EUNSUPPORTED, "the explicit ERK runs the mechanism models (MECH_H2, MECH_DRM19) per cell");
   b->method = method;
   return prepare_kernel(b);
@@ -685,7 +689,8 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
       return use_tpc(b) ? launch_tpc(b, o, y, f_ext, aux, st)
                         : launch_integrate<ModelDRM19>(b, o, y, f_ext, aux, st);
     case BDFB_MODEL_MECH_GRI53:
-      return fail(b, BDFB_EUNSUPPORTED, "MECH_GRI53 (n = 54, config C5) runs in the global-norm mode");
+      if (use_split(b)) return launch_split(b, o, y, f_ext, aux, st);
+      return fail(b, BDFB_EUNSUPPORTED, "MECH_GRI53 (n = 54) runs the SPLIT kernel per cell, or the global-norm mode");
   }
   return fail(b, BDFB_ENOMODEL, "unknown model");
 }

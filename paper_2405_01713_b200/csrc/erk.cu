@@ -25,6 +25,7 @@
 #include "erk_api.h"
 #include "gen/tpc_drm19_class.cuh"
 #include "gen/tpc_h2_lidryer.cuh"
+#include "gen/tpc_gri53_class.cuh"
 
 namespace bdfb {
 namespace {
@@ -372,6 +373,7 @@ cudaError_t erk_geometry(int mech, int device, long long ncells, long long* thre
   switch (mech) {
     case BDFB_MODEL_MECH_H2: return geometry<Tpc_h2_lidryer>(device, ncells, threads, doubles_per_thread);
     case BDFB_MODEL_MECH_DRM19: return geometry<Tpc_drm19_class>(device, ncells, threads, doubles_per_thread);
+    case BDFB_MODEL_MECH_GRI53: return geometry<Tpc_gri53_class>(device, ncells, threads, doubles_per_thread);
   }
   return cudaErrorInvalidValue;
 }
@@ -386,6 +388,9 @@ cudaError_t erk_integrate(int mech, const Opts& o, double* y, const double* fext
       break;
     case BDFB_MODEL_MECH_DRM19:
       erk_kernel<Tpc_drm19_class><<<grid, BDFB_ERK_BLOCK, 0, st>>>(o, y, fext, aux, atol, ws, counter, agg, cs);
+      break;
+    case BDFB_MODEL_MECH_GRI53:
+      erk_kernel<Tpc_gri53_class><<<grid, BDFB_ERK_BLOCK, 0, st>>>(o, y, fext, aux, atol, ws, counter, agg, cs);
       break;
     default:
       return cudaErrorInvalidValue;

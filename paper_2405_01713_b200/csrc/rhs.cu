@@ -15,6 +15,7 @@
 #include "gen/tpc_gri53_class.cuh"
 #include "mech_model.cuh"
 #include "split_api.h"
+#include "split_big.cuh"
 
 namespace bdfb {
 
@@ -66,6 +67,10 @@ BDFB_RHS_INST(Tpc_h2_lidryer, GH2, LS_GMRES)
 BDFB_RHS_INST(Tpc_drm19_class, GDRM, LS_DENSE)
 BDFB_RHS_INST(Tpc_drm19_class, GDRM, LS_DIAG)
 BDFB_RHS_INST(Tpc_drm19_class, GDRM, LS_GMRES)
+using GGRI = LanesOf<Tpc_gri53_class>::GM;
+BDFB_RHS_INST(Tpc_gri53_class, GGRI, LS_DENSE)
+BDFB_RHS_INST(Tpc_gri53_class, GGRI, LS_DIAG)
+BDFB_RHS_INST(Tpc_gri53_class, GGRI, LS_GMRES)
 #undef BDFB_RHS_INST
 
 // f = R(y) + F for N cells (YC), the K_rhs code path (diagnostic entry point bdfb_eval_rhs)

@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(128) split_lu_diag_kernel(long long N, double*
 
 using KH2 = SplitK<Tpc_h2_lidryer, ModelMech<mech_h2_lidryer::Traits>>;
 using KDRM = SplitK<Tpc_drm19_class, ModelMech<mech_drm19_class::Traits>>;
+using KGRI = SplitK<Tpc_gri53_class, LanesOf<Tpc_gri53_class>::GM>;   // n = 54 (split_big.cuh setup kernels)
 
 }  // namespace
 
@@ -116,6 +117,7 @@ cudaError_t split_geometry(int mech, int ls, int device, SplitGeom* gm) {
   switch (mech) {
     case BDFB_MODEL_MECH_H2: return KH2::geometry(device, gm);
     case BDFB_MODEL_MECH_DRM19: return KDRM::geometry(device, gm);
+    case BDFB_MODEL_MECH_GRI53: return KGRI::geometry(device, gm);
   }
   return cudaErrorInvalidValue;
 }
@@ -134,6 +136,9 @@ cudaError_t split_integrate(int mech, int ls, const Opts& o, double* y, const do
                        phase_ms, st2, xev);
     case BDFB_MODEL_MECH_DRM19:
       return KDRM::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches, events,
+                        phase_ms, st2, xev);
+    case BDFB_MODEL_MECH_GRI53:
+      return KGRI::run(o, y, fext, aux, atol, sb, gm, counter, agg, cs, h_live, batch, st, launches, events,
                         phase_ms, st2, xev);
   }
   return cudaErrorInvalidValue;

@@ -16,6 +16,8 @@ template <int LS>
 using KH2L = SplitK<Tpc_h2_lidryer, ModelMech<mech_h2_lidryer::Traits>, LS>;
 template <int LS>
 using KDRML = SplitK<Tpc_drm19_class, ModelMech<mech_drm19_class::Traits>, LS>;
+template <int LS>
+using KGRIL = SplitK<Tpc_gri53_class, LanesOf<Tpc_gri53_class>::GM, LS>;
 }  // namespace
 
 cudaError_t split_mf_geometry(int mech, int ls, int device, SplitGeom* gm) {
@@ -24,6 +26,8 @@ cudaError_t split_mf_geometry(int mech, int ls, int device, SplitGeom* gm) {
     case BDFB_MODEL_MECH_H2 * 4 + LS_GMRES: return KH2L<LS_GMRES>::geometry(device, gm);
     case BDFB_MODEL_MECH_DRM19 * 4 + LS_DIAG: return KDRML<LS_DIAG>::geometry(device, gm);
     case BDFB_MODEL_MECH_DRM19 * 4 + LS_GMRES: return KDRML<LS_GMRES>::geometry(device, gm);
+    case BDFB_MODEL_MECH_GRI53 * 4 + LS_DIAG: return KGRIL<LS_DIAG>::geometry(device, gm);
+    case BDFB_MODEL_MECH_GRI53 * 4 + LS_GMRES: return KGRIL<LS_GMRES>::geometry(device, gm);
   }
   return cudaErrorInvalidValue;
 }
@@ -40,6 +44,8 @@ cudaError_t split_mf_integrate(int mech, int ls, const Opts& o, double* y, const
     case BDFB_MODEL_MECH_H2 * 4 + LS_GMRES: return BDFB_MF_RUN(KH2L<LS_GMRES>);
     case BDFB_MODEL_MECH_DRM19 * 4 + LS_DIAG: return BDFB_MF_RUN(KDRML<LS_DIAG>);
     case BDFB_MODEL_MECH_DRM19 * 4 + LS_GMRES: return BDFB_MF_RUN(KDRML<LS_GMRES>);
+    case BDFB_MODEL_MECH_GRI53 * 4 + LS_DIAG: return BDFB_MF_RUN(KGRIL<LS_DIAG>);
+    case BDFB_MODEL_MECH_GRI53 * 4 + LS_GMRES: return BDFB_MF_RUN(KGRIL<LS_GMRES>);
   }
 #undef BDFB_MF_RUN
   return cudaErrorInvalidValue;

@@ -8,6 +8,7 @@
 
 #include "bdf_split.cuh"
 #include "split_api.h"
+#include "split_big.cuh"
 
 namespace bdfb {
 namespace {
@@ -18,8 +19,14 @@ struct SplitK {
   static constexpr size_t ctl_smem() {
     return BDFB_SPLIT_TS_SMEM ? sizeof(double) * (size_t)TS_STRIDE * BDFB_SPLIT_CTL_BLOCK : 0;
   }
+  static constexpr bool BIG = Mech::N > 32;   // split_big.cuh setup kernels (lanes Jacobian, register-row LU)
   static constexpr size_t jac_smem() {
-    return sizeof(double) * (size_t)(GM::SG + GM::JG + GM::N * (GM::N | 1)) * (BDFB_SPLIT_BLOCK / GM::G);
+    if constexpr (BIG) {
+      using MR = typename LanesOf<Mech>::type;
+      return sizeof(double) * (size_t)(MR::SG + MR::JG) * 4;
+    } else {
+      return sizeof(double) * (size_t)(GM::SG + GM::JG + GM::N * (GM::N | 1)) * (BDFB_SPLIT_BLOCK / GM::G);
+    }
   }
 
   static cudaError_t geometry(int device, SplitGeom* gm) {
@@ -32,10 +39,17 @@ struct SplitK {
     if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) return e;
     if ((e = split_rhs_occupancy<Mech, GM, LS>(&pr)) != cudaSuccess) return e;
     if (pr < 1) return cudaErrorInvalidConfiguration;
-    if (LS == LS_DENSE && jac_smem() > 48 * 1024 &&
-        (e = cudaFuncSetAttribute(split_jac_kernel<Mech, GM, LS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)jac_smem())) != cudaSuccess)
-      return e;
+    if constexpr (BIG) {
+      if (LS == LS_DENSE && jac_smem() > 48 * 1024 &&
+          (e = cudaFuncSetAttribute(split_jac_lanes_kernel<Mech, GM, LS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)jac_smem())) != cudaSuccess)
+        return e;
+    } else {
+      if (LS == LS_DENSE && jac_smem() > 48 * 1024 &&
+          (e = cudaFuncSetAttribute(split_jac_kernel<Mech, GM, LS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)jac_smem())) != cudaSuccess)
+        return e;
+    }
     gm->rhs_grid = nsm * pr;
     gm->setup_grid = nsm * 8;
     gm->vec_doubles = SP::D;
@@ -97,14 +111,22 @@ struct SplitK {
           ss = st2;
           if (events) cudaEventRecord(ev[5], st2);
         }
-        if constexpr (LS == LS_DENSE) {   // the matrix-free linear solvers have no setup kernels
+        if constexpr (LS == LS_DENSE && BIG) {   // n > 32: lanes Jacobian, one cell per warp
+          const unsigned gj = (unsigned)gm.setup_grid;
+          split_jac_lanes_kernel<Mech, GM, LS><<<gj, 128, jac_smem(), ss>>>(b, it);
+        } else if constexpr (LS == LS_DENSE) {   // the matrix-free linear solvers have no setup kernels
           if (b.jac_dq)
             split_dqjac_kernel<Mech, GM, LS><<<gdq, blk, 0, ss>>>(b, it);
           else
             split_jac_kernel<Mech, GM, LS><<<gjac, blk, jac_smem(), ss>>>(b, it);
         }
         if (events) cudaEventRecord(ev[2], ss);
-        if constexpr (LS == LS_DENSE) split_lu_kernel<Mech, GM, LS><<<glu, blk, 0, ss>>>(b, it);
+        if constexpr (LS == LS_DENSE && BIG) {
+          // one 384-thread block per SM (setup_grid = 8 per SM), grid-stride over the setup list
+          split_lu_rows_kernel<Mech, GM, LS><<<(unsigned)(gm.setup_grid / 8), GLU<Mech::N>::T, 0, ss>>>(b, it);
+        } else if constexpr (LS == LS_DENSE) {
+          split_lu_kernel<Mech, GM, LS><<<glu, blk, 0, ss>>>(b, it);
+        }
         if (events) cudaEventRecord(ev[3], ss);
         if (ovl) {
           cudaEventRecord(xev[2 * k + 1], st2);
