@@ -591,13 +591,12 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
   using I = typename SP::I;
   constexpr int N = Mech::N;
   extern __shared__ double smem[];           // TS records of the block's threads (TS_STRIDE each)
-  __shared__ double satol[N];
+  // every shared structure of K_ctl is warp-private (TS staging, statistics): no block barrier, so a warp whose
+  // lanes finish early leaves without waiting for the block's slowest warp (ncu: block barriers were ~10% of
+  // the stall cycles); atol is read through L1 from global memory
   __shared__ Agg wacc[BDFB_SPLIT_CTL_BLOCK / 32];
-  __shared__ unsigned long long blive;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < N) satol[threadIdx.x] = atol[threadIdx.x];
   if (lane == 0) wacc[warp] = Agg{};
-  if (threadIdx.x == 0) blive = 0;
   unsigned* cnt = b.cnt + 3 * (it & 1);
   if (blockIdx.x == 0 && threadIdx.x == 0) {   // the next iteration's lists and live count (their last
     unsigned* nx = b.cnt + 3 * ((it + 1) & 1);   // readers, iteration it - 1, have finished)
@@ -641,7 +640,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
 #endif
   }
 #endif
-  __syncthreads();   // satol, wacc, blive
+  __syncwarp();   // the warp's staged TS records, wacc
 #if BDFB_SPLIT_TS_SMEM
   TS& s = *reinterpret_cast<TS*>(smem + threadIdx.x * TS_STRIDE);
 #else
@@ -714,7 +713,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
       }
     }
     // one call site: lanes that resumed and lanes that consumed an RHS value run the rest together
-    if (run) act = SP::template finish<BDFB_SPLIT_INIT_KERNEL != 0>(o, s, w, act, lu, y, fext, aux, satol, counter,
+    if (run) act = SP::template finish<BDFB_SPLIT_INIT_KERNEL != 0>(o, s, w, act, lu, y, fext, aux, atol, counter,
                                                                       wacc[warp], cs);
     if (act == I::A_STORE) init = true;   // deferred store (K_init)
   }
@@ -737,7 +736,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     oi = __shfl_sync(0xffffffffu, oi, 0);
     if (init) b.ilist[oi + __popc(bi & below)] = (int)slot;
     const unsigned bl = __ballot_sync(0xffffffffu, act == I::A_RET);
-    if (lane == 0 && bl) atomicAdd(&blive, (unsigned long long)__popc(bl));
+    if (lane == 0 && bl) atomicAdd(&b.live[it & 1], (unsigned long long)__popc(bl));
   }
 #if BDFB_SPLIT_TS_SMEM
   __syncwarp();
@@ -747,8 +746,7 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
     for (long long i = lane; i < nrec; i += 32) dst[i] = wsm[i];
   }
 #endif
-  __syncthreads();
-  if (threadIdx.x == 0 && blive) atomicAdd(&b.live[it & 1], blive);
+  __syncwarp();
   if (lane == 0 && wacc[warp].cells_done) {
     const Agg& a = wacc[warp];
     atomicAdd(&agg->n_failed, a.n_failed);
@@ -870,6 +868,22 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_kernel(SplitBufs b
     }
     if (g.lane == 0) t->coop = r;
     g.sync();
+  }
+}
+
+// K_jac variant: one thread per Jacobian-list entry, the generated straight-line column-major Jacobian
+// (gen/tpc_<mech>.cuh jac_cm) reading yq from VEC (stride 32) into the slot's J record, scratch in its LU record
+// (K_lu overwrites it right after).  Selected with BDFB_SPLIT_JAC_TPC=1 (measurement).
+template <class Mech, class GM, int LS = LS_DENSE>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_tpc_kernel(SplitBufs b, int it) {
+  using SP = Split<Mech, GM, LS>;
+  const long long cnt = b.cnt[3 * (it & 1) + 1];
+  for (long long e = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; e < cnt;
+       e += (long long)gridDim.x * BDFB_SPLIT_BLOCK) {
+    const long long slot = b.jlist[e];
+    const typename SP::W w = SP::ws(b, slot);
+    TS* t = SP::ts(b, slot);
+    t->coop = Mech::template jac_cm<32>(&w.yq(0), t->aux, b.J + slot * SP::JREC, SP::lurec(b, slot));
   }
 }
 

@@ -86,6 +86,8 @@ struct SplitK {
       if (want > sm) sm = want;
     }
     split_init_kernel<Mech, GM, LS><<<gs, blk, 0, st>>>(b);
+    bool jac_tpc = false;   // BDFB_SPLIT_JAC_TPC=1: thread-per-entry generated Jacobian (measurement)
+    if (const char* jt = getenv("BDFB_SPLIT_JAC_TPC")) jac_tpc = atoi(jt) == 1;
     int n = 1;
     cudaError_t e;
     for (int i = 0; i < SPLIT_PHASES; ++i) phase_ms[i] = 0.0;
@@ -117,6 +119,8 @@ struct SplitK {
         } else if constexpr (LS == LS_DENSE) {   // the matrix-free linear solvers have no setup kernels
           if (b.jac_dq)
             split_dqjac_kernel<Mech, GM, LS><<<gdq, blk, 0, ss>>>(b, it);
+          else if (jac_tpc)
+            split_jac_tpc_kernel<Mech, GM, LS><<<(unsigned)gm.rhs_grid, blk, 0, ss>>>(b, it);
           else
             split_jac_kernel<Mech, GM, LS><<<gjac, blk, jac_smem(), ss>>>(b, it);
         }
