@@ -31,6 +31,7 @@ Emitted device functions (struct Tpc_<name>):
 from __future__ import annotations
 
 import json
+import re
 import math
 import os
 import struct
@@ -278,6 +279,7 @@ def generate(name, out_dir):
         A("  }\n")
 
     # ------------------------------------------------------------------ rhs
+    rhs_start = len(L)
     A(f"  __device__ __forceinline__ static int rhs(const double (&yv)[{N}], double rho, double (&f)[{N}]) {{\n")
     for k in range(N):
         A(f"  const double y{k} = yv[{k}];\n")
@@ -287,18 +289,29 @@ def generate(name, out_dir):
     else:
         _nasa(A, tab, tm, eg_body)
     post_thermo(A)
+    # cv = sum_k y_k cv_k before the reactions (same terms, same order as a fused tail): the y_k die here
+    # instead of staying live across the reaction loop
+    A("  double cv = 0.0;\n")
+
+    def cv_body(k, a):
+        A(f"    cv = fma(y{k} * {d(RU / W[k])}, {d(a[0] - 1)} + T * ({d(a[1])} + T * ({d(a[2])} + T * ({d(a[3])} + T * {d(a[4])}))), cv);\n")
+
+    def cv_body_sel(k, c):
+        A(f"    cv = fma(y{k} * {d(RU / W[k])}, {c(0, lambda x: x - 1)} + T * ({c(1)} + T * ({c(2)} + T * ({c(3)} + T * {c(4)}))), cv);\n")
+    if NASA_SELECT:
+        _nasa_sel(A, tab, tm, cv_body_sel)
+    else:
+        _nasa(A, tab, tm, cv_body)
     for k in range(K):
         A(f"  double w{k} = 0.0;\n")
     for r, x in enumerate(rx):
         reaction(A, r, x, False)
-    A("  double cv = 0.0, su = 0.0;\n")
+    A("  double su = 0.0;\n")
 
     def tail_body(k, a):
-        A(f"    cv = fma(y{k} * {d(RU / W[k])}, {d(a[0] - 1)} + T * ({d(a[1])} + T * ({d(a[2])} + T * ({d(a[3])} + T * {d(a[4])}))), cv);\n")
         A(f"    su = fma({d(a[0] - 1)} + T * ({d(a[1] / 2)} + T * ({d(a[2] / 3)} + T * ({d(a[3] / 4)} + T * {d(a[4] / 5)}))) + "
           f"{d(a[5])} * invT, w{k}, su);\n")
     def tail_body_sel(k, c):
-        A(f"    cv = fma(y{k} * {d(RU / W[k])}, {c(0, lambda x: x - 1)} + T * ({c(1)} + T * ({c(2)} + T * ({c(3)} + T * {c(4)}))), cv);\n")
         A(f"    su = fma({c(0, lambda x: x - 1)} + T * ({c(1, lambda x: x / 2)} + T * ({c(2, lambda x: x / 3)} + T * ({c(3, lambda x: x / 4)} + T * {c(4, lambda x: x / 5)}))) + "
           f"{c(5)} * invT, w{k}, su);\n")
     if NASA_SELECT:
@@ -309,6 +322,25 @@ def generate(name, out_dir):
     for k in range(K):
         A(f"  f[{k}] = {d(W[k])} * w{k} * irho;\n")
     A(f"  f[{K}] = -su * {d(RU)} * T / (rho * cv);\n  return 0;\n  }}\n\n")
+    # rhs_sm<SS>: the same operations with e^{-g/RT} and its reciprocal in a per-thread shared-memory column
+    # (sm[k SS] and sm[(K + k) SS], SS = the block's thread count) instead of registers: 2K fewer live values
+    # across the reaction loop (the register-resident version spills at 168 registers)
+    src = "".join(L[rhs_start:])
+    src = src.replace(f"static int rhs(const double (&yv)[{N}], double rho, double (&f)[{N}]) {{",
+                      f"static int rhs_sm(const double (&yv)[{N}], double rho, double (&f)[{N}], "
+                      f"double* __restrict__ sm) {{", 1)
+    src = src.replace("  __device__ __forceinline__ static int rhs_sm", "  template <int SS>\n  __device__ __forceinline__ static int rhs_sm", 1)
+    src = re.sub(r"  double eg(\d+);\n", "", src)
+    src = re.sub(r"const double ieg(\d+) = 1\.0 / eg(\d+);",
+                 lambda m: f"sm[{K + int(m.group(1))} * SS] = 1.0 / sm[{int(m.group(2))} * SS];", src)
+    src = re.sub(r"(?<![A-Za-z0-9_])ieg(\d+)\b", lambda m: f"sm[{K + int(m.group(1))} * SS]", src)
+    src = re.sub(r"(?<![A-Za-z0-9_])eg(\d+)\b", lambda m: f"sm[{int(m.group(1))} * SS]", src)
+    # reads through a volatile view, so that the compiler reloads them from shared memory instead of keeping
+    # the stored values live in registers (which would undo the point of the variant)
+    src = src.replace("sm[", "sv[")
+    src = re.sub(r"^(\s*)sv\[([^\]]*)\] = ", lambda m: f"{m.group(1)}sm[{m.group(2)}] = ", src, flags=re.M)
+    src = src.replace("double* __restrict__ sm) {\n", "double* __restrict__ sm) {\n  volatile const double* sv = sm;\n", 1)
+    A(src)
 
     # ------------------------------------------------------------------ jac
     jac_start = len(L)
@@ -427,7 +459,6 @@ def generate(name, out_dir):
     A("  }\n  return 0;\n  }\n")
     # jac_cm: the same body with y at yp[k * SY] (e.g. a warp-blocked SoA state), J column-major and
     # contiguous (J(i, j) at J[j * N + i], the split kernel's per-cell record) and contiguous scratch
-    import re
     body = "".join(L[jac_start:])
     body = body.replace("  template <long long SS>  // compile-time element stride (0: runtime Srt)\n",
                         "  template <long long SY>  // element stride of y; J column-major, contiguous\n")

@@ -1093,11 +1093,13 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b,
 // VAR 0: 128-thread blocks, 3 per SM, free-running warps; VAR 1: the same with a block barrier per
 // grid-stride trip; VAR 2: one 384-thread block per SM with a barrier per trip, so that all 12 warps of an SM
 // walk the ~10K-instruction generated RHS together (instruction-cache locality; see erk.cu)
+// VAR 3: VAR 0 with e^{-g/RT} and its reciprocals in shared memory (rhs_sm: 2K fewer live registers)
 template <int VAR>
 struct RhsVar {
   static constexpr int BLOCK = VAR == 2 ? 384 : BDFB_SPLIT_BLOCK;
-  static constexpr int MINB = VAR == 2 ? 1 : BDFB_SPLIT_RHS_MINB;
-  static constexpr bool SYNC = VAR != 0;
+  static constexpr int MINB = VAR == 2 ? 1 : (VAR == 4 ? 4 : BDFB_SPLIT_RHS_MINB);   // VAR 4: VAR 3 at 16 warps/SM
+  static constexpr bool SYNC = VAR == 1 || VAR == 2;
+  static constexpr bool SM = VAR == 3 || VAR == 4;
 };
 template <class Mech, class GM, int LS = LS_DENSE, int VAR = 0>
 __global__ void __launch_bounds__(RhsVar<VAR>::BLOCK, RhsVar<VAR>::MINB) split_rhs_kernel(SplitBufs b, int it) {
@@ -1118,7 +1120,13 @@ __global__ void __launch_bounds__(RhsVar<VAR>::BLOCK, RhsVar<VAR>::MINB) split_r
     double yv[N], fv[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) yv[k] = w.yq(k);
-    const int rv = Mech::rhs(yv, t->aux, fv);
+    int rv;
+    if constexpr (V::SM) {
+      extern __shared__ double rsm[];   // 2K doubles per thread, column-major by thread
+      rv = Mech::template rhs_sm<V::BLOCK>(yv, t->aux, fv, rsm + threadIdx.x);
+    } else {
+      rv = Mech::rhs(yv, t->aux, fv);
+    }
 #pragma unroll
     for (int k = 0; k < N; ++k) w.fr(k) = fv[k] + w.fext(k);
     b.rv[slot] = rv;

@@ -77,6 +77,17 @@ __device__ __forceinline__ double wnorm_k(const EW<N>& w, int s) {   // ||k_s||_
 // the request of a phase, the generated RHS and f + F into its k slot (k1 for f(t0, y0) and f(tn, yn), k2 for
 // the initial-step probe, k_s for stage s), out of line: the register-hungry RHS gets its own allocation and
 // the state machine around it stays light
+// e^{-g/RT} and its reciprocals of the generated RHS in shared memory (rhs_sm; 2K doubles per thread) when they
+// fit next to the scalar state, else in registers
+template <class Mech>
+__host__ __device__ constexpr bool erk_sm() {
+  return 2 * Mech::K * BDFB_ERK_BLOCK * 8 + 15 * 8 * BDFB_ERK_BLOCK <= 200 * 1024;
+}
+template <class Mech>
+__host__ __device__ constexpr size_t erk_sm_bytes() {
+  return erk_sm<Mech>() ? sizeof(double) * 2 * Mech::K * BDFB_ERK_BLOCK : 0;
+}
+
 template <class Mech>
 __device__ __noinline__ int erk_eval(const EW<Mech::N> w, int phase, double hs, double h0, double rho) {
   constexpr int N = Mech::N;
@@ -108,7 +119,13 @@ __device__ __noinline__ int erk_eval(const EW<Mech::N> w, int phase, double hs, 
       yv[i] = hs * acc + w.y(i);
     }
   }
-  const int rv = Mech::rhs(yv, rho, fv);
+  int rv;
+  if constexpr (erk_sm<Mech>()) {
+    extern __shared__ double esm[];
+    rv = Mech::template rhs_sm<BDFB_ERK_BLOCK>(yv, rho, fv, esm + threadIdx.x);
+  } else {
+    rv = Mech::rhs(yv, rho, fv);
+  }
 #pragma unroll
   for (int i = 0; i < N; ++i) w.k(dst, i) = fv[i] + w.F(i);
   return rv;
@@ -356,7 +373,12 @@ cudaError_t geometry(int device, long long ncells, long long* threads, long long
   int nsm = 0, pr = 0;
   cudaError_t e;
   if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pr, erk_kernel<Mech>, BDFB_ERK_BLOCK, 0)) != cudaSuccess)
+  if (erk_sm_bytes<Mech>() > 48 * 1024 &&
+      (e = cudaFuncSetAttribute(erk_kernel<Mech>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)erk_sm_bytes<Mech>())) != cudaSuccess)
+    return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pr, erk_kernel<Mech>, BDFB_ERK_BLOCK,
+                                                         erk_sm_bytes<Mech>())) != cudaSuccess)
     return e;
   if (pr < 1) return cudaErrorInvalidConfiguration;
   long long blocks = (long long)nsm * pr;
@@ -384,13 +406,13 @@ cudaError_t erk_integrate(int mech, const Opts& o, double* y, const double* fext
   const unsigned grid = (unsigned)(threads / BDFB_ERK_BLOCK);
   switch (mech) {
     case BDFB_MODEL_MECH_H2:
-      erk_kernel<Tpc_h2_lidryer><<<grid, BDFB_ERK_BLOCK, 0, st>>>(o, y, fext, aux, atol, ws, counter, agg, cs);
+      erk_kernel<Tpc_h2_lidryer><<<grid, BDFB_ERK_BLOCK, erk_sm_bytes<Tpc_h2_lidryer>(), st>>>(o, y, fext, aux, atol, ws, counter, agg, cs);
       break;
     case BDFB_MODEL_MECH_DRM19:
-      erk_kernel<Tpc_drm19_class><<<grid, BDFB_ERK_BLOCK, 0, st>>>(o, y, fext, aux, atol, ws, counter, agg, cs);
+      erk_kernel<Tpc_drm19_class><<<grid, BDFB_ERK_BLOCK, erk_sm_bytes<Tpc_drm19_class>(), st>>>(o, y, fext, aux, atol, ws, counter, agg, cs);
       break;
     case BDFB_MODEL_MECH_GRI53:
-      erk_kernel<Tpc_gri53_class><<<grid, BDFB_ERK_BLOCK, 0, st>>>(o, y, fext, aux, atol, ws, counter, agg, cs);
+      erk_kernel<Tpc_gri53_class><<<grid, BDFB_ERK_BLOCK, erk_sm_bytes<Tpc_gri53_class>(), st>>>(o, y, fext, aux, atol, ws, counter, agg, cs);
       break;
     default:
       return cudaErrorInvalidValue;

@@ -19,22 +19,35 @@
 
 namespace bdfb {
 
-// K_rhs organisation (RhsVar in bdf_split.cuh): BDFB_SPLIT_RHS_VAR = 0 | 1 | 2 (default 0)
+// K_rhs organisation (RhsVar in bdf_split.cuh): BDFB_SPLIT_RHS_VAR = 0..4 overrides; default 3 (e^{-g/RT} in
+// shared memory: C4 K_rhs 1013 -> 930 ms, no spills) when its 2K doubles per thread fit 64 KB per block, else 0
+template <class Mech>
 static int rhs_var() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BDFB_SPLIT_RHS_VAR");
-    v = e ? atoi(e) : 0;
-    if (v < 0 || v > 2) v = 0;
+    v = e ? atoi(e) : (2 * Mech::K * RhsVar<3>::BLOCK * 8 <= 64 * 1024 ? 3 : 0);
+    if (v < 0 || v > 4) v = 0;
   }
   return v;
 }
 
+template <class Mech>
+constexpr size_t rhs_sm_bytes() {
+  return sizeof(double) * 2 * Mech::K * RhsVar<3>::BLOCK;
+}
+
 template <class Mech, class GM, int LS>
 cudaError_t split_rhs_run(unsigned grid, cudaStream_t st, const SplitBufs& b, int it) {
-  switch (rhs_var()) {
+  switch (rhs_var<Mech>()) {
     case 1: split_rhs_kernel<Mech, GM, LS, 1><<<grid, RhsVar<1>::BLOCK, 0, st>>>(b, it); break;
     case 2: split_rhs_kernel<Mech, GM, LS, 2><<<grid, RhsVar<2>::BLOCK, 0, st>>>(b, it); break;
+    case 3:
+      split_rhs_kernel<Mech, GM, LS, 3><<<grid, RhsVar<3>::BLOCK, rhs_sm_bytes<Mech>(), st>>>(b, it);
+      break;
+    case 4:
+      split_rhs_kernel<Mech, GM, LS, 4><<<grid, RhsVar<4>::BLOCK, rhs_sm_bytes<Mech>(), st>>>(b, it);
+      break;
     default: split_rhs_kernel<Mech, GM, LS, 0><<<grid, RhsVar<0>::BLOCK, 0, st>>>(b, it);
   }
   return cudaSuccess;
@@ -45,11 +58,25 @@ cudaError_t split_rhs_run(unsigned grid, cudaStream_t st, const SplitBufs& b, in
 template <class Mech, class GM, int LS>
 cudaError_t split_rhs_occupancy(int* blocks_per_sm) {
   cudaError_t e;
-  switch (rhs_var()) {
+  switch (rhs_var<Mech>()) {
     case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 1>,
                                                             RhsVar<1>::BLOCK, 0); break;
     case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 2>,
                                                             RhsVar<2>::BLOCK, 0); break;
+    case 3:
+      e = cudaFuncSetAttribute(split_rhs_kernel<Mech, GM, LS, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)rhs_sm_bytes<Mech>());
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 3>,
+                                                          RhsVar<3>::BLOCK, rhs_sm_bytes<Mech>());
+      break;
+    case 4:
+      e = cudaFuncSetAttribute(split_rhs_kernel<Mech, GM, LS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)rhs_sm_bytes<Mech>());
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 4>,
+                                                          RhsVar<4>::BLOCK, rhs_sm_bytes<Mech>());
+      break;
     default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 0>,
                                                              RhsVar<0>::BLOCK, 0);
   }
@@ -76,29 +103,45 @@ BDFB_RHS_INST(Tpc_gri53_class, GGRI, LS_GMRES)
 // f = R(y) + F for N cells (YC), the K_rhs code path (diagnostic entry point bdfb_eval_rhs)
 template <class Mech>
 __global__ void __launch_bounds__(128) eval_rhs_kernel(long long N, const double* y, const double* fext,
-                                                       const double* aux, double* f, int* status) {
+                                                       const double* aux, double* f, int* status, int use_sm) {
   constexpr int n = Mech::N;
   const long long c = blockIdx.x * 128ll + threadIdx.x;
   if (c >= N) return;
   double yv[n], fv[n];
 #pragma unroll
   for (int i = 0; i < n; ++i) yv[i] = y[(long long)i * N + c];
-  const int rv = Mech::rhs(yv, aux[c], fv);
+  int rv;
+  if (use_sm) {   // the device function K_rhs runs (the host's RhsVar choice)
+    extern __shared__ double rsm[];
+    rv = Mech::template rhs_sm<128>(yv, aux[c], fv, rsm + threadIdx.x);
+  } else {
+    rv = Mech::rhs(yv, aux[c], fv);
+  }
 #pragma unroll
   for (int i = 0; i < n; ++i) f[(long long)i * N + c] = fv[i] + (fext ? fext[(long long)i * N + c] : 0.0);
   if (status) status[c] = rv;
+}
+
+template <class Mech>
+static void launch_eval_rhs(unsigned g, long long N, const double* y, const double* fext, const double* aux, double* f,
+                            int* status, cudaStream_t st) {
+  const int sm = rhs_var<Mech>() >= 3;
+  const size_t bytes = sm ? sizeof(double) * 2 * Mech::K * 128 : 0;
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(eval_rhs_kernel<Mech>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  eval_rhs_kernel<Mech><<<g, 128, bytes, st>>>(N, y, fext, aux, f, status, sm);
 }
 
 cudaError_t tpc_eval_rhs(int mech, long long N, const double* y, const double* fext, const double* aux, double* f,
                          int* status, cudaStream_t st) {
   const unsigned g = (unsigned)((N + 127) / 128);
   switch (mech) {
-    case BDFB_MODEL_MECH_H2: eval_rhs_kernel<Tpc_h2_lidryer><<<g, 128, 0, st>>>(N, y, fext, aux, f, status); break;
+    case BDFB_MODEL_MECH_H2: launch_eval_rhs<Tpc_h2_lidryer>(g, N, y, fext, aux, f, status, st); break;
     case BDFB_MODEL_MECH_DRM19:
-      eval_rhs_kernel<Tpc_drm19_class><<<g, 128, 0, st>>>(N, y, fext, aux, f, status);
+      launch_eval_rhs<Tpc_drm19_class>(g, N, y, fext, aux, f, status, st);
       break;
     case BDFB_MODEL_MECH_GRI53:
-      eval_rhs_kernel<Tpc_gri53_class><<<g, 128, 0, st>>>(N, y, fext, aux, f, status);
+      launch_eval_rhs<Tpc_gri53_class>(g, N, y, fext, aux, f, status, st);
       break;
     default: return cudaErrorInvalidValue;
   }
