@@ -631,12 +631,20 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, BDFB_SPLIT_CTL_MINB)
 #if BDFB_SPLIT_PREFETCH
   // bulk L2 prefetch (one TMA instruction each) of the warp's 32 LU records and of its state rows: the
   // Newton solve's column loads and the Nordsieck passes then hit L2 instead of waiting on HBM
+  // (3: the warp's Nordsieck rows only, 4: its Nordsieck, weight, correction and request rows -- the rows the
+  // ATTEMPT pass and the residual read, 6 n resp. 9 n elements x 256 B)
   if (lane == 0 && w0 + 32 <= b.slots) {
+#if BDFB_SPLIT_PREFETCH <= 2
     const double* lu0 = SP::lurec(b, w0);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lu0), "r"((unsigned)(32 * SP::LUREC * 8)) : "memory");
-#if BDFB_SPLIT_PREFETCH > 1
+#endif
+#if BDFB_SPLIT_PREFETCH == 2
     const double* v0 = b.vec + ((w0 >> 5) * SP::D) * 32;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v0), "r"((unsigned)(SP::D * 32 * 8)) : "memory");
+#elif BDFB_SPLIT_PREFETCH >= 3
+    constexpr int ROWS = BDFB_SPLIT_PREFETCH == 3 ? (QMAX + 1) * N : SP::W::O_DEL;
+    const double* v0 = b.vec + ((w0 >> 5) * SP::D) * 32;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v0), "r"((unsigned)(ROWS * 32 * 8)) : "memory");
 #endif
   }
 #endif
