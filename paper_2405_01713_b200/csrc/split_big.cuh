@@ -34,17 +34,27 @@ struct LanesOf<Tpc_gri53_class> {
   using GM = GMStub<Tpc_gri53_class::N>;
 };
 
-// K_jac, one cell per warp (grid-stride over the Jacobian list); status -> TS.coop
+// K_jac, one cell per warp (grid-stride over the Jacobian list), two warps per block; the Jacobian is assembled in
+// shared memory (its sparse scattered row updates are read-modify-writes: in the J record they were HBM round
+// trips) and copied to the record coalesced; status -> TS.coop
+constexpr int JL_WARPS = 2;
+template <class Mech>
+struct JacLanesSmem {
+  using MR = typename LanesOf<Mech>::type;
+  static constexpr int MS = Mech::N | 1;
+  static constexpr int PER_WARP = Mech::N * MS + MR::SG + MR::JG;   // doubles
+};
 template <class Mech, class GM, int LS>
-__global__ void __launch_bounds__(128) split_jac_lanes_kernel(SplitBufs b, int it) {
+__global__ void __launch_bounds__(32 * JL_WARPS) split_jac_lanes_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM, LS>;
   using MR = typename LanesOf<Mech>::type;
-  constexpr int N = Mech::N, R = MR::R;
+  constexpr int N = Mech::N, R = MR::R, MS = JacLanesSmem<Mech>::MS;
   extern __shared__ double smem[];
   Grp<32> g;
-  double* sc = smem + (threadIdx.x >> 5) * (MR::SG + MR::JG);
-  const long long cnt = b.cnt[3 * (it & 1) + 1], warps = (long long)gridDim.x * 4;
-  for (long long e = ((long long)blockIdx.x * 128 + threadIdx.x) >> 5; e < cnt; e += warps) {
+  double* A = smem + (threadIdx.x >> 5) * JacLanesSmem<Mech>::PER_WARP;
+  double* sc = A + N * MS;
+  const long long cnt = b.cnt[3 * (it & 1) + 1], warps = (long long)gridDim.x * JL_WARPS;
+  for (long long e = ((long long)blockIdx.x * 32 * JL_WARPS + threadIdx.x) >> 5; e < cnt; e += warps) {
     const long long slot = b.jlist[e];
     const typename SP::W w = SP::ws(b, slot);
     TS* t = SP::ts(b, slot);
@@ -54,8 +64,18 @@ __global__ void __launch_bounds__(128) split_jac_lanes_kernel(SplitBufs b, int i
       const int i = g.lane + 32 * r;
       yy[r] = i < N ? w.yq(i) : 0.0;
     }
-    // row i, column j at J[j N + i] (the record's column-major layout)
-    const int rv = MR::jac(g, yy, t->aux, b.J + slot * SP::JREC, 1, N, sc, sc + MR::SG);
+    // row i, column j at A[j MS + i], then to the record's column-major J[j N + i]
+    const int rv = MR::jac(g, yy, t->aux, A, 1, MS, sc, sc + MR::SG);
+    g.sync();
+    if (!rv) {
+      double* J = b.J + slot * SP::JREC;
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = g.lane + 32 * r;
+          if (i < N) J[j * N + i] = A[j * MS + i];
+        }
+    }
     if (g.lane == 0) t->coop = rv ? 1 : 0;
     g.sync();
   }

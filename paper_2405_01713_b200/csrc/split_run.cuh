@@ -22,8 +22,7 @@ struct SplitK {
   static constexpr bool BIG = Mech::N > 32;   // split_big.cuh setup kernels (lanes Jacobian, register-row LU)
   static constexpr size_t jac_smem() {
     if constexpr (BIG) {
-      using MR = typename LanesOf<Mech>::type;
-      return sizeof(double) * (size_t)(MR::SG + MR::JG) * 4;
+      return sizeof(double) * (size_t)JacLanesSmem<Mech>::PER_WARP * JL_WARPS;
     } else {
       return sizeof(double) * (size_t)(GM::SG + GM::JG + GM::N * (GM::N | 1)) * (BDFB_SPLIT_BLOCK / GM::G);
     }
@@ -115,7 +114,7 @@ struct SplitK {
         }
         if constexpr (LS == LS_DENSE && BIG) {   // n > 32: lanes Jacobian, one cell per warp
           const unsigned gj = (unsigned)gm.setup_grid;
-          split_jac_lanes_kernel<Mech, GM, LS><<<gj, 128, jac_smem(), ss>>>(b, it);
+          split_jac_lanes_kernel<Mech, GM, LS><<<gj, 32 * JL_WARPS, jac_smem(), ss>>>(b, it);
         } else if constexpr (LS == LS_DENSE) {   // the matrix-free linear solvers have no setup kernels
           if (b.jac_dq)
             split_dqjac_kernel<Mech, GM, LS><<<gdq, blk, 0, ss>>>(b, it);
