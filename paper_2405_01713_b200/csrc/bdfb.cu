@@ -579,6 +579,7 @@ static int run_global(bdfb_batch* b, const Opts& o, double* y, const double* fex
       const int s2 = (int)(sizeof(double) * GLK<Model>::PG_SET * GLK<Model>::GPB);
       if (s1 > 48 * 1024) cudaFuncSetAttribute(gl_rhs<Model>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
       if (s2 > 48 * 1024) cudaFuncSetAttribute(gl_setup<Model>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2);
+      cudaFuncSetAttribute(gl_lu<Model::N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gl_lu_smem<Model::N>());
     } else {
       auto* kr = gk_rhs<Model>;
       auto* ks = gk_setup<Model>;

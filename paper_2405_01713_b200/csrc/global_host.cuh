@@ -274,7 +274,7 @@ struct GlobalRunner {
             N, 1, gamma, B.v.yq, aux, B.J, B.LU, B.perm, B.invd, B.flag, 1);
       }
       ++launches; gl_lu<Model::N><<<(unsigned)((N + GLU<Model::N>::CPB - 1) / GLU<Model::N>::CPB), GLU<Model::N>::T,
-                                    0, st>>>(N, gamma, B.J, B.LU, B.perm, B.invd, B.flag);
+                                    gl_lu_smem<Model::N>(), st>>>(N, gamma, B.J, B.LU, B.perm, B.invd, B.flag);
     } else {
       ++launches; gk_setup<Model><<<gridg(), 128, smemg(), st>>>(prm, N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU,
                                                                   B.pos, B.perm, B.invd, B.flag);

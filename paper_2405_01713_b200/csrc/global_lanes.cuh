@@ -314,29 +314,45 @@ template <int NN>
 __global__ void __launch_bounds__(GLU<NN>::T, 1)
     gl_lu(long long N, double gamma, const double* J, double* LU, int* perm, double* invd, int* flag) {
   __shared__ GLUShared<NN> sh;
-  constexpr int TC = GLU<NN>::TC;
+  // the block's six matrices staged element-major, cell-minor (T[e CPB + cb]): the cell-minor HBM layout is then
+  // read and written as runs of CPB consecutive cells instead of one scattered 8-byte access per row and column
+  // (ncu: the scattered stores and loads were ~40% of the kernel's stall samples)
+  extern __shared__ double T[];
+  constexpr int TC = GLU<NN>::TC, CPB = GLU<NN>::CPB, E = NN * NN;
   const int cb = threadIdx.x / TC, i = threadIdx.x % TC;
-  const long long c = (long long)blockIdx.x * GLU<NN>::CPB + cb;
+  const long long c0 = (long long)blockIdx.x * CPB, c = c0 + cb;
+  const int ncb = N - c0 < CPB ? (int)(N - c0) : CPB;
+  for (int x = threadIdx.x; x < E * CPB; x += blockDim.x) {
+    const int e = x / CPB, cc = x - e * CPB;
+    if (cc < ncb) T[x] = J[(long long)e * N + c0 + cc];
+  }
+  __syncthreads();
   const bool alive = c < N;
   const bool own = i < NN && alive;
   double a[NN];
 #pragma unroll
-  for (int j = 0; j < NN; ++j) a[j] = own ? (i == j ? 1.0 : 0.0) - gamma * J[((long long)i * NN + j) * N + c] : 0.0;
+  for (int j = 0; j < NN; ++j) a[j] = own ? (i == j ? 1.0 : 0.0) - gamma * T[(i * NN + j) * CPB + cb] : 0.0;
   int pos = i;
   double dinv = 0.0;
   const int info = glu_columns<NN>(sh, a, pos, dinv, i, cb, alive, std::make_integer_sequence<int, NN>{});
-  if (!alive) return;
-  if (info) {
-    if (i == 0) atomicOr(flag, 1);
-    return;
-  }
-  if (own) {
-    const long long p = pos;
+  if (alive && info && i == 0) atomicOr(flag, 1);
+  if (own && !info) {
+    const int p = pos;
 #pragma unroll
-    for (int j = 0; j < NN; ++j) LU[(p * NN + j) * N + c] = a[j];
-    perm[p * N + c] = i;
-    invd[p * N + c] = dinv;
+    for (int j = 0; j < NN; ++j) T[(p * NN + j) * CPB + cb] = a[j];
+    perm[(long long)p * N + c] = i;
+    invd[(long long)p * N + c] = dinv;
   }
+  __syncthreads();
+  for (int x = threadIdx.x; x < E * CPB; x += blockDim.x) {
+    const int e = x / CPB, cc = x - e * CPB;
+    if (cc < ncb) LU[(long long)e * N + c0 + cc] = T[x];
+  }
+}
+
+template <int NN>
+constexpr size_t gl_lu_smem() {
+  return sizeof(double) * (size_t)NN * NN * GLU<NN>::CPB;
 }
 
 template <int NN>
