@@ -465,6 +465,7 @@ struct GroupIntegrator {
       case PH_ETF3: act = -5; break;
       default: act = X_LOAD; break;
     }
+    g.sync();   // every lane has read the phase before any lane rewrites it (racecheck)
     for (;;) {
       switch (act) {
         case -1: {  // f(t0, y0) ready
@@ -742,7 +743,9 @@ struct GroupIntegrator {
         }
         case X_LOAD: {
           g.sync();
-          if (s->cell + 1 < s->chunk_end) {
+          const bool in_chunk = s->cell + 1 < s->chunk_end;
+          g.sync();   // every lane has read the record before lane 0 updates it (racecheck)
+          if (in_chunk) {
             if (g.lane == 0) s->cell = s->cell + 1;
           } else {
             long long c0 = 0;

@@ -1253,6 +1253,7 @@ __global__ void __launch_bounds__(BDFB_TPC_BLOCK, BDFB_TPC_MINB)
   for (;;) {
     live = I::trip(o, s, w, live, rv, fr, y, fext, aux, satol, counter, acc, cs, coop) == I::A_RET;
 #ifndef BDFB_NO_BLOCK_SYNC
+    __syncwarp();   // reconverge the warp before the block barrier (synccheck)
     if (!__syncthreads_or(live)) break;
 #else
     if (!__any_sync(0xffffffffu, live)) break;
