@@ -156,7 +156,7 @@ def phase_flops(cfg, st, method="bdf", ls="dense"):
     u = unit_flops(cfg)
     att = st["nst"] + st["netf"] + st["ncfn"]
     if method == "erk4":   # one kernel: RHS calls and the stage algebra; no algebraic solver
-        return {"rhs": st["nfe"] * u["rhs"], "ctl": (st["nst"] + st["netf"]) * u["erk_attempt"]}
+        return {"rhs": st["nfe"] * u["rhs"], "ctl": (st["nst"] + st["netf"]) * u["erk_attempt"], "jac": 0, "lu": 0}
     nli = st.get("nli", 0)   # GMRES: one RHS call per Krylov iteration (Jv quotient)
     ph = {"rhs": (st["nfe"] + nli) * u["rhs"], "jac": st["nje"] * u["jac"], "lu": st["nsetups"] * u["setup"],
           "ctl": st["nni"] * u["solve"] + att * u["attempt"] + st["nst"] * u["step"] + nli * u["krylov"]}
@@ -517,7 +517,7 @@ def main():
     roof = dict(roof_common, achieved=whole, frac=whole / peak, traffic=traffic_per_launch(cfg, N), kernel=kname,
                 kernel_ms=statistics.mean(kern_ms), flops_per_launch=statistics.mean(flops))
     phases = None
-    if phase_ms and phase_ms[0] and args.method == "bdf":
+    if phase_ms and phase_ms[0]:
         # SPLIT: four kernels per trip, timed per phase with CUDA events on the launch stream.  The roofline is
         # the dominant kernel's algorithmic FP64 fraction; the whole-step fraction sits beside it; K_ctl's HBM
         # traffic (its slot-state round trips, an implementation cost, not algorithmic bytes) is a diagnostic.
@@ -536,7 +536,8 @@ def main():
                                       "model": "DESIGN.md §6 (slot-state round trips: implementation bytes)"}
         dom = max(pm, key=pm.get)
         big = n > 32   # split_big.cuh setup kernels
-        knames = {"ctl": "split_ctl_kernel", "jac": "split_jac_lanes_kernel" if big else "split_jac_kernel",
+        knames = {"ctl": "erk_ctl_kernel" if args.method == "erk4" else "split_ctl_kernel",
+                  "jac": "split_jac_lanes_kernel" if big else "split_jac_kernel",
                   "lu": "split_lu_rows_kernel" if big else "split_lu_kernel", "rhs": "split_rhs_kernel"}
         roof = dict(roof_common, achieved=phases[dom]["tflops"], frac=phases[dom]["frac"],
                     traffic=traffic_split(cfg, stats[-1]) if dom == "ctl" else None,

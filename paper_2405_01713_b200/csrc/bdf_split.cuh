@@ -184,7 +184,8 @@ struct Split {
   static constexpr int X_V = D0, X_FY = X_V + (KMAXL + 1) * N, X_H = X_FY + N, X_GIV = X_H + (KMAXL + 1) * KMAXL,
                        X_SIG = X_GIV + 2 * KMAXL, X_BETA = X_SIG + 1, X_ROT = X_BETA + 1, X_L = X_ROT + 1,
                        X_DQ = X_L + 1, X_NLI = X_DQ + 1, X_END = X_NLI + 1;
-  static constexpr int D = LS == LS_DENSE ? D0 : (LS == LS_DIAG ? ((D0 + N + 1 + 1) & ~1) : ((X_END + 1) & ~1));
+  static constexpr int D = (LS == LS_DENSE || LS == 3 /* LS_ERK: erk_split.cuh */)
+                               ? D0 : (LS == LS_DIAG ? ((D0 + N + 1 + 1) & ~1) : ((X_END + 1) & ~1));
   static constexpr int JREC = (N * N + 3) / 4 * 4;
   static constexpr int LU_INVD = N * N, LU_PERM = N * N + N;     // perm: ints at double offset LU_PERM
   // perm: ints at double offset LU_PERM (contiguous records) or one double element per entry (SoA)

@@ -33,6 +33,7 @@
 #include "tpc_api.h"
 #include "bdf_split.cuh"
 #include "split_api.h"
+#include "erk_split.cuh"
 #include "erk_api.h"
 
 using namespace bdfb;
@@ -133,10 +134,13 @@ static void free_split(bdfb_batch* b) {
 }
 
 // SPLIT kernel: slot pool of S = min(n_cells rounded up to 32, BDFB_SPLIT_SLOTS env or 393216) slots
+// the pool's organisation: the Newton linear solver, or the SPLIT-organised explicit ERK
+static int split_ls(const bdfb_batch* b) { return b->method == BDFB_METHOD_ERK4 ? LS_ERK : b->ls; }
+
 static int prepare_split(bdfb_batch* b) {
   cudaError_t e = cudaSetDevice(b->device);
   SplitGeom gm{};
-  if (e == cudaSuccess) e = split_geometry(b->model, b->ls, b->device, &gm);
+  if (e == cudaSuccess) e = split_geometry(b->model, split_ls(b), b->device, &gm);
   if (e != cudaSuccess) return cuda_fail(b, e, "split geometry");
   long long cap = 393216;   // measured on C4: 196608 2.51M, 262144 2.65M, 393216 2.78M, 524288 2.76M, 786432 2.79M cells/s
   if (const char* env = getenv("BDFB_SPLIT_SLOTS")) cap = atoll(env) > 0 ? atoll(env) : cap;
@@ -198,7 +202,7 @@ static int launch_split(bdfb_batch* b, const Opts& o, double* y, const double* f
           return fail(b, BDFB_ECUDA, "ordering events");
     }
   }
-  cudaError_t e = split_integrate(b->model, b->ls, o, y, fext, aux, b->d_atol, b->sb, b->sgeom, b->d_counter, b->d_agg,
+  cudaError_t e = split_integrate(b->model, split_ls(b), o, y, fext, aux, b->d_atol, b->sb, b->sgeom, b->d_counter, b->d_agg,
                                   b->cs, b->h_live, batch, st, &launches, b->sev.data(), b->phase_ms,
                                   overlap ? b->st2 : nullptr, overlap ? b->xev.data() : nullptr);
   b->nphases = SPLIT_PHASES;
@@ -241,8 +245,14 @@ static int launch_erk(bdfb_batch* b, const Opts& o, double* y, const double* fex
   return BDFB_OK;
 }
 
+// ERK organisation: the SPLIT pool with K_erk + K_rhs (default), or the persistent erk_kernel (BDFB_ERK_PERSISTENT=1)
+static bool erk_persistent() {
+  const char* e = getenv("BDFB_ERK_PERSISTENT");
+  return e && atoi(e) == 1;
+}
+
 static int prepare_kernel(bdfb_batch* b) {
-  if (b->method == BDFB_METHOD_ERK4) return prepare_erk(b);
+  if (b->method == BDFB_METHOD_ERK4) return erk_persistent() ? prepare_erk(b) : prepare_split(b);
   if (b->opt.mode == BDFB_MODE_PER_CELL && use_split(b)) return prepare_split(b);
   if (b->opt.mode != BDFB_MODE_PER_CELL || !use_tpc(b)) return BDFB_OK;
   long long slots = 0, dps = 0, ips = 0;
@@ -676,7 +686,8 @@ extern "C" int bdfb_integrate(bdfb_batch* b, double t0, double tf, double* y, co
       default: return fail(b, BDFB_EUNSUPPORTED, "global-norm mode: group models only (MECH_H2, MECH_DRM19)");
     }
   }
-  if (b->method == BDFB_METHOD_ERK4) return launch_erk(b, o, y, f_ext, aux, st);
+  if (b->method == BDFB_METHOD_ERK4)
+    return erk_persistent() ? launch_erk(b, o, y, f_ext, aux, st) : launch_split(b, o, y, f_ext, aux, st);
   switch (b->model) {
     case BDFB_MODEL_LINEAR: return launch_integrate<ModelLinear>(b, o, y, f_ext, aux, st);
     case BDFB_MODEL_ROBERTSON: return launch_integrate<ModelRobertson>(b, o, y, f_ext, aux, st);

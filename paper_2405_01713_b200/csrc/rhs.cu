@@ -98,6 +98,9 @@ using GGRI = LanesOf<Tpc_gri53_class>::GM;
 BDFB_RHS_INST(Tpc_gri53_class, GGRI, LS_DENSE)
 BDFB_RHS_INST(Tpc_gri53_class, GGRI, LS_DIAG)
 BDFB_RHS_INST(Tpc_gri53_class, GGRI, LS_GMRES)
+BDFB_RHS_INST(Tpc_h2_lidryer, GH2, 3)      // LS_ERK
+BDFB_RHS_INST(Tpc_drm19_class, GDRM, 3)
+BDFB_RHS_INST(Tpc_gri53_class, GGRI, 3)
 #undef BDFB_RHS_INST
 
 // f = R(y) + F for N cells (YC), the K_rhs code path (diagnostic entry point bdfb_eval_rhs)

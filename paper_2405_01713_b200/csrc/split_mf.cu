@@ -1,4 +1,5 @@
 // split_mf.cu -- the SPLIT per-cell integrator with the matrix-free linear solvers of the Newton
+// iteration and the SPLIT-organised explicit ERK (LS_ERK, erk_split.cuh); originally: the matrix-free solvers of the Newton
 // iteration: CVDiag (LS_DIAG) and inexact Newton-Krylov GMRES with the difference-quotient Jv
 // (LS_GMRES, approaches 1A/1B).  Same slot pool and kernels as split.cu minus the setup
 // kernels (K_jac, K_lu); a separate translation unit of libbdfb.so so that the dense build is unchanged.
@@ -28,6 +29,9 @@ cudaError_t split_mf_geometry(int mech, int ls, int device, SplitGeom* gm) {
     case BDFB_MODEL_MECH_DRM19 * 4 + LS_GMRES: return KDRML<LS_GMRES>::geometry(device, gm);
     case BDFB_MODEL_MECH_GRI53 * 4 + LS_DIAG: return KGRIL<LS_DIAG>::geometry(device, gm);
     case BDFB_MODEL_MECH_GRI53 * 4 + LS_GMRES: return KGRIL<LS_GMRES>::geometry(device, gm);
+    case BDFB_MODEL_MECH_H2 * 4 + LS_ERK: return KH2L<LS_ERK>::geometry(device, gm);
+    case BDFB_MODEL_MECH_DRM19 * 4 + LS_ERK: return KDRML<LS_ERK>::geometry(device, gm);
+    case BDFB_MODEL_MECH_GRI53 * 4 + LS_ERK: return KGRIL<LS_ERK>::geometry(device, gm);
   }
   return cudaErrorInvalidValue;
 }
@@ -46,6 +50,9 @@ cudaError_t split_mf_integrate(int mech, int ls, const Opts& o, double* y, const
     case BDFB_MODEL_MECH_DRM19 * 4 + LS_GMRES: return BDFB_MF_RUN(KDRML<LS_GMRES>);
     case BDFB_MODEL_MECH_GRI53 * 4 + LS_DIAG: return BDFB_MF_RUN(KGRIL<LS_DIAG>);
     case BDFB_MODEL_MECH_GRI53 * 4 + LS_GMRES: return BDFB_MF_RUN(KGRIL<LS_GMRES>);
+    case BDFB_MODEL_MECH_H2 * 4 + LS_ERK: return BDFB_MF_RUN(KH2L<LS_ERK>);
+    case BDFB_MODEL_MECH_DRM19 * 4 + LS_ERK: return BDFB_MF_RUN(KDRML<LS_ERK>);
+    case BDFB_MODEL_MECH_GRI53 * 4 + LS_ERK: return BDFB_MF_RUN(KGRIL<LS_ERK>);
   }
 #undef BDFB_MF_RUN
   return cudaErrorInvalidValue;

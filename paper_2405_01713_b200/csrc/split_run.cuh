@@ -9,6 +9,7 @@
 #include "bdf_split.cuh"
 #include "split_api.h"
 #include "split_big.cuh"
+#include "erk_split.cuh"
 
 namespace bdfb {
 namespace {
@@ -99,7 +100,11 @@ struct SplitK {
         cudaEvent_t* ev = events + k * (SPLIT_PHASES + 2);
         if (ovl && last_l) cudaStreamWaitEvent(st, last_l, 0);
         if (events) cudaEventRecord(ev[0], st);
-        split_ctl_kernel<Mech, GM, LS><<<gctl, BDFB_SPLIT_CTL_BLOCK, sm, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
+        if constexpr (LS == LS_ERK)
+          erk_ctl_kernel<Mech, GM><<<gs, blk, 0, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
+        else
+          split_ctl_kernel<Mech, GM, LS><<<gctl, BDFB_SPLIT_CTL_BLOCK, sm, st>>>(o, b, it, y, fext, aux, atol, counter,
+                                                                           agg, cs);
 #if BDFB_SPLIT_INIT_KERNEL
         split_init_cells_kernel<Mech, GM, LS><<<ginit, blk, 0, st>>>(o, b, it, y, fext, aux, atol, counter, agg, cs);
         ++n;
