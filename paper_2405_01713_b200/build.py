@@ -31,6 +31,21 @@ def sources():
             [os.path.join(PKG, "codegen", "gen_mech.py"), os.path.join(PKG, "codegen", "gen_tpc.py"), __file__])
 
 
+def unit_deps(path: str, seen=None) -> set:
+    """The file and every quoted #include it reaches (transitively), for per-unit rebuild decisions."""
+    seen = set() if seen is None else seen
+    path = os.path.normpath(path)
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as f:
+        for line in f:
+            s = line.strip()
+            if s.startswith("#include \""):
+                unit_deps(os.path.join(os.path.dirname(path), s.split('"')[1]), seen)
+    return seen
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     sys.path.insert(0, REPO)
     from paper_2405_01713_b200.codegen import gen_mech, gen_tpc
@@ -41,20 +56,33 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if all(os.path.getmtime(s) <= t for s in sources()):
             return LIB
     objs, procs = [], []
+    always = [__file__] + glob.glob(os.path.join(REPO, "mechanisms", "*.json"))
     for u in UNITS:
         obj = os.path.join(PKG, "build", u.replace(".cu", ".o"))
         os.makedirs(os.path.dirname(obj), exist_ok=True)
         objs.append(obj)
+        deps = list(unit_deps(os.path.join(CSRC, u))) + always
+        if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in deps):
+            procs.append(None)     # object up to date with every file the unit includes
+            continue
         fl = [UNIT_FMAD.get(u, f) if f == "-fmad=false" else f for f in FLAGS]
         procs.append(subprocess.Popen([NVCC] + ARCH + fl + ["-c", "-o", obj, os.path.join(CSRC, u)],
                                       stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
     info, err = [], None
+    info_path = os.path.join(PKG, "ptxas_info.txt")
+    old = {}
+    if os.path.exists(info_path):   # keep the ptxas report of units that were not recompiled
+        for chunk in open(info_path).read().split("==== ")[1:]:
+            old[chunk.split("\n", 1)[0]] = "==== " + chunk
     for u, p in zip(UNITS, procs):
+        if p is None:
+            info.append(old.get(u, f"==== {u}\n(up to date)\n"))
+            continue
         out, e = p.communicate()
         info.append(f"==== {u}\n{out}{e}")
         if p.returncode != 0:
             err = f"nvcc failed on {u}:\n" + e[-4000:]
-    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+    with open(info_path, "w") as f:
         f.write("".join(info))
     if err:
         raise RuntimeError(err)

@@ -378,8 +378,11 @@ def generate(name, out_dir):
     _nasa(A, tab, tm, jac_tail)
     A("  const double icv = 1.0 / cv, irho = 1.0 / rho;\n")
     A("  const double fT0 = -su * irho * icv;\n")
+    p1_end = len(L)
+    col_start = []
     # pass 2: species columns
     for j in range(K):
+        col_start.append(len(L))
         A(f"  {{ // column {j} ({sp[j]})\n")
         rows = {}
         terms = []
@@ -435,6 +438,7 @@ def generate(name, out_dir):
         A(f"    J[{K * N + j}*S] = -s * icv - fT0 * sc[{O_CV + j}*S] * icv;\n")
         A("  }\n")
     # temperature column
+    col_start.append(len(L))
     A("  {\n")
     rowsT = {}
     for r in range(NR):
@@ -456,7 +460,9 @@ def generate(name, out_dir):
         else:
             A(f"    J[{i * N + K}*S] = 0.0;\n")
     A(f"    J[{K * N + K}*S] = -scw * irho * icv - s * icv - fT0 * dcv * icv;\n")
-    A("  }\n  return 0;\n  }\n")
+    A("  }\n")
+    col_end = len(L)
+    A("  return 0;\n  }\n")
     # jac_cm: the same body with y at yp[k * SY] (e.g. a warp-blocked SoA state), J column-major and
     # contiguous (J(i, j) at J[j * N + i], the split kernel's per-cell record) and contiguous scratch
     body = "".join(L[jac_start:])
@@ -472,6 +478,54 @@ def generate(name, out_dir):
     body = re.sub(r"sc\[(\d+)\*S\]", lambda m: f"sc[{m.group(1)}]", body)
     assert "*S]" not in body, "unconverted stride in jac_cm"
     A(body)
+    # jac_p1 / jac_col: jac_cm split in two passes with the same operations (so the same J bit for bit).
+    # Pass 1 (one thread per cell): thermo, every reaction's kf, kr, dq/dT, dq/d[M], the energy sums, then
+    # C_k, u_k/W_k and the scalars into the scratch sc.  Pass 2 (one thread per (cell, column j), warp-uniform
+    # j): column j of J from the scratch.  The Jacobian list of one SPLIT iteration is ~10^4 cells, so a
+    # thread per cell leaves most of the GPU idle behind one long serial chain; the column pass has N times
+    # the threads.  Scratch offsets after jac's: C_k at O_C, u_k/W_k at O_U, then icv, irho, fT0, scw, dcv.
+    O_C = NSC
+    O_U = O_C + K
+    O_SC = O_U + K
+    NSC2 = O_SC + 5
+
+    def conv(t):
+        t = re.sub(r"yp\[(\d+)\*S\]", lambda m: f"yp[{m.group(1)}*SY]", t)
+        t = re.sub(r"J\[(\d+)\*S\]", lambda m: f"J[{(int(m.group(1)) % N) * N + int(m.group(1)) // N}]", t)
+        t = re.sub(r"sc\[(\d+)\*S\]", lambda m: f"sc[{m.group(1)}]", t)
+        return t
+    p1 = "".join(L[jac_start:p1_end])
+    p1 = p1.replace("  template <long long SS>  // compile-time element stride (0: runtime Srt)\n",
+                    "  template <long long SY, long long SC>  // element strides of y and of the scratch\n")
+    p1 = p1.replace("__device__ __noinline__ static int jac(const double* __restrict__ yp, double rho, "
+                    "double* __restrict__ J, double* __restrict__ sc, long long Srt) {\n",
+                    "__device__ __forceinline__ static int jac_p1(const double* __restrict__ yp, double rho, "
+                    "double* __restrict__ sc) {\n")
+    p1 = p1.replace("  const long long S = SS ? SS : Srt;\n", "")
+    p1 = conv(p1)
+    for k in range(K):
+        p1 += f"  sc[{O_C + k}] = C{k};\n  sc[{O_U + k}] = uoW{k};\n"
+    p1 += (f"  sc[{O_SC}] = icv;\n  sc[{O_SC + 1}] = irho;\n  sc[{O_SC + 2}] = fT0;\n  sc[{O_SC + 3}] = scw;\n"
+           f"  sc[{O_SC + 4}] = dcv;\n  return 0;\n  }}\n\n")
+    p1 = re.sub(r"sc\[(\d+)\]", lambda m: f"sc[{m.group(1)}*SC]", p1)
+    assert "*S]" not in p1, "unconverted stride in jac_p1"
+    A(p1)
+    A(f"  static constexpr int NSC2 = {NSC2};   // scratch doubles of jac_p1 / jac_col\n")
+    A("  // column j (0..N-1) of the column-major J from jac_p1's scratch (element stride SC)\n")
+    A("  template <long long SC>\n  __device__ __forceinline__ static void jac_col(int j, const double* __restrict__ sc, "
+      "double* __restrict__ J) {\n")
+    A(f"  const double icv = sc[{O_SC}*SC], irho = sc[{O_SC + 1}*SC], fT0 = sc[{O_SC + 2}*SC], "
+      f"scw = sc[{O_SC + 3}*SC], dcv = sc[{O_SC + 4}*SC];\n")
+    A("  (void)irho; (void)scw; (void)dcv; (void)fT0;\n  switch (j) {\n")
+    for c in range(N):
+        seg = "".join(L[col_start[c]:(col_start[c + 1] if c + 1 < N else col_end)])
+        seg = conv(seg)
+        seg = re.sub(r"(?<![A-Za-z0-9_])C(\d+)\b", lambda m: f"sc[{O_C + int(m.group(1))}]", seg)
+        seg = re.sub(r"(?<![A-Za-z0-9_])uoW(\d+)\b", lambda m: f"sc[{O_U + int(m.group(1))}]", seg)
+        seg = re.sub(r"sc\[(\d+)\]", lambda m: f"sc[{m.group(1)}*SC]", seg)
+        assert "*S]" not in seg, "unconverted stride in jac_col"
+        A(f"  case {c}:\n{seg}  break;\n")
+    A("  }\n  }\n")
     A("};\n}  // namespace bdfb\n")
     os.makedirs(out_dir, exist_ok=True)
     p = os.path.join(out_dir, f"tpc_{name}.cuh")

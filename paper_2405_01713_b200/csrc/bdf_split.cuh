@@ -76,6 +76,16 @@ namespace bdfb {
 // split-local phases: waiting for the setup kernels; finished, to be stored by K_init; a Jv request of GMRES
 constexpr int PH_SETUP = 6, PH_STORE = 7, PH_KRY = 8;
 
+// 1: K_rhs also runs the Newton residual and the LU solve of a PH_NRES request whose matrix is current (dense
+// direct solver, n <= 32), so that the 4 KB LU-record stream of the solve leaves the memory-bound, divergent
+// K_ctl; K_ctl then finds the correction in the del row (rv = RV_SOLVED) and runs only the Newton update and
+// test (same operations, same order).  Measured on C4: K_ctl 3274 -> 3155 ms but K_rhs 933 -> 2560 ms (the
+// stream stalls the RHS warps instead of overlapping them): off, kept as an option.
+#ifndef BDFB_SPLIT_RHS_SOLVE
+#define BDFB_SPLIT_RHS_SOLVE 0
+#endif
+constexpr int RV_SOLVED = -1;   // b.rv code: K_rhs returned f = R + F consumed and delta = M^-1 (-G) in del
+
 // linear solver inside the Newton iteration (bdfb_set_linear_solver; Table 1)
 enum : int { LS_DENSE = 0, LS_DIAG = 1, LS_GMRES = 2 };
 constexpr int KMAXL = 5;            // Krylov dimension of the VEC record (CVODE's default maxl; reading R29)
@@ -87,6 +97,8 @@ struct SplitBufs {
   double* ts;                  // S * TS_STRIDE
   double* J;                   // S * JREC
   double* LU;                  // S * LUREC
+  double* jscr;                // two-pass Jacobian scratch, Jacobian-list entry e, element r at
+                               // jscr[((e/32) NSC2 + r) 32 + e%32] (S * NSC2; null when unused)
   int* rv;                     // S: RHS status of the last request
   int* slist;                  // setup list (slots)
   int* jlist;                  // Jacobian list (slots)
@@ -105,6 +117,14 @@ struct SplitBufs {
 #define BDFB_SPLIT_LU_SOA 0   // measured on C4: K_ctl -4% but K_lu 1.05 -> 2.22 s (scattered 8-byte writes): off
 #endif
 constexpr int LU_STRIDE = BDFB_SPLIT_LU_SOA ? 32 : 1;
+
+// VEC layout: 0 = warp-blocked SoA (element e of slot s at vec[((s/32) D + e) 32 + s%32]: a warp of consecutive
+// slots reads one element as one 256-byte line); 1 = slot-major (slot s's D doubles contiguous: a lane's rows are
+// its own lines, so lanes that sit out a divergent stage fetch no sectors)
+#ifndef BDFB_SPLIT_VEC_AOS
+#define BDFB_SPLIT_VEC_AOS 0
+#endif
+constexpr int VEC_S = BDFB_SPLIT_VEC_AOS ? 1 : 32;
 
 // Substitutions of LU_SOLVE (listing; reading R16) on a column-major LU
 // record (factors in pivoted row order | 1/U_kk | perm), b already permuted:
@@ -173,7 +193,7 @@ __device__ __forceinline__ void lurec_substitute(const double* __restrict__ lu, 
 template <class Mech, class GM, int LS = LS_DENSE>
 struct Split {
   static constexpr int N = Mech::N;
-  using I = TpcIntegrator<Mech, GM, 32, false>;
+  using I = TpcIntegrator<Mech, GM, VEC_S, false>;
   using W = typename I::W;
   static constexpr int D0 = W::DOUBLES;
   // extra VEC elements of the matrix-free linear solvers.  CVDiag: f at the setup point, gamma of the
@@ -201,7 +221,8 @@ struct Split {
   static_assert(sizeof(TS) <= sizeof(double) * TS_STRIDE, "TS record");
 
   __device__ static W ws(const SplitBufs& b, long long slot) {
-    return W{b.vec + ((slot >> 5) * D) * 32 + (slot & 31), nullptr};
+    if constexpr (VEC_S == 1) return W{b.vec + slot * D, nullptr};
+    else return W{b.vec + ((slot >> 5) * D) * 32 + (slot & 31), nullptr};
   }
   __device__ static TS* ts(const SplitBufs& b, long long slot) {
     return reinterpret_cast<TS*>(b.ts + slot * TS_STRIDE);
@@ -222,6 +243,15 @@ struct Split {
       for (int i = 0; i < N; ++i) b[i] = sc * b[i];
     }
     return newton_update(s, w, b);
+  }
+
+  // the Newton residual and the substitutions already ran in K_rhs (RV_SOLVED): delta is in the del row
+  __device__ static int solved(TS& s, const W& w) {
+    s.nni++;
+    double x[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = w.del(i);
+    return newton_update(s, w, x);
   }
 
   // ycor += delta, ||delta|| and the Newton test of Eq. 4 (TpcIntegrator::solve's tail), for every linear solver
@@ -700,10 +730,14 @@ __global__ void __launch_bounds__(BDFB_SPLIT_CTL_BLOCK, (Mech::N > 32 ? 2 : BDFB
           (LS == LS_GMRES && ph == PH_KRY)) {
         rv = b.rv[slot];
         if (ph != PH_KRY) s.nfe++;   // the Jv quotients' RHS calls are not counted in nfe (CVODE's nfeDQ)
+        if (LS != LS_DENSE || rv != RV_SOLVED) {
 #pragma unroll
-        for (int i = 0; i < N; ++i) fr[i] = w.fr(i);
+          for (int i = 0; i < N; ++i) fr[i] = w.fr(i);
+        }
       }
-      if (LS == LS_DIAG && ph == PH_DIAG) {
+      if (LS == LS_DENSE && rv == RV_SOLVED) {   // consume + SOLVE ran in K_rhs
+        act = SP::solved(s, w);
+      } else if (LS == LS_DIAG && ph == PH_DIAG) {
         act = SP::diag_consume(s, w, rv, fr);
       } else if (LS == LS_GMRES && ph == PH_KRY) {
         act = SP::kry_consume(s, w, rv, fr, b.maxl);
@@ -898,7 +932,45 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_tpc_kernel(SplitBu
     const long long slot = b.jlist[e];
     const typename SP::W w = SP::ws(b, slot);
     TS* t = SP::ts(b, slot);
-    t->coop = Mech::template jac_cm<32>(&w.yq(0), t->aux, b.J + slot * SP::JREC, SP::lurec(b, slot));
+    t->coop = Mech::template jac_cm<VEC_S>(&w.yq(0), t->aux, b.J + slot * SP::JREC, SP::lurec(b, slot));
+  }
+}
+
+// K_jac in two passes (default for n <= 32 when the scratch fits the LU record): the generated jac_cm split
+// into pass 1, one thread per Jacobian-list entry (thermo, every reaction's kf, kr, dq/dT, dq/d[M], the energy
+// sums; gen/tpc_<mech>.cuh jac_p1) into a warp-blocked SoA scratch indexed by the list position (pass 1 stores
+// and pass 2 loads are one 256-byte line per warp), and pass 2, one thread per (entry, column j) with j
+// warp-uniform and column-major across warps (each warp of a block runs the same column's code), writing
+// column j of the J record (jac_col).  Same operations as jac_cm.  The
+// Jacobian list of one iteration is ~10^4 cells: one thread per cell leaves most of the GPU idle behind one
+// serial chain (the group/lanes K_jac: ~53K warp instructions per Jacobian, ncu profiles/r2).
+template <class Mech, class GM, int LS = LS_DENSE>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_p1_kernel(SplitBufs b, int it) {
+  using SP = Split<Mech, GM, LS>;
+  const long long cnt = b.cnt[3 * (it & 1) + 1];
+  for (long long e = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; e < cnt;
+       e += (long long)gridDim.x * BDFB_SPLIT_BLOCK) {
+    const long long slot = b.jlist[e];
+    const typename SP::W w = SP::ws(b, slot);
+    TS* t = SP::ts(b, slot);
+    t->coop = Mech::template jac_p1<VEC_S, 32>(&w.yq(0), t->aux, b.jscr + ((e >> 5) * Mech::NSC2) * 32 + (e & 31));
+  }
+}
+template <class Mech, class GM, int LS = LS_DENSE>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_p2_kernel(SplitBufs b, int it) {
+  using SP = Split<Mech, GM, LS>;
+  constexpr int N = Mech::N;
+  const long long cnt = b.cnt[3 * (it & 1) + 1];
+  const long long neb = (cnt + 31) / 32;                       // 32-entry blocks
+  const int lane = threadIdx.x & 31;
+  const long long nw = neb * N, wstride = ((long long)gridDim.x * BDFB_SPLIT_BLOCK) >> 5;
+  for (long long gw = ((long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x) >> 5; gw < nw; gw += wstride) {
+    const int j = (int)(gw / neb);                             // column: warp-uniform, equal for neighbour warps
+    const long long e = (gw - j * neb) * 32 + lane;
+    if (e >= cnt) continue;
+    const long long slot = b.jlist[e];
+    if (SP::ts(b, slot)->coop) continue;                       // pass 1 failed (T <= 0): recoverable
+    Mech::template jac_col<32>(j, b.jscr + ((e >> 5) * Mech::NSC2) * 32 + (e & 31), b.J + slot * SP::JREC);
   }
 }
 
@@ -962,46 +1034,50 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, 3) split_dqjac_kernel(SplitB
 // (reading R16), so pivots and factors are bit-identical to the oracle.
 // Versus one cell per warp (coop_factor) every shuffle of the pivot row
 // serves 4 cells and every lane has ~3 rows of FMAs: ~4x fewer instructions
-// per factorisation.  Returns 0, or k+1 for an exact zero pivot (uniform).
+// per factorisation.
+// The whole warp runs every column together (full-mask shuffles, no early exit): a shuffle with a per-group
+// mask compiled to a convergence barrier around every SHFL (WARPSYNC + BSSY/BSYNC + ENDCOLLECTIVE: 3.1K of the
+// kernel's 19K SASS instructions, ncu IPC 1.4, 2.4K warp instructions per LU).  A group whose pivot is an exact
+// zero keeps computing on garbage that is never stored; info = k + 1 of its first zero pivot, else 0.
 constexpr int OCT = 8;
 // column k of oct_factor (k a compile-time constant so that a[][] stays in registers)
 template <int N, int K>
-__device__ __forceinline__ bool oct_column(unsigned gmask, int gl, double (&a)[(N + OCT - 1) / OCT][N],
-                                           int (&pos)[(N + OCT - 1) / OCT], double (&dinv)[(N + OCT - 1) / OCT]) {
+__device__ __forceinline__ void oct_column(int gl, double (&a)[(N + OCT - 1) / OCT][N], int (&pos)[(N + OCT - 1) / OCT],
+                                           double (&dinv)[(N + OCT - 1) / OCT], int& info) {
   constexpr int R = (N + OCT - 1) / OCT;
-  // local candidate: max |a[s][K]| over owned rows with pos >= K, ties -> smaller pos
+  // local candidate: max |a[s][K]| over owned rows with pos >= K, ties -> smaller pos; (pos, row) packed in one
+  // int (pos in the high half: positions are distinct, so packed order = position order)
   double bv = -1.0;
-  int bp = 0x7fffffff, br = -1;
+  int bpr = 0x7fffffff;
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     const int r = gl + OCT * s;
     if (r < N && pos[s] >= K) {
       const double v = fabs(a[s][K]);
-      if (v > bv || (v == bv && pos[s] < bp)) {
+      const int pr = (pos[s] << 16) | r;
+      if (v > bv || (v == bv && pr < bpr)) {
         bv = v;
-        bp = pos[s];
-        br = r;
+        bpr = pr;
       }
     }
   }
 #pragma unroll
   for (int off = OCT / 2; off >= 1; off >>= 1) {
-    const double ov = __shfl_xor_sync(gmask, bv, off, OCT);
-    const int op = __shfl_xor_sync(gmask, bp, off, OCT);
-    const int orr = __shfl_xor_sync(gmask, br, off, OCT);
-    if (ov > bv || (ov == bv && op < bp)) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, off, OCT);
+    const int opr = __shfl_xor_sync(0xffffffffu, bpr, off, OCT);
+    if (ov > bv || (ov == bv && opr < bpr)) {
       bv = ov;
-      bp = op;
-      br = orr;
+      bpr = opr;
     }
   }
-  if (!(bv > 0.0)) return false;               // exact zero pivot (uniform in the group)
-  const int pl = br % OCT, ps = br / OCT;      // owner lane and slot of the pivot row
+  if (!(bv > 0.0) && info == 0) info = K + 1;   // exact zero pivot (uniform in the group)
+  const int bp = bpr >> 16, br = bpr & 0xffff;
+  const int pl = br & (OCT - 1), ps = br / OCT;   // owner lane and slot of the pivot row
   double pk = 0.0;
 #pragma unroll
   for (int s = 0; s < R; ++s)
     if (s == ps) pk = a[s][K];
-  const double pv = __shfl_sync(gmask, pk, pl, OCT);
+  const double pv = __shfl_sync(0xffffffffu, pk, pl, OCT);
   const double rinv = 1.0 / pv;
 #pragma unroll
   for (int s = 0; s < R; ++s) {
@@ -1013,11 +1089,16 @@ __device__ __forceinline__ bool oct_column(unsigned gmask, int gl, double (&a)[(
       pos[s] = bp;
     }
   }
+  // multipliers; rows that take no update this column (already pivoted, or padding) get m = 0, so the update
+  // below is one unpredicated DFMA per row: fma(-0, pj, a) = a (for finite pj; a -0.0 entry may become +0.0,
+  // equal as a number -- reading R16 note in DESIGN.md) instead of a DFMA and two selects
   double m[R];
 #pragma unroll
   for (int s = 0; s < R; ++s) {
-    m[s] = a[s][K] * rinv;
-    if ((gl + OCT * s < N) && pos[s] > K) a[s][K] = m[s];
+    const bool upd = (gl + OCT * s < N) && pos[s] > K;
+    const double mk = a[s][K] * rinv;
+    m[s] = upd ? mk : 0.0;
+    if (upd) a[s][K] = mk;
   }
 #pragma unroll
   for (int j = K + 1; j < N; ++j) {
@@ -1025,50 +1106,54 @@ __device__ __forceinline__ bool oct_column(unsigned gmask, int gl, double (&a)[(
 #pragma unroll
     for (int s = 0; s < R; ++s)
       if (s == ps) pj = a[s][j];
-    pj = __shfl_sync(gmask, pj, pl, OCT);
+    pj = __shfl_sync(0xffffffffu, pj, pl, OCT);
 #pragma unroll
     for (int s = 0; s < R; ++s)
-      if ((gl + OCT * s < N) && pos[s] > K) a[s][j] = fma(-m[s], pj, a[s][j]);
+      if (gl + OCT * s < N) a[s][j] = fma(-m[s], pj, a[s][j]);
   }
-  return true;
 }
 
 template <int N, int... Ks>
-__device__ __forceinline__ int oct_columns(unsigned gmask, int gl, double (&a)[(N + OCT - 1) / OCT][N],
-                                           int (&pos)[(N + OCT - 1) / OCT], double (&dinv)[(N + OCT - 1) / OCT],
-                                           std::integer_sequence<int, Ks...>) {
-  int info = 0;
-  // left to right; stops at the first zero pivot (info = k + 1)
-  (void)((oct_column<N, Ks>(gmask, gl, a, pos, dinv) ? true : (info = Ks + 1, false)) && ...);
-  return info;
+__device__ __forceinline__ void oct_columns(int gl, double (&a)[(N + OCT - 1) / OCT][N], int (&pos)[(N + OCT - 1) / OCT],
+                                            double (&dinv)[(N + OCT - 1) / OCT], int& info,
+                                            std::integer_sequence<int, Ks...>) {
+  (oct_column<N, Ks>(gl, a, pos, dinv, info), ...);   // left to right
 }
 
+// called by all 32 lanes of the warp together (4 groups); returns 0 or k + 1 of the group's first zero pivot
 template <int N>
-__device__ __forceinline__ int oct_factor(unsigned gmask, int gl, double (&a)[(N + OCT - 1) / OCT][N],
-                                          int (&pos)[(N + OCT - 1) / OCT], double (&dinv)[(N + OCT - 1) / OCT]) {
+__device__ __forceinline__ int oct_factor(int gl, double (&a)[(N + OCT - 1) / OCT][N], int (&pos)[(N + OCT - 1) / OCT],
+                                          double (&dinv)[(N + OCT - 1) / OCT]) {
   constexpr int R = (N + OCT - 1) / OCT;
+  static_assert(N < (1 << 15), "packed (pos, row)");
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     pos[s] = gl + OCT * s;
     dinv[s] = 0.0;
   }
-  return oct_columns<N>(gmask, gl, a, pos, dinv, std::make_integer_sequence<int, N>{});
+  int info = 0;
+  oct_columns<N>(gl, a, pos, dinv, info, std::make_integer_sequence<int, N>{});
+  return info;
 }
 
-// K_lu: one setup-list entry per group of 8 lanes (grid-stride); M = I - gamma J
-// from the cell's column-major J, oct_factor, factors stored column-major in
-// pivoted row order + 1/U_kk + perm, as the Newton solve of K_ctl reads them.
+// K_lu: one setup-list entry per group of 8 lanes (grid-stride, warp-uniform trips: a group without an entry,
+// or whose Jacobian failed, factors the identity and stores nothing); M = I - gamma J from the cell's
+// column-major J, oct_factor, factors stored column-major in pivoted row order + 1/U_kk + perm, as the Newton
+// solve reads them.
 template <class Mech, class GM, int LS = LS_DENSE>
-__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b, int it) {
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, 3) split_lu_kernel(SplitBufs b, int it) {   // 12 warps/SM
   using SP = Split<Mech, GM, LS>;
   constexpr int N = Mech::N, R = (N + OCT - 1) / OCT;
   const int lane = threadIdx.x & 31, gl = lane & (OCT - 1);
-  const unsigned gmask = 0xffu << (lane & ~(OCT - 1));
   const long long cnt = b.cnt[3 * (it & 1)], groups = (long long)gridDim.x * (BDFB_SPLIT_BLOCK / OCT);
-  for (long long e = ((long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x) / OCT; e < cnt; e += groups) {
-    const long long slot = b.slist[e];
+  // CTA-uniform trip condition and branch-free entry loads, so that the compiler can prove the warp converged
+  // at every shuffle (no BRA.DIV guard splitting the column code into basic blocks)
+  for (long long e0 = (long long)blockIdx.x * (BDFB_SPLIT_BLOCK / OCT); e0 < cnt; e0 += groups) {
+    const long long e = e0 + threadIdx.x / OCT;
+    const bool have = e < cnt;
+    const long long slot = b.slist[have ? e : cnt - 1];
     TS* t = SP::ts(b, slot);
-    if (t->coop) continue;                       // the Jacobian failed: the resumed trip handles it (uniform)
+    const bool work = have && t->coop == 0;    // the Jacobian failed: the resumed trip handles it
     const double gm = t->gamma;
     const double* J = b.J + slot * SP::JREC;
     double* lu = SP::lurec(b, slot);
@@ -1077,12 +1162,15 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b,
     for (int s = 0; s < R; ++s) {
       const int r = gl + OCT * s;
 #pragma unroll
-      for (int j = 0; j < N; ++j) a[s][j] = (r < N) ? (r == j ? 1.0 : 0.0) - gm * J[j * N + r] : 0.0;
+      for (int j = 0; j < N; ++j) {
+        const double v = (r == j ? 1.0 : 0.0) - gm * J[j * N + (r < N ? r : 0)];
+        a[s][j] = (r < N) ? (work ? v : (r == j ? 1.0 : 0.0)) : 0.0;
+      }
     }
     int pos[R];
     double dinv[R];
-    const int info = oct_factor<N>(gmask, gl, a, pos, dinv);
-    if (!info) {
+    const int info = oct_factor<N>(gl, a, pos, dinv);
+    if (work && !info) {
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int r = gl + OCT * s;
@@ -1095,8 +1183,8 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_lu_kernel(SplitBufs b,
         }
       }
     }
-    __syncwarp(gmask);
-    if (gl == 0) t->coop = info;
+    __syncwarp();
+    if (work && gl == 0) t->coop = info;
   }
 }
 
@@ -1141,6 +1229,33 @@ __global__ void __launch_bounds__(RhsVar<VAR>::BLOCK, RhsVar<VAR>::MINB) split_r
       rv = Mech::template rhs_sm<V::BLOCK>(yv, t->aux, fv, rsm + threadIdx.x);
     } else {
       rv = Mech::rhs(yv, t->aux, fv);
+    }
+    if constexpr (LS == LS_DENSE && BDFB_SPLIT_RHS_SOLVE && N <= 32) {
+      if (rv == 0 && ph == PH_NRES && !t->setup) {
+        // consume (PH_NRES: del = -gamma f + (rl1 zn[1] + ycor)) and SOLVE (LU_SOLVE on the slot's record, the
+        // stale-gamma scaling) of TpcIntegrator / Split::solve, operation for operation
+        const double rl1 = t->rl1, gm = t->gamma, gamrat = t->gamrat;
+        const double* lu = SP::lurec(b, slot);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double fr = fv[i] + w.fext(i);
+          const double tt = rl1 * w.zn(1, i) + w.acor(i);
+          w.del(i) = -gm * fr + tt;
+        }
+        double x[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[i] = -w.del(SP::lu_perm(lu, i));
+        lurec_substitute<N, LU_STRIDE>(lu, x);
+        if (gamrat != 1.0) {
+          const double sc = 2.0 / (1.0 + gamrat);
+#pragma unroll
+          for (int i = 0; i < N; ++i) x[i] = sc * x[i];
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) w.del(i) = x[i];
+        b.rv[slot] = RV_SOLVED;
+        continue;
+      }
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) w.fr(k) = fv[k] + w.fext(k);

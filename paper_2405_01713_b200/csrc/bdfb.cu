@@ -124,6 +124,7 @@ static void free_split(bdfb_batch* b) {
   cudaFree(b->sb.ts);
   cudaFree(b->sb.J);
   cudaFree(b->sb.LU);
+  cudaFree(b->sb.jscr);
   cudaFree(b->sb.rv);
   cudaFree(b->sb.slist);
   cudaFree(b->sb.jlist);
@@ -146,7 +147,8 @@ static int prepare_split(bdfb_batch* b) {
   if (const char* env = getenv("BDFB_SPLIT_SLOTS")) cap = atoll(env) > 0 ? atoll(env) : cap;
   long long S = b->ncells < cap ? b->ncells : cap;
   S = (S + 31) / 32 * 32;
-  if (S != b->sb.slots || gm.vec_doubles != b->sgeom.vec_doubles || gm.lurec != b->sgeom.lurec) {
+  if (S != b->sb.slots || gm.vec_doubles != b->sgeom.vec_doubles || gm.lurec != b->sgeom.lurec ||
+      gm.jscr != b->sgeom.jscr) {
     free_split(b);
     bool ok = true;
     auto A = [&](void** p, size_t bytes) { if (ok && bytes && cudaMalloc(p, bytes) != cudaSuccess) ok = false; };
@@ -154,6 +156,7 @@ static int prepare_split(bdfb_batch* b) {
     A((void**)&b->sb.ts, sizeof(double) * (size_t)gm.ts_doubles * S);
     A((void**)&b->sb.J, sizeof(double) * (size_t)gm.jrec * S);
     A((void**)&b->sb.LU, sizeof(double) * (size_t)gm.lurec * S);
+    A((void**)&b->sb.jscr, sizeof(double) * (size_t)gm.jscr * S);
     A((void**)&b->sb.rv, sizeof(int) * (size_t)S);
     A((void**)&b->sb.slist, sizeof(int) * (size_t)S);
     A((void**)&b->sb.jlist, sizeof(int) * (size_t)S);

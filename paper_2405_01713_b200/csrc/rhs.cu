@@ -19,15 +19,20 @@
 
 namespace bdfb {
 
-// K_rhs organisation (RhsVar in bdf_split.cuh): BDFB_SPLIT_RHS_VAR = 0..4 overrides; default 3 (e^{-g/RT} in
-// shared memory: C4 K_rhs 1013 -> 930 ms, no spills) when its 2K doubles per thread fit 64 KB per block, else 0
+// K_rhs organisation (RhsVar in bdf_split.cuh): 3 (e^{-g/RT} in shared memory: C4 K_rhs 1013 -> 930 ms, no
+// spills) when its 2K doubles per thread fit 64 KB per block, else 0 (free-running 128-thread blocks);
+// BDFB_SPLIT_RHS_VAR = 0 forces 0.  VARs 1, 2 and 4 (block-synchronous trips, 16 warps/SM) measured equal or
+// slower in round 2 (profiles/r2/history.md) and are no longer instantiated (they tripled the unit's compile time).
+template <class Mech>
+__host__ __device__ constexpr bool rhs_sm_fits() {
+  return 2 * Mech::K * RhsVar<3>::BLOCK * 8 <= 64 * 1024;
+}
 template <class Mech>
 static int rhs_var() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BDFB_SPLIT_RHS_VAR");
-    v = e ? atoi(e) : (2 * Mech::K * RhsVar<3>::BLOCK * 8 <= 64 * 1024 ? 3 : 0);
-    if (v < 0 || v > 4) v = 0;
+    v = (rhs_sm_fits<Mech>() && !(e && atoi(e) == 0)) ? 3 : 0;
   }
   return v;
 }
@@ -39,17 +44,13 @@ constexpr size_t rhs_sm_bytes() {
 
 template <class Mech, class GM, int LS>
 cudaError_t split_rhs_run(unsigned grid, cudaStream_t st, const SplitBufs& b, int it) {
-  switch (rhs_var<Mech>()) {
-    case 1: split_rhs_kernel<Mech, GM, LS, 1><<<grid, RhsVar<1>::BLOCK, 0, st>>>(b, it); break;
-    case 2: split_rhs_kernel<Mech, GM, LS, 2><<<grid, RhsVar<2>::BLOCK, 0, st>>>(b, it); break;
-    case 3:
+  if constexpr (rhs_sm_fits<Mech>()) {
+    if (rhs_var<Mech>() == 3) {
       split_rhs_kernel<Mech, GM, LS, 3><<<grid, RhsVar<3>::BLOCK, rhs_sm_bytes<Mech>(), st>>>(b, it);
-      break;
-    case 4:
-      split_rhs_kernel<Mech, GM, LS, 4><<<grid, RhsVar<4>::BLOCK, rhs_sm_bytes<Mech>(), st>>>(b, it);
-      break;
-    default: split_rhs_kernel<Mech, GM, LS, 0><<<grid, RhsVar<0>::BLOCK, 0, st>>>(b, it);
+      return cudaSuccess;
+    }
   }
+  split_rhs_kernel<Mech, GM, LS, 0><<<grid, RhsVar<0>::BLOCK, 0, st>>>(b, it);
   return cudaSuccess;
 }
 
@@ -57,30 +58,18 @@ cudaError_t split_rhs_run(unsigned grid, cudaStream_t st, const SplitBufs& b, in
 // that the caller's grid (nsm x blocks) covers the same threads
 template <class Mech, class GM, int LS>
 cudaError_t split_rhs_occupancy(int* blocks_per_sm) {
-  cudaError_t e;
-  switch (rhs_var<Mech>()) {
-    case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 1>,
-                                                            RhsVar<1>::BLOCK, 0); break;
-    case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 2>,
-                                                            RhsVar<2>::BLOCK, 0); break;
-    case 3:
-      e = cudaFuncSetAttribute(split_rhs_kernel<Mech, GM, LS, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)rhs_sm_bytes<Mech>());
+  if constexpr (rhs_sm_fits<Mech>()) {
+    if (rhs_var<Mech>() == 3) {
+      cudaError_t e = cudaFuncSetAttribute(split_rhs_kernel<Mech, GM, LS, 3>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rhs_sm_bytes<Mech>());
       if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 3>,
                                                           RhsVar<3>::BLOCK, rhs_sm_bytes<Mech>());
-      break;
-    case 4:
-      e = cudaFuncSetAttribute(split_rhs_kernel<Mech, GM, LS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)rhs_sm_bytes<Mech>());
-      if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 4>,
-                                                          RhsVar<4>::BLOCK, rhs_sm_bytes<Mech>());
-      break;
-    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 0>,
-                                                             RhsVar<0>::BLOCK, 0);
+      return e;
+    }
   }
-  return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, split_rhs_kernel<Mech, GM, LS, 0>,
+                                                       RhsVar<0>::BLOCK, 0);
 }
 
 #define BDFB_RHS_INST(M, G, LS)                                                                       \
@@ -114,9 +103,13 @@ __global__ void __launch_bounds__(128) eval_rhs_kernel(long long N, const double
 #pragma unroll
   for (int i = 0; i < n; ++i) yv[i] = y[(long long)i * N + c];
   int rv;
-  if (use_sm) {   // the device function K_rhs runs (the host's RhsVar choice)
-    extern __shared__ double rsm[];
-    rv = Mech::template rhs_sm<128>(yv, aux[c], fv, rsm + threadIdx.x);
+  if constexpr (rhs_sm_fits<Mech>()) {
+    if (use_sm) {   // the device function K_rhs runs (the host's RhsVar choice)
+      extern __shared__ double rsm[];
+      rv = Mech::template rhs_sm<128>(yv, aux[c], fv, rsm + threadIdx.x);
+    } else {
+      rv = Mech::rhs(yv, aux[c], fv);
+    }
   } else {
     rv = Mech::rhs(yv, aux[c], fv);
   }

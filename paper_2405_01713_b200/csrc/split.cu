@@ -30,20 +30,21 @@ __global__ void __launch_bounds__(128) split_lu_diag_kernel(long long N, double*
   constexpr int LUREC = S == 1 ? (NN * NN + NN + (NN + 1) / 2 + 3) / 4 * 4 : NN * NN + 2 * NN;
   constexpr int LU_INVD = NN * NN, LU_PERM = NN * NN + NN;
   const int lane = threadIdx.x & 31, gl = lane & (OCT - 1);
-  const unsigned gmask = 0xffu << (lane & ~(OCT - 1));
   const long long c = ((long long)blockIdx.x * 128 + threadIdx.x) / OCT;
-  if (c >= N) return;                         // whole groups exit together (N is per group)
+  const bool have = c < N;                    // the whole warp factors (oct_factor is warp-collective)
+  if (__all_sync(0xffffffffu, !have)) return;
   double* lu = S == 1 ? rec + c * LUREC : rec + ((c >> 5) * LUREC) * 32 + (c & 31);   // K_lu's record layout
   double a[R][NN];
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     const int r = gl + OCT * s;
 #pragma unroll
-    for (int j = 0; j < NN; ++j) a[s][j] = (r < NN) ? M[((long long)r * NN + j) * N + c] : 0.0;
+    for (int j = 0; j < NN; ++j) a[s][j] = (r < NN) ? (have ? M[((long long)r * NN + j) * N + c] : (r == j ? 1.0 : 0.0)) : 0.0;
   }
   int pos[R];
   double dinv[R];
-  const int inf = oct_factor<NN>(gmask, gl, a, pos, dinv);
+  const int inf = oct_factor<NN>(gl, a, pos, dinv);
+  if (!have) return;
   if (!inf) {
 #pragma unroll
     for (int s = 0; s < R; ++s) {
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(128) split_lu_diag_kernel(long long N, double*
       }
     }
   }
-  __syncwarp(gmask);
+  __syncwarp(__activemask());
   if (gl != 0) return;
   info[c] = inf;
   if (inf) return;

@@ -15,6 +15,7 @@ struct SplitGeom {
   int rhs_grid;                            // resident blocks of K_rhs on the device
   int setup_grid;                          // blocks of the (grid-stride) Jacobian / LU kernels
   int vec_doubles, ts_doubles, jrec, lurec;   // doubles per slot of the VEC, TS, J and LU records
+  int jscr;                                    // doubles per slot of the two-pass Jacobian scratch (0: none)
 };
 
 // ls: LS_DENSE | LS_DIAG | LS_GMRES (bdf_split.cuh); the matrix-free solvers are built in split_mf.cu

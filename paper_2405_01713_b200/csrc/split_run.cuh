@@ -21,6 +21,8 @@ struct SplitK {
     return BDFB_SPLIT_TS_SMEM ? sizeof(double) * (size_t)TS_STRIDE * BDFB_SPLIT_CTL_BLOCK : 0;
   }
   static constexpr bool BIG = Mech::N > 32;   // split_big.cuh setup kernels (lanes Jacobian, register-row LU)
+  // two-pass generated Jacobian (split_jac_p1/p2_kernel), n <= 32
+  static constexpr bool JAC2 = !BIG && LS == LS_DENSE;
   static constexpr size_t jac_smem() {
     if constexpr (BIG) {
       return sizeof(double) * (size_t)JacLanesSmem<Mech>::PER_WARP * JL_WARPS;
@@ -56,6 +58,8 @@ struct SplitK {
     gm->ts_doubles = TS_STRIDE;
     gm->jrec = LS == LS_DENSE ? SP::JREC : 0;   // no J / LU records for the matrix-free solvers
     gm->lurec = LS == LS_DENSE ? SP::LUREC : 0;
+    if constexpr (JAC2) gm->jscr = Mech::NSC2;
+    else gm->jscr = 0;
     return cudaSuccess;
   }
 
@@ -75,7 +79,17 @@ struct SplitK {
     const unsigned ginit = gs < (unsigned)gm.setup_grid ? gs : (unsigned)gm.setup_grid;   // grid-stride over the list
     unsigned gdq = (unsigned)gm.rhs_grid;   // K_dqjac: grid-stride over (entry, column)
     unsigned glu = (unsigned)((S * OCT + blk - 1) / blk);
-    if (glu > (unsigned)gm.setup_grid) glu = (unsigned)gm.setup_grid;
+    if constexpr (!BIG) {   // K_lu: a persistent grid of exactly the resident blocks (no partial last wave)
+      static int lu_res = -1;
+      if (lu_res < 0) {
+        int per = 0, nsm = gm.setup_grid / 8;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, split_lu_kernel<Mech, GM, LS>, blk, 0) != cudaSuccess ||
+            per < 1)
+          per = 2;
+        lu_res = per * nsm;
+      }
+      if (glu > (unsigned)lu_res) glu = (unsigned)lu_res;
+    }
     unsigned grhs = (unsigned)gm.rhs_grid;
     if (grhs > gs) grhs = gs;
     if (const char* g = getenv("BDFB_SPLIT_RHS_FULLGRID"))   // experiments: one thread per slot
@@ -88,6 +102,8 @@ struct SplitK {
     split_init_kernel<Mech, GM, LS><<<gs, blk, 0, st>>>(b);
     bool jac_tpc = false;   // BDFB_SPLIT_JAC_TPC=1: thread-per-entry generated Jacobian (measurement)
     if (const char* jt = getenv("BDFB_SPLIT_JAC_TPC")) jac_tpc = atoi(jt) == 1;
+    bool jac2 = true;       // BDFB_SPLIT_JAC2=0: the group (lanes) Jacobian instead of the two-pass generated one
+    if (const char* j2 = getenv("BDFB_SPLIT_JAC2")) jac2 = atoi(j2) != 0;
     int n = 1;
     cudaError_t e;
     for (int i = 0; i < SPLIT_PHASES; ++i) phase_ms[i] = 0.0;
@@ -125,7 +141,13 @@ struct SplitK {
             split_dqjac_kernel<Mech, GM, LS><<<gdq, blk, 0, ss>>>(b, it);
           else if (jac_tpc)
             split_jac_tpc_kernel<Mech, GM, LS><<<(unsigned)gm.rhs_grid, blk, 0, ss>>>(b, it);
-          else
+          else if (JAC2 && jac2 && b.jscr) {
+            if constexpr (JAC2) {
+              split_jac_p1_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
+              split_jac_p2_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
+              ++n;
+            }
+          } else
             split_jac_kernel<Mech, GM, LS><<<gjac, blk, jac_smem(), ss>>>(b, it);
         }
         if (events) cudaEventRecord(ev[2], ss);
