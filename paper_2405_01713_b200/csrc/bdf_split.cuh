@@ -954,8 +954,51 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_p1_kernel(SplitBuf
     const typename SP::W w = SP::ws(b, slot);
     TS* t = SP::ts(b, slot);
     t->coop = Mech::template jac_p1<VEC_S, 32>(&w.yq(0), t->aux, b.jscr + ((e >> 5) * Mech::NSC2) * 32 + (e & 31));
+    static_assert(Mech::NSC2 <= Mech::NSC3, "scratch");
   }
 }
+// K_jac pass 1 parted (default): thread per (entry, part P) with P warp-uniform and equal for neighbour warps
+// (jac_part: the reactions dealt round-robin to Mech::NPART parts), then jac_sum, one thread per entry (partial
+// production rates in part order, the energy sums and scalars): NPART x the threads of split_jac_p1_kernel
+// over NPART x shorter chains (ncu: p1 ran ~2 warps per SM, IPC 0.3, instruction-cache bound)
+template <class Mech, class GM, int LS = LS_DENSE>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_part_kernel(SplitBufs b, int it) {
+  using SP = Split<Mech, GM, LS>;
+  const long long cnt = b.cnt[3 * (it & 1) + 1];
+  const long long neb = (cnt + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const long long nw = neb * Mech::NPART, wstride = ((long long)gridDim.x * BDFB_SPLIT_BLOCK) >> 5;
+  for (long long gw = ((long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x) >> 5; gw < nw; gw += wstride) {
+    const int P = (int)(gw / neb);
+    const long long e = (gw - P * neb) * 32 + lane;
+    if (e >= cnt) continue;
+    const long long slot = b.jlist[e];
+    const typename SP::W w = SP::ws(b, slot);
+    TS* t = SP::ts(b, slot);
+    const int rv = Mech::template jac_part<VEC_S, 32>(P, &w.yq(0), t->aux,
+                                                       b.jscr + ((e >> 5) * Mech::NSC3) * 32 + (e & 31));
+    if (P == 0) t->coop = rv;
+  }
+}
+template <class Mech, class GM, int LS = LS_DENSE>
+__global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_sum_kernel(SplitBufs b, int it) {
+  using SP = Split<Mech, GM, LS>;
+  const long long cnt = b.cnt[3 * (it & 1) + 1];
+  for (long long e = (long long)blockIdx.x * BDFB_SPLIT_BLOCK + threadIdx.x; e < cnt;
+       e += (long long)gridDim.x * BDFB_SPLIT_BLOCK) {
+    const long long slot = b.jlist[e];
+    const TS* t = SP::ts(b, slot);
+    if (t->coop) continue;
+    Mech::template jac_sum<32>(t->aux, b.jscr + ((e >> 5) * Mech::NSC3) * 32 + (e & 31));
+  }
+}
+#ifndef BDFB_SPLIT_JAC_PARTS
+#define BDFB_SPLIT_JAC_PARTS 1   // 0: pass 1 one thread per entry (split_jac_p1_kernel)
+#endif
+// scratch stride (doubles per entry) of the two-pass Jacobian
+template <class Mech>
+__host__ __device__ constexpr int jac_scr_doubles() { return BDFB_SPLIT_JAC_PARTS ? Mech::NSC3 : Mech::NSC2; }
+
 template <class Mech, class GM, int LS = LS_DENSE>
 __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_p2_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM, LS>;
@@ -970,7 +1013,8 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_p2_kernel(SplitBuf
     if (e >= cnt) continue;
     const long long slot = b.jlist[e];
     if (SP::ts(b, slot)->coop) continue;                       // pass 1 failed (T <= 0): recoverable
-    Mech::template jac_col<32>(j, b.jscr + ((e >> 5) * Mech::NSC2) * 32 + (e & 31), b.J + slot * SP::JREC);
+    Mech::template jac_col<32>(j, b.jscr + ((e >> 5) * jac_scr_doubles<Mech>()) * 32 + (e & 31),
+                               b.J + slot * SP::JREC);
   }
 }
 
@@ -1040,6 +1084,16 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK, 3) split_dqjac_kernel(SplitB
 // kernel's 19K SASS instructions, ncu IPC 1.4, 2.4K warp instructions per LU).  A group whose pivot is an exact
 // zero keeps computing on garbage that is never stored; info = k + 1 of its first zero pivot, else 0.
 constexpr int OCT = 8;
+// a[ps][j] for a runtime slot ps < R (a chain of R - 1 selects: the pivot row is always a real row, so the last
+// slot needs no test; the zero-initialised form cost R selects per double -- 41% of K_lu's instructions were FSEL)
+template <int R, int NN>
+__device__ __forceinline__ double oct_pick(const double (&a)[R][NN], int ps, int j) {
+  double v = a[R - 1][j];
+#pragma unroll
+  for (int s = R - 2; s >= 0; --s) v = (ps == s) ? a[s][j] : v;
+  return v;
+}
+
 // column k of oct_factor (k a compile-time constant so that a[][] stays in registers)
 template <int N, int K>
 __device__ __forceinline__ void oct_column(int gl, double (&a)[(N + OCT - 1) / OCT][N], int (&pos)[(N + OCT - 1) / OCT],
@@ -1073,11 +1127,7 @@ __device__ __forceinline__ void oct_column(int gl, double (&a)[(N + OCT - 1) / O
   if (!(bv > 0.0) && info == 0) info = K + 1;   // exact zero pivot (uniform in the group)
   const int bp = bpr >> 16, br = bpr & 0xffff;
   const int pl = br & (OCT - 1), ps = br / OCT;   // owner lane and slot of the pivot row
-  double pk = 0.0;
-#pragma unroll
-  for (int s = 0; s < R; ++s)
-    if (s == ps) pk = a[s][K];
-  const double pv = __shfl_sync(0xffffffffu, pk, pl, OCT);
+  const double pv = __shfl_sync(0xffffffffu, oct_pick<R>(a, ps, K), pl, OCT);
   const double rinv = 1.0 / pv;
 #pragma unroll
   for (int s = 0; s < R; ++s) {
@@ -1102,11 +1152,7 @@ __device__ __forceinline__ void oct_column(int gl, double (&a)[(N + OCT - 1) / O
   }
 #pragma unroll
   for (int j = K + 1; j < N; ++j) {
-    double pj = 0.0;
-#pragma unroll
-    for (int s = 0; s < R; ++s)
-      if (s == ps) pj = a[s][j];
-    pj = __shfl_sync(0xffffffffu, pj, pl, OCT);
+    const double pj = __shfl_sync(0xffffffffu, oct_pick<R>(a, ps, j), pl, OCT);
 #pragma unroll
     for (int s = 0; s < R; ++s)
       if (gl + OCT * s < N) a[s][j] = fma(-m[s], pj, a[s][j]);

@@ -58,7 +58,7 @@ struct SplitK {
     gm->ts_doubles = TS_STRIDE;
     gm->jrec = LS == LS_DENSE ? SP::JREC : 0;   // no J / LU records for the matrix-free solvers
     gm->lurec = LS == LS_DENSE ? SP::LUREC : 0;
-    if constexpr (JAC2) gm->jscr = Mech::NSC2;
+    if constexpr (JAC2) gm->jscr = jac_scr_doubles<Mech>();
     else gm->jscr = 0;
     return cudaSuccess;
   }
@@ -143,7 +143,13 @@ struct SplitK {
             split_jac_tpc_kernel<Mech, GM, LS><<<(unsigned)gm.rhs_grid, blk, 0, ss>>>(b, it);
           else if (JAC2 && jac2 && b.jscr) {
             if constexpr (JAC2) {
-              split_jac_p1_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
+              if (BDFB_SPLIT_JAC_PARTS) {
+                split_jac_part_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
+                split_jac_sum_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
+                ++n;
+              } else {
+                split_jac_p1_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
+              }
               split_jac_p2_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
               ++n;
             }
