@@ -318,7 +318,11 @@ int bdfb_eval_rhs(bdfb_batch *b, double t, const double *y, const double *f_ext,
                   const double *aux, double *f, int32_t *status, void *stream);
 
 /* J = dR/dy for every cell: J[(i*n + j)*N + c] (device, N*n*n fp64).
- * Only for dense-solver models (not NYX_KWH).                               */
+ * Only for dense-solver models (not NYX_KWH).  Mechanism models with the
+ * SPLIT (or AUTO) kernel and the analytic Jacobian run the SPLIT path's
+ * K_jac code: the two-pass generated Jacobian (reaction parts, the ordered
+ * production-rate sum, one column per thread), with its device scratch
+ * allocated and freed on `stream`; a cell whose T <= 0 keeps its J entries. */
 int bdfb_eval_jac(bdfb_batch *b, double t, const double *y, const double *aux, double *J,
                   void *stream);
 

@@ -510,14 +510,14 @@ def generate(name, out_dir):
     p1 = re.sub(r"sc\[(\d+)\]", lambda m: f"sc[{m.group(1)}*SC]", p1)
     assert "*S]" not in p1, "unconverted stride in jac_p1"
     A(p1)
-    # ---- parted pass 1 (jac_part<SY, SC, P> + jac_sum<SC>): the reactions dealt round-robin to NPART parts
-    # (one warp-uniform part per thread), so a Jacobian list of ~10^4 cells runs NPART x the threads over
-    # NPART x shorter chains.  Part P evaluates the thermo of the species its reactions need (h/RT into the
-    # scratch, identical values from every part), its reactions' kf, kr, dq/dT, dq/d[M] (the same expressions
-    # as jac) and partial production rates; part 0 also the per-species h/RT, cv_k, C_k, u_k/W_k and the
-    # energy sums that need no rates (cv, dcv).  jac_sum (one thread per cell) adds the partial rates in part
-    # order and forms su, scw, icv, irho, fT0 (the production rates are summed in a different order than in
-    # jac: J agrees with it to rounding, R19).  Scratch: jac's layout, then WP[P][k] at O_WP + P K + k.
+    # ---- parted pass 1 (jac_part<SY, SC>(P, ...) + jac_sum<SY, SC>): the reactions dealt round-robin to NPART
+    # parts (one warp-uniform part per thread), so a Jacobian list of ~10^4 cells runs NPART x the threads over
+    # NPART x shorter chains.  Part P evaluates the thermo of the species its reversible reactions need (h/RT
+    # into the scratch: identical values from every part), its reactions' kf, kr, dq/dT, dq/d[M] (the
+    # expressions of jac) and its partial production rates.  jac_sum (one thread per cell, after the parts):
+    # C_k, cv_k, u_k/W_k, cv, dcv (jac_tail's expressions), the production rates added in part order, su, scw,
+    # icv, irho, fT0 (the rates are summed in another order than jac's: J agrees with it to rounding, R19).
+    # Scratch: jac's layout, then WP[P][k] at O_WP + P K + k.
     NPART = 4
     O_WP = NSC2
     NSC3 = O_WP + NPART * K
@@ -530,8 +530,6 @@ def generate(name, out_dir):
             x = rx[r]
             if x["reversible"]:
                 need |= {idx[t] for t in x["reactants"]} | {idx[t] for t in x["products"]}
-        if P == 0:
-            need = set(range(K))
         touched = sorted({i for r in rs for i in nu[r]})
         touched_all.append(touched)
         B = []
@@ -542,16 +540,14 @@ def generate(name, out_dir):
             AB(f"  const double y{k} = yp[{k}*SY];\n")
         thermo_common(AB)
 
-        def th(k, a, AB=AB, need=need, P=P):
+        def th(k, a, AB=AB, need=need):
             if k not in need:
                 return
-            eg_body(k, a) if False else AB(
-                f"    eg{k} = fexp({d(a[0])} * (lnT - 1.0) + {d(a[1] / 2)} * T + {d(a[2] / 6)} * T2 + {d(a[3] / 12)} * T3 + "
-                f"{d(a[4] / 20)} * T4 - {d(a[5])} * invT + {d(a[6])});\n")
+            AB(f"    eg{k} = fexp({d(a[0])} * (lnT - 1.0) + {d(a[1] / 2)} * T + {d(a[2] / 6)} * T2 + {d(a[3] / 12)} * T3 + "
+               f"{d(a[4] / 20)} * T4 - {d(a[5])} * invT + {d(a[6])});\n")
             AB(f"    sc[{O_H + k}*S] = {d(a[0])} + T * ({d(a[1] / 2)} + T * ({d(a[2] / 3)} + T * ({d(a[3] / 4)} + T * {d(a[4] / 5)}))) + {d(a[5])} * invT;\n")
-            if P == 0:
-                AB(f"    sc[{O_CV + k}*S] = ({d(a[0] - 1)} + T * ({d(a[1])} + T * ({d(a[2])} + T * ({d(a[3])} + T * {d(a[4])})))) * {d(RU / W[k])};\n")
-        _nasa(AB, tab, tm, th)
+        if need:
+            _nasa(AB, tab, tm, th)
         for k in recip:
             if k in need:
                 AB(f"  const double ieg{k} = 1.0 / eg{k};\n")
@@ -563,18 +559,6 @@ def generate(name, out_dir):
             reaction(AB, r, rx[r], True)
         for k in touched:
             AB(f"  sc[{O_WP + P * K + k}*S] = w{k};\n")
-        if P == 0:
-            AB("  double cv = 0.0, dcv = 0.0;\n")
-
-            def tail0(k, a, AB=AB):
-                AB(f"    {{ const double hk = sc[{O_H + k}*S], cvk = sc[{O_CV + k}*S];\n")
-                AB(f"      sc[{O_U + k}*S] = (hk - 1.0) * {d(RU)} * T * {d(1.0 / W[k])};\n")
-                AB(f"      cv = fma(y{k}, cvk, cv);\n")
-                AB(f"      dcv = fma(y{k} * {d(RU / W[k])}, {d(a[1])} + T * ({d(2 * a[2])} + T * ({d(3 * a[3])} + T * {d(4 * a[4])})), dcv); }}\n")
-            _nasa(AB, tab, tm, tail0)
-            for k in range(K):
-                AB(f"  sc[{O_C + k}*S] = C{k};\n")
-            AB(f"  sc[{O_SC}*S] = cv;\n  sc[{O_SC + 4}*S] = dcv;\n")
         AB("  return 0;\n  }\n")
         body = "".join(B)
         body = re.sub(r"  double eg(\d+);\n", lambda m: m.group(0) if int(m.group(1)) in need else "", body)
@@ -586,20 +570,38 @@ def generate(name, out_dir):
     for P in range(NPART):
         A(f"  case {P}: return jac_part{P}<SY, SC>(yp, rho, sc);\n")
     A("  }\n  return 0;\n  }\n")
-    # jac_sum: production rates (parts in order), su, scw (species order, jac_tail's operations), the scalars
-    A("  template <long long SC>\n  __device__ __forceinline__ static void jac_sum(double rho, double* __restrict__ sc) {\n")
-    A("  double su = 0.0, scw = 0.0;\n")
+    B = []
+    AB = B.append
+    AB("  template <long long SY, long long SC>\n  __device__ __forceinline__ static int jac_sum("
+       "const double* __restrict__ yp, double rho, double* __restrict__ sc) {\n")
+    for k in range(N):
+        AB(f"  const double y{k} = yp[{k}*SY];\n")
+    AB(f"  const double T = y{K};\n  if (!(T > 0.0)) return 1;\n  const double invT = 1.0 / T;\n")
     for k in range(K):
+        AB(f"  sc[{O_C + k}*S] = rho * y{k} * {d(1.0 / W[k])};\n")
+    AB("  double cv = 0.0, su = 0.0, scw = 0.0, dcv = 0.0;\n")
+
+    def tails(k, a, AB=AB):
         parts_k = [P for P in range(NPART) if k in touched_all[P]]
-        if not parts_k:
-            A(f"  {{ const double w = 0.0;\n")
-        else:
-            A(f"  {{ const double w = " + " + ".join(f"sc[{O_WP + P * K + k}*SC]" for P in parts_k) + ";\n")
-        A(f"    su = fma(sc[{O_U + k}*SC] * {d(W[k])}, w, su);\n")
-        A(f"    scw = fma(sc[{O_CV + k}*SC] * {d(W[k])}, w, scw); }}\n")
-    A(f"  const double icv = 1.0 / sc[{O_SC}*SC], irho = 1.0 / rho;\n")
-    A(f"  sc[{O_SC}*SC] = icv;\n  sc[{O_SC + 1}*SC] = irho;\n  sc[{O_SC + 2}*SC] = -su * irho * icv;\n"
-      f"  sc[{O_SC + 3}*SC] = scw;\n  }}\n")
+        wsum = " + ".join(f"sc[{O_WP + P * K + k}*S]" for P in parts_k) if parts_k else "0.0"
+        AB(f"    {{ const double hk = {d(a[0])} + T * ({d(a[1] / 2)} + T * ({d(a[2] / 3)} + T * ({d(a[3] / 4)} + T * {d(a[4] / 5)}))) + {d(a[5])} * invT;\n")
+        AB(f"      const double cvk = ({d(a[0] - 1)} + T * ({d(a[1])} + T * ({d(a[2])} + T * ({d(a[3])} + T * {d(a[4])})))) * {d(RU / W[k])};\n")
+        AB(f"      sc[{O_CV + k}*S] = cvk;\n")
+        AB(f"      const double uoW = (hk - 1.0) * {d(RU)} * T * {d(1.0 / W[k])};\n")
+        AB(f"      sc[{O_U + k}*S] = uoW;\n")
+        AB(f"      const double w = {wsum};\n")
+        AB(f"      cv = fma(y{k}, cvk, cv);\n")
+        AB(f"      su = fma(uoW * {d(W[k])}, w, su);\n")
+        AB(f"      scw = fma(cvk * {d(W[k])}, w, scw);\n")
+        AB(f"      dcv = fma(y{k} * {d(RU / W[k])}, {d(a[1])} + T * ({d(2 * a[2])} + T * ({d(3 * a[3])} + T * {d(4 * a[4])})), dcv); }}\n")
+    _nasa(AB, tab, tm, tails)
+    AB("  const double icv = 1.0 / cv, irho = 1.0 / rho;\n")
+    AB(f"  sc[{O_SC}*S] = icv;\n  sc[{O_SC + 1}*S] = irho;\n  sc[{O_SC + 2}*S] = -su * irho * icv;\n"
+       f"  sc[{O_SC + 3}*S] = scw;\n  sc[{O_SC + 4}*S] = dcv;\n  return 0;\n  }}\n")
+    body = "".join(B)
+    body = re.sub(r"sc\[(\d+)\*S\]", lambda m: f"sc[{m.group(1)}*SC]", body)
+    assert "*S]" not in body, "unconverted stride in jac_sum"
+    A(body)
     A(f"  static constexpr int NSC2 = {NSC2};   // scratch doubles of jac_p1 / jac_col\n")
     A("  // column j (0..N-1) of the column-major J from jac_p1's scratch (element stride SC)\n")
     A("  template <long long SC>\n  __device__ __forceinline__ static void jac_col(int j, const double* __restrict__ sc, "

@@ -958,9 +958,9 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_p1_kernel(SplitBuf
   }
 }
 // K_jac pass 1 parted (default): thread per (entry, part P) with P warp-uniform and equal for neighbour warps
-// (jac_part: the reactions dealt round-robin to Mech::NPART parts), then jac_sum, one thread per entry (partial
-// production rates in part order, the energy sums and scalars): NPART x the threads of split_jac_p1_kernel
-// over NPART x shorter chains (ncu: p1 ran ~2 warps per SM, IPC 0.3, instruction-cache bound)
+// (jac_part: the reactions dealt round-robin to Mech::NPART parts), then jac_sum, one thread per entry (the
+// per-species thermo, the production rates added in part order, the energy sums and scalars): NPART x the
+// threads of split_jac_p1_kernel over NPART x shorter chains (ncu: p1 ran ~2 warps per SM, IPC 0.3)
 template <class Mech, class GM, int LS = LS_DENSE>
 __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_part_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM, LS>;
@@ -989,7 +989,8 @@ __global__ void __launch_bounds__(BDFB_SPLIT_BLOCK) split_jac_sum_kernel(SplitBu
     const long long slot = b.jlist[e];
     const TS* t = SP::ts(b, slot);
     if (t->coop) continue;
-    Mech::template jac_sum<32>(t->aux, b.jscr + ((e >> 5) * Mech::NSC3) * 32 + (e & 31));
+    const typename SP::W w = SP::ws(b, slot);
+    Mech::template jac_sum<VEC_S, 32>(&w.yq(0), t->aux, b.jscr + ((e >> 5) * Mech::NSC3) * 32 + (e & 31));
   }
 }
 #ifndef BDFB_SPLIT_JAC_PARTS

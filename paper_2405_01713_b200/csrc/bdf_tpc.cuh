@@ -68,6 +68,15 @@ constexpr int kAttemptUnroll = BDFB_ATTEMPT_UNROLL;   // chunks of the ATTEMPT p
 #endif
 // LU stage organisation: 0 block-packed thread-per-cell (default), 1 warp-cooperative
 // per cell, 2 thread-per-cell in place (experiments; identical results)
+// set_bdf (every attempt) and prepare_next (every step): out of line by default (register budget of the
+// control kernels); BDFB_HOT_INLINE_ON=1 inlines them (the call saves/restores live registers through local
+// memory: 517 STL/LDL in K_ctl's SASS)
+#if defined(BDFB_HOT_INLINE_ON) && BDFB_HOT_INLINE_ON
+#define BDFB_HOT_INLINE __forceinline__
+#else
+#define BDFB_HOT_INLINE __noinline__
+#endif
+
 #ifndef BDFB_TPC_LU
 #define BDFB_TPC_LU 0
 #endif
@@ -330,7 +339,7 @@ struct TpcIntegrator {
   }
 
   // cvSetBDF + cvSetTqBDF (scalar)
-  __device__ static __noinline__ void set_bdf(TS& s) {
+  __device__ static BDFB_HOT_INLINE void set_bdf(TS& s) {
     const int q = s.q;
     const double h = s.h;
     double xi_inv = 1.0, xistar_inv = 1.0, alpha0 = -1.0, alpha0_hat = -1.0, hsum = h;
@@ -485,7 +494,7 @@ struct TpcIntegrator {
   }
 
   // PREPARE_NEXT (ddn = ||zn[q]||, dup = ||acor - cquot zn[qmax]||, from the complete-step pass)
-  __device__ static __noinline__ void prepare_next(const Opts& o, TS& s, const W& w, double dsm, double ddn,
+  __device__ static BDFB_HOT_INLINE void prepare_next(const Opts& o, TS& s, const W& w, double dsm, double ddn,
                                                    double dup) {
     if (s.etamax == 1.0) {
       s.qwait = s.qwait > 2 ? s.qwait : 2;

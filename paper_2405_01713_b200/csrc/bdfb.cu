@@ -967,6 +967,10 @@ extern "C" int bdfb_eval_jac(bdfb_batch* b, double t, const double* y, const dou
   if (model_needs_aux(b->model) && !aux) return fail(b, BDFB_EINVAL, "this model needs aux (density)");
   cudaSetDevice(b->device);
   cudaStream_t st = (cudaStream_t)stream;
+  if (use_split(b) && b->jac_mode != BDFB_JAC_DQ) {   // the SPLIT path's K_jac code (two-pass generated Jacobian)
+    const cudaError_t e = split_jac_diag(b->model, b->ncells, y, aux, J, st);
+    return e == cudaSuccess ? BDFB_OK : cuda_fail(b, e, "split Jacobian diagnostic");
+  }
   switch (b->model) {
     case BDFB_MODEL_LINEAR: return launch_eval<ModelLinear>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);
     case BDFB_MODEL_ROBERTSON: return launch_eval<ModelRobertson>(b, t, y, nullptr, aux, nullptr, nullptr, J, st);

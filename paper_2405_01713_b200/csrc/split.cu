@@ -88,6 +88,86 @@ __global__ void __launch_bounds__(128) split_lu_diag_kernel(long long N, double*
   }
 }
 
+// Jacobian diagnostic: the SPLIT path's two-pass generated Jacobian (jac_part / jac_sum / jac_col, the device
+// functions of split_jac_part/sum/p2_kernel, the same warp-uniform part and column mapping and the same
+// warp-blocked scratch) on N states in YC layout; J[(i n + j) N + c] out.
+template <class Mech>
+__global__ void __launch_bounds__(128) jd_pack(long long N, const double* y, double* yb) {
+  constexpr int n = Mech::N;
+  const long long c = blockIdx.x * 128ll + threadIdx.x;
+  if (c >= N) return;
+  for (int k = 0; k < n; ++k) yb[((c >> 5) * n + k) * 32 + (c & 31)] = y[(long long)k * N + c];
+}
+template <class Mech>
+__global__ void __launch_bounds__(128) jd_part(long long N, const double* yb, const double* aux, double* scr,
+                                               int* status) {
+  constexpr int n = Mech::N;
+  const long long neb = (N + 31) / 32, nw = neb * Mech::NPART;
+  const int lane = threadIdx.x & 31;
+  for (long long gw = (blockIdx.x * 128ll + threadIdx.x) >> 5; gw < nw; gw += (gridDim.x * 128ll) >> 5) {
+    const int P = (int)(gw / neb);
+    const long long e = (gw - P * neb) * 32 + lane;
+    if (e >= N) continue;
+    const int rv = Mech::template jac_part<32, 32>(P, yb + ((e >> 5) * n) * 32 + (e & 31), aux[e],
+                                                   scr + ((e >> 5) * Mech::NSC3) * 32 + (e & 31));
+    if (P == 0) status[e] = rv;
+  }
+}
+template <class Mech>
+__global__ void __launch_bounds__(128) jd_sum(long long N, const double* yb, const double* aux, double* scr,
+                                              const int* status) {
+  constexpr int n = Mech::N;
+  const long long e = blockIdx.x * 128ll + threadIdx.x;
+  if (e >= N || status[e]) return;
+  Mech::template jac_sum<32, 32>(yb + ((e >> 5) * n) * 32 + (e & 31), aux[e],
+                                 scr + ((e >> 5) * Mech::NSC3) * 32 + (e & 31));
+}
+template <class Mech>
+__global__ void __launch_bounds__(128) jd_col(long long N, const double* scr, const int* status, double* Jrec) {
+  constexpr int n = Mech::N;
+  const long long neb = (N + 31) / 32, nw = neb * n;
+  const int lane = threadIdx.x & 31;
+  for (long long gw = (blockIdx.x * 128ll + threadIdx.x) >> 5; gw < nw; gw += (gridDim.x * 128ll) >> 5) {
+    const int j = (int)(gw / neb);
+    const long long e = (gw - j * neb) * 32 + lane;
+    if (e >= N || status[e]) continue;
+    Mech::template jac_col<32>(j, scr + ((e >> 5) * Mech::NSC3) * 32 + (e & 31), Jrec + e * (n * n));
+  }
+}
+template <class Mech>
+__global__ void __launch_bounds__(128) jd_unpack(long long N, const double* Jrec, const int* status, double* J) {
+  constexpr int n = Mech::N;
+  const long long c = blockIdx.x * 128ll + threadIdx.x;
+  if (c >= N || status[c]) return;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) J[((long long)i * n + j) * N + c] = Jrec[c * (n * n) + j * n + i];
+}
+template <class Mech>
+cudaError_t jac_diag(long long N, const double* y, const double* aux, double* J, cudaStream_t st) {
+  constexpr int n = Mech::N;
+  const long long Np = (N + 31) / 32 * 32;
+  double *yb = nullptr, *scr = nullptr, *Jrec = nullptr;
+  int* status = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&yb, sizeof(double) * n * Np, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&scr, sizeof(double) * Mech::NSC3 * Np, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&Jrec, sizeof(double) * n * n * Np, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&status, sizeof(int) * Np, st);
+  if (e == cudaSuccess) {
+    const unsigned g = (unsigned)((N + 127) / 128);
+    jd_pack<Mech><<<g, 128, 0, st>>>(N, y, yb);
+    jd_part<Mech><<<g * Mech::NPART, 128, 0, st>>>(N, yb, aux, scr, status);
+    jd_sum<Mech><<<g, 128, 0, st>>>(N, yb, aux, scr, status);
+    jd_col<Mech><<<g * n, 128, 0, st>>>(N, scr, status, Jrec);
+    jd_unpack<Mech><<<g, 128, 0, st>>>(N, Jrec, status, J);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(yb, st);
+  cudaFreeAsync(scr, st);
+  cudaFreeAsync(Jrec, st);
+  cudaFreeAsync(status, st);
+  return e;
+}
+
 using KH2 = SplitK<Tpc_h2_lidryer, ModelMech<mech_h2_lidryer::Traits>>;
 using KDRM = SplitK<Tpc_drm19_class, ModelMech<mech_drm19_class::Traits>>;
 using KGRI = SplitK<Tpc_gri53_class, LanesOf<Tpc_gri53_class>::GM>;   // n = 54 (split_big.cuh setup kernels)
@@ -111,6 +191,15 @@ cudaError_t split_lu_diag(int n, long long N, double* M, int* piv, double* b, in
 // scratch doubles per cell of the diagnostic's record pool (the caller rounds N up to a multiple of 32)
 size_t split_lu_rec_doubles(int n) {
   return LU_STRIDE == 1 ? (size_t)((n * n + n + (n + 1) / 2 + 3) / 4 * 4) : (size_t)(n * n + 2 * n);
+}
+
+cudaError_t split_jac_diag(int mech, long long N, const double* y, const double* aux, double* J, cudaStream_t st) {
+  switch (mech) {
+    case BDFB_MODEL_MECH_H2: return jac_diag<Tpc_h2_lidryer>(N, y, aux, J, st);
+    case BDFB_MODEL_MECH_DRM19: return jac_diag<Tpc_drm19_class>(N, y, aux, J, st);
+    case BDFB_MODEL_MECH_GRI53: return jac_diag<Tpc_gri53_class>(N, y, aux, J, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t split_geometry(int mech, int ls, int device, SplitGeom* gm) {

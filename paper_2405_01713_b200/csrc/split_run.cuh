@@ -21,8 +21,8 @@ struct SplitK {
     return BDFB_SPLIT_TS_SMEM ? sizeof(double) * (size_t)TS_STRIDE * BDFB_SPLIT_CTL_BLOCK : 0;
   }
   static constexpr bool BIG = Mech::N > 32;   // split_big.cuh setup kernels (lanes Jacobian, register-row LU)
-  // two-pass generated Jacobian (split_jac_p1/p2_kernel), n <= 32
-  static constexpr bool JAC2 = !BIG && LS == LS_DENSE;
+  // two-pass generated Jacobian (split_jac_part/sum/p2_kernel; BDFB_SPLIT_JAC2=0: the group/lanes one)
+  static constexpr bool JAC2 = LS == LS_DENSE;
   static constexpr size_t jac_smem() {
     if constexpr (BIG) {
       return sizeof(double) * (size_t)JacLanesSmem<Mech>::PER_WARP * JL_WARPS;
@@ -133,9 +133,16 @@ struct SplitK {
           ss = st2;
           if (events) cudaEventRecord(ev[5], st2);
         }
-        if constexpr (LS == LS_DENSE && BIG) {   // n > 32: lanes Jacobian, one cell per warp
-          const unsigned gj = (unsigned)gm.setup_grid;
-          split_jac_lanes_kernel<Mech, GM, LS><<<gj, 32 * JL_WARPS, jac_smem(), ss>>>(b, it);
+        if constexpr (LS == LS_DENSE && BIG) {   // n > 32: two-pass generated Jacobian, or the lanes one
+          if (BDFB_SPLIT_JAC_PARTS && jac2 && b.jscr) {
+            split_jac_part_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
+            split_jac_sum_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
+            split_jac_p2_kernel<Mech, GM, LS><<<(unsigned)gm.setup_grid, blk, 0, ss>>>(b, it);
+            n += 2;
+          } else {
+            const unsigned gj = (unsigned)gm.setup_grid;
+            split_jac_lanes_kernel<Mech, GM, LS><<<gj, 32 * JL_WARPS, jac_smem(), ss>>>(b, it);
+          }
         } else if constexpr (LS == LS_DENSE) {   // the matrix-free linear solvers have no setup kernels
           if (b.jac_dq)
             split_dqjac_kernel<Mech, GM, LS><<<gdq, blk, 0, ss>>>(b, it);
