@@ -968,7 +968,7 @@ extern "C" int bdfb_eval_jac(bdfb_batch* b, double t, const double* y, const dou
   cudaSetDevice(b->device);
   cudaStream_t st = (cudaStream_t)stream;
   if (use_split(b) && b->jac_mode != BDFB_JAC_DQ) {   // the SPLIT path's K_jac code (two-pass generated Jacobian)
-    const cudaError_t e = split_jac_diag(b->model, b->ncells, y, aux, J, st);
+    const cudaError_t e = split_jac_diag(b->model, b->ncells, y, aux, J, nullptr, st);
     return e == cudaSuccess ? BDFB_OK : cuda_fail(b, e, "split Jacobian diagnostic");
   }
   switch (b->model) {

@@ -10,11 +10,24 @@
 #include <type_traits>
 #include <vector>
 
+#include "../../include/bdfb.h"
 #include "global_lanes.cuh"
 #include "global_mode.cuh"
 #include "global_tpc.cuh"
+#include "split_api.h"
 
 namespace bdfb {
+
+// n = 54 global-norm J: the generated two-pass Jacobian of the SPLIT path (default) or, with BDFB_GLOBAL_JAC2=0,
+// the table-driven lanes model (gl_setup; 263 ns per cell vs ~50 ns, profiles/r2)
+static inline bool gl_jac2() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BDFB_GLOBAL_JAC2");
+    v = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
 
 struct GlobalBuffers {           // allocated once (bdfb_create, GLOBAL_NORM mode)
   GVec v{};
@@ -269,9 +282,18 @@ struct GlobalRunner {
       ++launches; gt_setup<TM><<<gridc(), 128, 0, st>>>(N, jbad ? 1 : 0, gamma, B.v.yq, aux, B.J, B.LU, B.perm,
                                                          B.invd, B.flag);
     } else if constexpr (LANES) {
-      if (jbad) {   // J into HBM (table-driven lanes model), then the register-row LU
-        ++launches; gl_setup<Model><<<gridg(), 128, sizeof(double) * GLK<Model>::PG_SET * GLK<Model>::GPB, st>>>(
-            N, 1, gamma, B.v.yq, aux, B.J, B.LU, B.perm, B.invd, B.flag, 1);
+      if (jbad) {   // J into HBM, then the register-row LU
+        if (gl_jac2()) {   // the generated two-pass Jacobian of the SPLIT path (5 launches per 65536-cell chunk)
+          const cudaError_t je = split_jac_diag(BDFB_MODEL_MECH_GRI53, N, B.v.yq, aux, B.J, B.flag, st);
+          if (je != cudaSuccess) {   // e.g. no scratch: reported, and the setup fails (recoverably)
+            fprintf(stderr, "bdfb: global-norm Jacobian: %s\n", cudaGetErrorString(je));
+            cudaMemsetAsync(B.flag, 1, 1, st);
+          }
+          launches += 5 * (int)((N + 65535) / 65536);
+        } else {           // BDFB_GLOBAL_JAC2=0: the table-driven lanes model
+          ++launches; gl_setup<Model><<<gridg(), 128, sizeof(double) * GLK<Model>::PG_SET * GLK<Model>::GPB, st>>>(
+              N, 1, gamma, B.v.yq, aux, B.J, B.LU, B.perm, B.invd, B.flag, 1);
+        }
       }
       ++launches; gl_lu<Model::N><<<(unsigned)((N + GLU<Model::N>::CPB - 1) / GLU<Model::N>::CPB), GLU<Model::N>::T,
                                     gl_lu_smem<Model::N>(), st>>>(N, gamma, B.J, B.LU, B.perm, B.invd, B.flag);

@@ -210,8 +210,13 @@ __global__ void __launch_bounds__(128) gl_setup(long long N, int jbad, double ga
 // CPB cells per block of CPB x 32 ceil(n/32) threads: all 12 warps of an SM walk the same column of the
 // unrolled factorisation together (one barrier pair per column for all six cells: instruction-cache locality)
 template <int NN>
+#ifndef BDFB_GLU_THREADS
+#define BDFB_GLU_THREADS 384   // threads per block; 384 / BDFB_GLU_THREADS blocks per SM (the 12 warps either way)
+#endif
 struct GLU {
-  static constexpr int W = (NN + 31) / 32, TC = 32 * W, CPB = 384 / TC > 0 ? 384 / TC : 1, T = CPB * TC;
+  static constexpr int W = (NN + 31) / 32, TC = 32 * W,
+                       CPB = BDFB_GLU_THREADS / TC > 0 ? BDFB_GLU_THREADS / TC : 1, T = CPB * TC,
+                       BPS = 384 / T > 0 ? 384 / T : 1;   // resident blocks per SM
 };
 // shared state of a gl_lu block: per cell the published pivot row and 1/pivot, the warps' pivot candidates
 // (double-buffered by column parity)
@@ -311,7 +316,7 @@ __device__ __forceinline__ int glu_columns(GLUShared<NN>& sh, double (&a)[NN], i
 // per SM in lockstep.  Factors written in pivoted row order, cell-minor (element e of cell c at [e N + c]) with
 // perm and 1/U_kk (the tpc_solve layout).
 template <int NN>
-__global__ void __launch_bounds__(GLU<NN>::T, 1)
+__global__ void __launch_bounds__(GLU<NN>::T, GLU<NN>::BPS)
     gl_lu(long long N, double gamma, const double* J, double* LU, int* perm, double* invd, int* flag) {
   __shared__ GLUShared<NN> sh;
   // the block's six matrices staged element-major, cell-minor (T[e CPB + cb]): the cell-minor HBM layout is then

@@ -92,11 +92,11 @@ __global__ void __launch_bounds__(128) split_lu_diag_kernel(long long N, double*
 // functions of split_jac_part/sum/p2_kernel, the same warp-uniform part and column mapping and the same
 // warp-blocked scratch) on N states in YC layout; J[(i n + j) N + c] out.
 template <class Mech>
-__global__ void __launch_bounds__(128) jd_pack(long long N, const double* y, double* yb) {
+__global__ void __launch_bounds__(128) jd_pack(long long N, long long Nst, long long c0, const double* y, double* yb) {
   constexpr int n = Mech::N;
   const long long c = blockIdx.x * 128ll + threadIdx.x;
   if (c >= N) return;
-  for (int k = 0; k < n; ++k) yb[((c >> 5) * n + k) * 32 + (c & 31)] = y[(long long)k * N + c];
+  for (int k = 0; k < n; ++k) yb[((c >> 5) * n + k) * 32 + (c & 31)] = y[(long long)k * Nst + c0 + c];
 }
 template <class Mech>
 __global__ void __launch_bounds__(128) jd_part(long long N, const double* yb, const double* aux, double* scr,
@@ -135,30 +135,38 @@ __global__ void __launch_bounds__(128) jd_col(long long N, const double* scr, co
   }
 }
 template <class Mech>
-__global__ void __launch_bounds__(128) jd_unpack(long long N, const double* Jrec, const int* status, double* J) {
+__global__ void __launch_bounds__(128) jd_unpack(long long N, long long Nst, long long c0, const double* Jrec,
+                                                 const int* status, double* J, int* flag) {
   constexpr int n = Mech::N;
   const long long c = blockIdx.x * 128ll + threadIdx.x;
-  if (c >= N || status[c]) return;
+  if (c >= N) return;
+  if (status[c]) {
+    if (flag) atomicOr(flag, 1);
+    return;
+  }
   for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j) J[((long long)i * n + j) * N + c] = Jrec[c * (n * n) + j * n + i];
+    for (int j = 0; j < n; ++j) J[((long long)i * n + j) * Nst + c0 + c] = Jrec[c * (n * n) + j * n + i];
 }
+// N cells in chunks of at most JD_CHUNK (one scratch allocation): y[k N + c] in, J[(i n + j) N + c] out
+constexpr long long JD_CHUNK = 65536;
 template <class Mech>
-cudaError_t jac_diag(long long N, const double* y, const double* aux, double* J, cudaStream_t st) {
+cudaError_t jac_diag(long long N, const double* y, const double* aux, double* J, int* flag, cudaStream_t st) {
   constexpr int n = Mech::N;
-  const long long Np = (N + 31) / 32 * 32;
+  const long long C = N < JD_CHUNK ? (N + 31) / 32 * 32 : JD_CHUNK;
   double *yb = nullptr, *scr = nullptr, *Jrec = nullptr;
   int* status = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&yb, sizeof(double) * n * Np, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&scr, sizeof(double) * Mech::NSC3 * Np, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&Jrec, sizeof(double) * n * n * Np, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&status, sizeof(int) * Np, st);
-  if (e == cudaSuccess) {
-    const unsigned g = (unsigned)((N + 127) / 128);
-    jd_pack<Mech><<<g, 128, 0, st>>>(N, y, yb);
-    jd_part<Mech><<<g * Mech::NPART, 128, 0, st>>>(N, yb, aux, scr, status);
-    jd_sum<Mech><<<g, 128, 0, st>>>(N, yb, aux, scr, status);
-    jd_col<Mech><<<g * n, 128, 0, st>>>(N, scr, status, Jrec);
-    jd_unpack<Mech><<<g, 128, 0, st>>>(N, Jrec, status, J);
+  cudaError_t e = cudaMallocAsync((void**)&yb, sizeof(double) * n * C, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&scr, sizeof(double) * Mech::NSC3 * C, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&Jrec, sizeof(double) * n * n * C, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&status, sizeof(int) * C, st);
+  for (long long c0 = 0; e == cudaSuccess && c0 < N; c0 += C) {
+    const long long m = N - c0 < C ? N - c0 : C;
+    const unsigned g = (unsigned)((m + 127) / 128);
+    jd_pack<Mech><<<g, 128, 0, st>>>(m, N, c0, y, yb);
+    jd_part<Mech><<<g * Mech::NPART, 128, 0, st>>>(m, yb, aux + c0, scr, status);
+    jd_sum<Mech><<<g, 128, 0, st>>>(m, yb, aux + c0, scr, status);
+    jd_col<Mech><<<g * n, 128, 0, st>>>(m, scr, status, Jrec);
+    jd_unpack<Mech><<<g, 128, 0, st>>>(m, N, c0, Jrec, status, J, flag);
     e = cudaGetLastError();
   }
   cudaFreeAsync(yb, st);
@@ -193,11 +201,12 @@ size_t split_lu_rec_doubles(int n) {
   return LU_STRIDE == 1 ? (size_t)((n * n + n + (n + 1) / 2 + 3) / 4 * 4) : (size_t)(n * n + 2 * n);
 }
 
-cudaError_t split_jac_diag(int mech, long long N, const double* y, const double* aux, double* J, cudaStream_t st) {
+cudaError_t split_jac_diag(int mech, long long N, const double* y, const double* aux, double* J, int* flag,
+                           cudaStream_t st) {
   switch (mech) {
-    case BDFB_MODEL_MECH_H2: return jac_diag<Tpc_h2_lidryer>(N, y, aux, J, st);
-    case BDFB_MODEL_MECH_DRM19: return jac_diag<Tpc_drm19_class>(N, y, aux, J, st);
-    case BDFB_MODEL_MECH_GRI53: return jac_diag<Tpc_gri53_class>(N, y, aux, J, st);
+    case BDFB_MODEL_MECH_H2: return jac_diag<Tpc_h2_lidryer>(N, y, aux, J, flag, st);
+    case BDFB_MODEL_MECH_DRM19: return jac_diag<Tpc_drm19_class>(N, y, aux, J, flag, st);
+    case BDFB_MODEL_MECH_GRI53: return jac_diag<Tpc_gri53_class>(N, y, aux, J, flag, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -58,8 +58,10 @@ cudaError_t tpc_eval_rhs(int mech, long long N, const double* y, const double* f
 cudaError_t split_lu_diag(int n, long long N, double* M, int* piv, double* b, int* info, double* rec,
                           cudaStream_t st);
 size_t split_lu_rec_doubles(int n);
-// Jacobian diagnostic with the SPLIT path's two-pass generated Jacobian (jac_part / jac_sum / jac_col):
-// y[k N + c] in, J[(i n + j) N + c] out (cells whose T <= 0 are left untouched); device scratch allocated on st
-cudaError_t split_jac_diag(int mech, long long N, const double* y, const double* aux, double* J, cudaStream_t st);
+// The SPLIT path's two-pass generated Jacobian (jac_part / jac_sum / jac_col) on N cells in chunks of 65536:
+// y[k N + c] in, J[(i n + j) N + c] out (cells whose T <= 0 are left untouched and set *flag, if given, to 1);
+// device scratch allocated and freed on st.  The Jacobian diagnostic, and the global-norm mode's J for n = 54.
+cudaError_t split_jac_diag(int mech, long long N, const double* y, const double* aux, double* J, int* flag,
+                           cudaStream_t st);
 
 }  // namespace bdfb

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(32 * JL_WARPS) split_jac_lanes_kernel(SplitBuf
 
 // K_lu, six cells per block (grid-stride over the setup list in block-uniform trips)
 template <class Mech, class GM, int LS>
-__global__ void __launch_bounds__(GLU<Mech::N>::T, 1) split_lu_rows_kernel(SplitBufs b, int it) {
+__global__ void __launch_bounds__(GLU<Mech::N>::T, GLU<Mech::N>::BPS) split_lu_rows_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM, LS>;
   constexpr int N = Mech::N, TC = GLU<N>::TC, CPB = GLU<N>::CPB;
   __shared__ GLUShared<N> sh;
