@@ -334,7 +334,9 @@ def oracle_cells_per_s(cfg, budget_s=15.0, threads=None, rank_cells=None, steps=
         from synth import flame_field
         # a uniform random sample of the grid's cells (seeded): the workload's own mix of fresh, reacting and
         # burnt cells
-        pick = np.sort(np.random.default_rng(2405017130).choice(L ** 3, min(L ** 3, 40000), replace=False))
+        # (~3-4 s per pass of the oracle on 16 host cores for the H2 / DRM19 fields; the 53-species ones are slower)
+        nsamp = 120000 if cfg in ("C3", "C4") else 40000
+        pick = np.sort(np.random.default_rng(2405017130).choice(L ** 3, min(L ** 3, nsamp), replace=False))
         y, rho, F, _ = flame_field(mech, L, cells=pick, dt=dt)
         om, G = O.Model.mechanism(mech), CONFIGS_G[cfg]
         idx = np.arange(len(pick))

@@ -82,10 +82,18 @@ __global__ void __launch_bounds__(32 * JL_WARPS) split_jac_lanes_kernel(SplitBuf
 }
 
 // K_lu, six cells per block (grid-stride over the setup list in block-uniform trips)
+// K_lu block shape for n > 32: two 192-thread blocks per SM (3 cells each; GLUShared is sized for gl_lu's 6)
+// instead of gl_lu's one 384-thread block: a block waiting at its per-column barriers no longer idles the SM
+// (C5P K_lu 929 -> 846 ms, profiles/r2/history.md)
+template <int NN>
+struct LUR {
+  static constexpr int TC = GLU<NN>::TC, CPB = 192 / TC > 0 ? 192 / TC : 1, T = CPB * TC, BPS = 384 / T > 0 ? 384 / T : 1;
+  static_assert(CPB <= GLU<NN>::CPB, "GLUShared holds GLU<NN>::CPB cells");
+};
 template <class Mech, class GM, int LS>
-__global__ void __launch_bounds__(GLU<Mech::N>::T, GLU<Mech::N>::BPS) split_lu_rows_kernel(SplitBufs b, int it) {
+__global__ void __launch_bounds__(LUR<Mech::N>::T, LUR<Mech::N>::BPS) split_lu_rows_kernel(SplitBufs b, int it) {
   using SP = Split<Mech, GM, LS>;
-  constexpr int N = Mech::N, TC = GLU<N>::TC, CPB = GLU<N>::CPB;
+  constexpr int N = Mech::N, TC = LUR<N>::TC, CPB = LUR<N>::CPB;
   __shared__ GLUShared<N> sh;
   const int cb = threadIdx.x / TC, i = threadIdx.x % TC;
   const long long cnt = b.cnt[3 * (it & 1)];

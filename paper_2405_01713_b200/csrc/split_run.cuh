@@ -165,8 +165,8 @@ struct SplitK {
         }
         if (events) cudaEventRecord(ev[2], ss);
         if constexpr (LS == LS_DENSE && BIG) {
-          // one 384-thread block per SM (setup_grid = 8 per SM), grid-stride over the setup list
-          split_lu_rows_kernel<Mech, GM, LS><<<(unsigned)(gm.setup_grid / 8 * GLU<Mech::N>::BPS), GLU<Mech::N>::T, 0,
+          // two 192-thread blocks per SM (setup_grid = 8 per SM), grid-stride over the setup list
+          split_lu_rows_kernel<Mech, GM, LS><<<(unsigned)(gm.setup_grid / 8 * LUR<Mech::N>::BPS), LUR<Mech::N>::T, 0,
                                                 ss>>>(b, it);
         } else if constexpr (LS == LS_DENSE) {
           split_lu_kernel<Mech, GM, LS><<<glu, blk, 0, ss>>>(b, it);
