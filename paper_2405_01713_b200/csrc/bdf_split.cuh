@@ -1095,23 +1095,10 @@ __device__ __forceinline__ double oct_pick(const double (&a)[R][NN], int ps, int
   return v;
 }
 
-// 1: the pivot row reaches the group through shared memory -- the owner lane publishes all R of its rows from
-// column k on (16-byte stores, double-buffered by column parity) and every lane reads the pivot row at its runtime
-// slot ps with plain loads -- instead of R - 1 selects and 2 shuffles per column of the pivot row
-#ifndef BDFB_SPLIT_LU_SMEM
-#define BDFB_SPLIT_LU_SMEM 0
-#endif
-// the group's publication buffer: 2 parities x R rows x NP (N rounded up to even) doubles; blocks of
-// BDFB_SPLIT_BLOCK threads (OCT lanes per group)
-template <int N>
-struct OctPub {
-  static constexpr int R = (N + OCT - 1) / OCT, NP = (N + 1) & ~1, PER = 2 * R * NP;
-};
-
 // column k of oct_factor (k a compile-time constant so that a[][] stays in registers)
 template <int N, int K>
 __device__ __forceinline__ void oct_column(int gl, double (&a)[(N + OCT - 1) / OCT][N], int (&pos)[(N + OCT - 1) / OCT],
-                                           double (&dinv)[(N + OCT - 1) / OCT], int& info, double* pub) {
+                                           double (&dinv)[(N + OCT - 1) / OCT], int& info) {
   constexpr int R = (N + OCT - 1) / OCT;
   // local candidate: max |a[s][K]| over owned rows with pos >= K, ties -> smaller pos; (pos, row) packed in one
   // int (pos in the high half: positions are distinct, so packed order = position order)
@@ -1141,22 +1128,7 @@ __device__ __forceinline__ void oct_column(int gl, double (&a)[(N + OCT - 1) / O
   if (!(bv > 0.0) && info == 0) info = K + 1;   // exact zero pivot (uniform in the group)
   const int bp = bpr >> 16, br = bpr & 0xffff;
   const int pl = br & (OCT - 1), ps = br / OCT;   // owner lane and slot of the pivot row
-#if BDFB_SPLIT_LU_SMEM
-  constexpr int NP = OctPub<N>::NP;
-  double* pb = pub + (K & 1) * (R * NP);
-  if (gl == pl) {
-#pragma unroll
-    for (int s = 0; s < R; ++s)
-#pragma unroll
-      for (int j = K & ~1; j < N; j += 2)
-        *reinterpret_cast<double2*>(pb + s * NP + j) = make_double2(a[s][j], j + 1 < N ? a[s][j + 1] : 0.0);
-  }
-  __syncwarp();
-  const double* prow = pb + ps * NP;
-  const double pv = prow[K];
-#else
   const double pv = __shfl_sync(0xffffffffu, oct_pick<R>(a, ps, K), pl, OCT);
-#endif
   const double rinv = 1.0 / pv;
 #pragma unroll
   for (int s = 0; s < R; ++s) {
@@ -1181,11 +1153,7 @@ __device__ __forceinline__ void oct_column(int gl, double (&a)[(N + OCT - 1) / O
   }
 #pragma unroll
   for (int j = K + 1; j < N; ++j) {
-#if BDFB_SPLIT_LU_SMEM
-    const double pj = prow[j];
-#else
     const double pj = __shfl_sync(0xffffffffu, oct_pick<R>(a, ps, j), pl, OCT);
-#endif
 #pragma unroll
     for (int s = 0; s < R; ++s)
       if (gl + OCT * s < N) a[s][j] = fma(-m[s], pj, a[s][j]);
@@ -1194,9 +1162,9 @@ __device__ __forceinline__ void oct_column(int gl, double (&a)[(N + OCT - 1) / O
 
 template <int N, int... Ks>
 __device__ __forceinline__ void oct_columns(int gl, double (&a)[(N + OCT - 1) / OCT][N], int (&pos)[(N + OCT - 1) / OCT],
-                                            double (&dinv)[(N + OCT - 1) / OCT], int& info, double* pub,
+                                            double (&dinv)[(N + OCT - 1) / OCT], int& info,
                                             std::integer_sequence<int, Ks...>) {
-  (oct_column<N, Ks>(gl, a, pos, dinv, info, pub), ...);   // left to right
+  (oct_column<N, Ks>(gl, a, pos, dinv, info), ...);   // left to right
 }
 
 // called by all 32 lanes of the warp together (4 groups); returns 0 or k + 1 of the group's first zero pivot
@@ -1211,13 +1179,7 @@ __device__ __forceinline__ int oct_factor(int gl, double (&a)[(N + OCT - 1) / OC
     dinv[s] = 0.0;
   }
   int info = 0;
-#if BDFB_SPLIT_LU_SMEM
-  __shared__ __align__(16) double pubsm[(BDFB_SPLIT_BLOCK / OCT) * OctPub<N>::PER];
-  double* pub = pubsm + (threadIdx.x / OCT) * OctPub<N>::PER;
-#else
-  double* pub = nullptr;
-#endif
-  oct_columns<N>(gl, a, pos, dinv, info, pub, std::make_integer_sequence<int, N>{});
+  oct_columns<N>(gl, a, pos, dinv, info, std::make_integer_sequence<int, N>{});
   return info;
 }
 
