@@ -55,10 +55,18 @@ struct TS {
   signed char qc;                                  // order of the step whose completion is deferred (F_COMPLETE)
 };
 constexpr int TS_STRIDE = (int)((sizeof(TS) + 7) / 8) | 1;   // odd number of doubles
+// chunks (CH elements of every Nordsieck row) of the ATTEMPT pass in flight: measured on C4 K_ctl (same box, two
+// runs each): 1 -> 3151 ms, 2 -> 3295 ms, 4 -> 3709 ms (more rows in flight per lane only add L1/L2 queueing to a
+// kernel whose lanes already stream ~10 KB per trip; profiles/r2/history.md)
 #ifndef BDFB_ATTEMPT_UNROLL
-#define BDFB_ATTEMPT_UNROLL 2
+#define BDFB_ATTEMPT_UNROLL 1
 #endif
-constexpr int kAttemptUnroll = BDFB_ATTEMPT_UNROLL;   // chunks of the ATTEMPT pass in flight
+constexpr int kAttemptUnroll = BDFB_ATTEMPT_UNROLL;
+// components of the error test's PREPARE_NEXT norms per round of loads (11: 2 rounds for n = 22)
+#ifndef BDFB_ERRTEST_UNROLL
+#define BDFB_ERRTEST_UNROLL 11
+#endif
+constexpr int kErrtestUnroll = BDFB_ERRTEST_UNROLL;
 
 #ifndef BDFB_TPC_BLOCK
 #define BDFB_TPC_BLOCK 128
@@ -780,7 +788,7 @@ struct TpcIntegrator {
       double sdn = 0.0, sup = 0.0;
       if (nm1 || np1) {
         const double lq = s.l[q];
-#pragma unroll 11   // 2 rounds of loads in flight (latency-bound)
+#pragma unroll kErrtestUnroll   // rounds of loads in flight
         for (int i = 0; i < N; ++i) {
           const double a = w.acor(i), e = w.ewt(i);
           if (nm1) {
