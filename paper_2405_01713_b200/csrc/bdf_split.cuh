@@ -24,10 +24,11 @@
 //     A finished cell is stored and the slot loads the next cell from the
 //     device work counter, so the pool stays full until the counter runs out
 //     (per-cell adaptive stepping: a stiff cell holds its slot for more trips).
-//   K_jac (thread per listed slot): analytic Jacobian, generated straight-line
-//     code (gen/tpc_<mech>.cuh jac_cm), into the slot's J record.
-//   K_lu (one cell per group of G lanes): M = I - gamma J, LU with partial
-//     pivoting in registers (coop_factor: lane i holds row i), factors stored
+//   K_jac (Jacobian list): the generated analytic Jacobian in two passes --
+//     reactions in warp-uniform parts + an ordered sum (thread per cell and
+//     part), then one column per thread -- into the slot's J record.
+//   K_lu (setup list, one cell per group of 8 lanes, 4 per warp): M = I - gamma J,
+//     LU with partial pivoting in registers (oct_factor), factors stored
 //     column-major in pivoted row order with 1/U_kk and the permutation.
 //   K_ctl (pass B, thread per listed slot): the rest of the trip after the
 //     setup, to the next RHS request.

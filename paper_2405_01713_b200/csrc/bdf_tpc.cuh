@@ -62,6 +62,10 @@ constexpr int TS_STRIDE = (int)((sizeof(TS) + 7) / 8) | 1;   // odd number of do
 #define BDFB_ATTEMPT_UNROLL 1
 #endif
 constexpr int kAttemptUnroll = BDFB_ATTEMPT_UNROLL;
+// elements per ATTEMPT chunk (0: 4 when 4 divides n, else 2); 1 measured on C4 K_ctl: 3155 -> 3106 ms
+#ifndef BDFB_ATTEMPT_CH
+#define BDFB_ATTEMPT_CH 1
+#endif
 // components of the error test's PREPARE_NEXT norms per round of loads (11: 2 rounds for n = 22)
 #ifndef BDFB_ERRTEST_UNROLL
 #define BDFB_ERRTEST_UNROLL 11
@@ -889,7 +893,7 @@ struct TpcIntegrator {
       }
     }
     const double rtol = o.rtol;
-    constexpr int CH = (N % 4 == 0) ? 4 : 2;
+    constexpr int CH = BDFB_ATTEMPT_CH ? BDFB_ATTEMPT_CH : ((N % 4 == 0) ? 4 : 2);   // elements per chunk
     static_assert(N % CH == 0, "chunking");
     // rows to read: the new order, the old zn[q + 1] of a deferred decrease, the rows of a deferred completion
     const int qc = (fl & F_COMPLETE) ? s.qc : 0;
